@@ -1,0 +1,250 @@
+"""ctypes wrapper of the CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module.  It imports nothing from
+the CUDA package (paper_2311_16728_b200) and the CUDA package never imports it.
+
+Argument marshalling only; every number is computed in oracle.c (see its header for the
+paper passages each function follows).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+FP64, RECIPE = 0, 1
+_MODES = {"fp64": FP64, "recipe": RECIPE, FP64: FP64, RECIPE: RECIPE}
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (IEEE fp32 recipe needs -ffp-contract=off and no fast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        cmd = ["gcc", "-O2", "-std=gnu11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+               "-fPIC", "-shared", "-o", LIB + ".tmp", SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            _lib = C.CDLL(LIB)
+            _lib.orc_bin.restype = C.c_int64
+            _lib.orc_get_threads.restype = C.c_int
+    return _lib
+
+
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(int(n))
+
+
+def threads() -> int:
+    return int(lib().orc_get_threads())
+
+
+class OrcCamera(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("znear", C.c_float), ("lim_x", C.c_float), ("lim_y", C.c_float)]
+
+
+def _cams(cams):
+    if not isinstance(cams, (list, tuple)):
+        cams = [cams]
+    arr = (OrcCamera * len(cams))()
+    for k, c in enumerate(cams):
+        arr[k].R[:] = [float(v) for v in np.asarray(c.R, np.float32).reshape(9)]
+        arr[k].t[:] = [float(v) for v in np.asarray(c.t, np.float32).reshape(3)]
+        arr[k].fx, arr[k].fy, arr[k].cx, arr[k].cy = c.fx, c.fy, c.cx, c.cy
+        arr[k].width, arr[k].height = int(c.width), int(c.height)
+        arr[k].znear, arr[k].lim_x, arr[k].lim_y = c.znear, c.lim_x, c.lim_y
+    return arr, len(cams)
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _scene_args(scene):
+    arrs = [np.ascontiguousarray(scene.means, np.float32), np.ascontiguousarray(scene.quats, np.float32),
+            np.ascontiguousarray(scene.log_scales, np.float32),
+            np.ascontiguousarray(scene.opacity_logits, np.float32), np.ascontiguousarray(scene.sh, np.float32)]
+    D = int(round(np.sqrt(scene.sh.shape[1]))) - 1
+    return arrs, [C.c_int64(scene.means.shape[0]), C.c_int(D)] + [_p(a) for a in arrs]
+
+
+def project(scene, cam, mode="recipe") -> dict:
+    arrs, sargs = _scene_args(scene)
+    n = scene.means.shape[0]
+    out = dict(radius=np.zeros(n, np.int32), rect=np.zeros((n, 4), np.int32), depth=np.zeros(n),
+               mean2d=np.zeros((n, 2)), conic=np.zeros((n, 3)), rgb=np.zeros((n, 3)), sigma=np.zeros(n),
+               depth_bits=np.zeros(n, np.uint32), mean2d_f=np.zeros((n, 2), np.float32),
+               conic_f=np.zeros((n, 3), np.float32))
+    ca, _ = _cams(cam)
+    lib().orc_project(C.c_int(_MODES[mode]), *sargs, ca,
+                      *[_p(out[k]) for k in ("radius", "rect", "depth", "mean2d", "conic", "rgb", "sigma",
+                                             "depth_bits", "mean2d_f", "conic_f")])
+    return out
+
+
+def bin_pairs(scene, cams):
+    """Reference tile binning: sorted keys (u64), values (u32), ranges [V*tiles][2], tiles_touched [V][n]."""
+    arrs, sargs = _scene_args(scene)
+    ca, V = _cams(cams)
+    n = scene.means.shape[0]
+    tt = np.zeros((V, n), np.int32)
+    P = lib().orc_bin(*sargs, C.c_int(V), ca, None, None, None, _p(tt))
+    tiles = ((cams[0].width + 15) // 16) * ((cams[0].height + 15) // 16) if isinstance(cams, (list, tuple)) \
+        else ((cams.width + 15) // 16) * ((cams.height + 15) // 16)
+    keys = np.zeros(max(P, 1), np.uint64)
+    vals = np.zeros(max(P, 1), np.uint32)
+    ranges = np.zeros((V * tiles, 2), np.uint32)
+    lib().orc_bin(*sargs, C.c_int(V), ca, _p(keys), _p(vals), _p(ranges), _p(tt))
+    return keys[:P], vals[:P], ranges, tt
+
+
+def all_pixels(V, H, W) -> np.ndarray:
+    v, y, x = np.meshgrid(np.arange(V), np.arange(H), np.arange(W), indexing="ij")
+    return np.ascontiguousarray(np.stack([v.ravel(), y.ravel(), x.ravel()], 1).astype(np.int32))
+
+
+def render(scene, cams, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=None) -> dict:
+    """Per-pixel brute-force Eq. 3.  pixels: int32 [npix, 3] (view, y, x) or None = every pixel,
+    in which case outputs are reshaped to rgb [V,3,H,W], T/ncomp/last/flag [V,H,W]."""
+    arrs, sargs = _scene_args(scene)
+    ca, V = _cams(cams)
+    cam0 = cams[0] if isinstance(cams, (list, tuple)) else cams
+    full = pixels is None
+    pix = all_pixels(V, cam0.height, cam0.width) if full else np.ascontiguousarray(pixels, np.int32)
+    npix = pix.shape[0]
+    rgb = np.zeros((npix, 3))
+    T = np.zeros(npix)
+    nc = np.zeros(npix, np.int32)
+    last = np.zeros(npix, np.int64)
+    flag = np.zeros(npix, np.int32)
+    bga = np.asarray(bg, np.float64)
+    lib().orc_render(C.c_int(_MODES[mode]), *sargs, C.c_int(V), ca, _p(bga), C.c_int64(npix), _p(pix),
+                     _p(rgb), _p(T), _p(nc), _p(last), _p(flag))
+    out = dict(rgb=rgb, T=T, ncomp=nc, last=last, flag=flag, pixels=pix)
+    if full:
+        H, W = cam0.height, cam0.width
+        out.update(rgb=rgb.reshape(V, H, W, 3).transpose(0, 3, 1, 2).copy(), T=T.reshape(V, H, W),
+                   ncomp=nc.reshape(V, H, W), last=last.reshape(V, H, W), flag=flag.reshape(V, H, W))
+    return out
+
+
+def backward(scene, cams, dL_drgb, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=None) -> dict:
+    """Gradients of sum_v <dL/dI_v, I_v>.  dL_drgb: [V,3,H,W] (pixels None) or [npix,3]."""
+    arrs, sargs = _scene_args(scene)
+    ca, V = _cams(cams)
+    cam0 = cams[0] if isinstance(cams, (list, tuple)) else cams
+    if pixels is None:
+        pix = all_pixels(V, cam0.height, cam0.width)
+        g = np.ascontiguousarray(np.asarray(dL_drgb, np.float64).transpose(0, 2, 3, 1).reshape(-1, 3))
+    else:
+        pix = np.ascontiguousarray(pixels, np.int32)
+        g = np.ascontiguousarray(np.asarray(dL_drgb, np.float64).reshape(-1, 3))
+    n = scene.means.shape[0]
+    K = scene.sh.shape[1]
+    out = dict(means=np.zeros((n, 3)), quats=np.zeros((n, 4)), log_scales=np.zeros((n, 3)),
+               opacity_logits=np.zeros(n), sh=np.zeros((n, K, 3)), grad2d_norm=np.zeros(n),
+               flagged=np.zeros(n, np.int32))
+    bga = np.asarray(bg, np.float64)
+    lib().orc_backward(C.c_int(_MODES[mode]), *sargs, C.c_int(V), ca, _p(bga), C.c_int64(pix.shape[0]), _p(pix),
+                       _p(g), *[_p(out[k]) for k in ("means", "quats", "log_scales", "opacity_logits", "sh",
+                                                      "grad2d_norm", "flagged")])
+    return out
+
+
+def loss(render_img, gt, lam=0.2, grad=True, ssim_map=False):
+    """Eq. 4 for one view; images [3,H,W].  Returns (loss, mean_ssim, dL/drender or None)
+    (+ the per-pixel SSIM map if ssim_map)."""
+    r = np.ascontiguousarray(render_img, np.float64)
+    g = np.ascontiguousarray(gt, np.float64)
+    if r.shape != g.shape or r.ndim != 3 or r.shape[0] != 3:
+        raise ValueError("DimensionMismatch")
+    H, W = r.shape[1:]
+    out_l, out_s = C.c_double(), C.c_double()
+    d = np.zeros_like(r) if grad else None
+    smap = np.zeros_like(r) if ssim_map else None
+    lib().orc_loss(_p(r), _p(g), C.c_int(H), C.c_int(W), C.c_double(lam), C.byref(out_l), C.byref(out_s), _p(d),
+                   _p(smap))
+    if ssim_map:
+        return out_l.value, out_s.value, d, smap
+    return out_l.value, out_s.value, d
+
+
+def pyramid(img, n_levels: int) -> list:
+    """Levels 0..n of the Gaussian pyramid of a [C,H,W] image (level 0 = input)."""
+    x = np.ascontiguousarray(img, np.float64)
+    Cc, H, W = x.shape
+    if n_levels < 0 or (n_levels > 0 and min(H, W) <= 2 ** n_levels):
+        raise ValueError("TooManyLevels")
+    levels = [x]
+    for _ in range(n_levels):
+        Cc, H, W = levels[-1].shape
+        out = np.zeros((Cc, (H + 1) // 2, (W + 1) // 2))
+        lib().orc_pyramid_level(_p(levels[-1]), C.c_int(Cc), C.c_int(H), C.c_int(W), _p(out))
+        levels.append(out)
+    return levels
+
+
+def adam(p, g, m, v, lr, beta1=0.9, beta2=0.999, eps=1e-15, step=1, sgd_mode=False):
+    """In-place optimiser step on fp64 copies; returns (p, m, v)."""
+    p = np.ascontiguousarray(p, np.float64).copy()
+    g = np.ascontiguousarray(g, np.float64)
+    m = np.ascontiguousarray(m, np.float64).copy()
+    v = np.ascontiguousarray(v, np.float64).copy()
+    lib().orc_adam(C.c_int64(p.size), _p(p), _p(g), _p(m), _p(v), C.c_double(lr), C.c_double(beta1),
+                   C.c_double(beta2), C.c_double(eps), C.c_int64(step), C.c_int(int(sgd_mode)))
+    return p, m, v
+
+
+def debug_cov(mean, quat, log_scale, cam):
+    """(Sigma3 [3,3], Sigma2 (a, b, c) incl. floor) from the fp64 projection, or None if culled."""
+    S3 = np.zeros(9)
+    S2 = np.zeros(3)
+    ca, _ = _cams(cam)
+    ok = lib().orc_debug_cov(_p(np.asarray(mean, np.float32)), _p(np.asarray(quat, np.float32)),
+                             _p(np.asarray(log_scale, np.float32)), ca, _p(S3), _p(S2))
+    return (S3.reshape(3, 3), S2) if ok else None
+
+
+def sh_basis(D, dirs):
+    d = np.ascontiguousarray(dirs, np.float64).reshape(-1, 3)
+    Y = np.zeros((d.shape[0], 16))
+    dY = np.zeros((d.shape[0], 16, 3))
+    lib().orc_sh_basis(C.c_int(D), C.c_int64(d.shape[0]), _p(d), _p(Y), _p(dY))
+    return Y, dY
+
+
+def exp_scale_f32(s):
+    s = np.ascontiguousarray(s, np.float32)
+    out = np.zeros_like(s)
+    lib().orc_exp_scale_f32(C.c_int64(s.size), _p(s), _p(out))
+    return out
+
+
+def total_loss(scene, cams, gts, lam=0.2, mode="fp64", bg=(0.0, 0.0, 0.0)):
+    """sum_v L(render_v, gt_v): the iteration objective."""
+    r = render(scene, cams, mode=mode, bg=bg)
+    return sum(loss(r["rgb"][v], gts[v], lam, grad=False)[0] for v in range(r["rgb"].shape[0]))
+
+
+def total_grad(scene, cams, gts, lam=0.2, mode="fp64", bg=(0.0, 0.0, 0.0)):
+    """Analytic gradient of total_loss: loss gradient per view fed to the backward."""
+    r = render(scene, cams, mode=mode, bg=bg)
+    dL = np.stack([loss(r["rgb"][v], gts[v], lam)[2] for v in range(r["rgb"].shape[0])])
+    return backward(scene, cams, dL, mode=mode, bg=bg), r, dL
