@@ -1,0 +1,192 @@
+/*
+ * gs.h -- C ABI of libgs.so, the B200 (sm_100a) hot path of Photo-SLAM's photorealistic
+ * mapping (arXiv 2311.16728): render the hyper-primitive map with a tile-based Gaussian
+ * splatting rasteriser (Eq. 3), evaluate the photometric loss (Eq. 4,
+ * PAPER.md:181-184), back-propagate it to the primitive parameters, build the
+ * Gaussian pyramid (Eq. 5) and apply the optimiser step.
+ * Citations are /root/reference lines; readings R1..R26 are listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *  - Pointers are DEVICE pointers unless marked (host).  The caller allocates every buffer
+ *    (including the workspace sized by gs_workspace_size); the library never allocates,
+ *    frees or synchronises, except gs_query_status which synchronises `stream`.
+ *  - All work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream) and the
+ *    call returns immediately; CUDA-graph capture of any call sequence is allowed.
+ *  - Argument and shape errors are returned synchronously (GS_ERR_INVALID_ARG /
+ *    GS_ERR_SHAPE) and nothing is enqueued.  A failed kernel launch returns GS_ERR_CUDA.
+ *    Pair-capacity overflow is detected on the device: it sets a flag that
+ *    gs_query_status reports as GS_ERR_CAPACITY (that call's outputs are then invalid).
+ *  - No exception or C++ type crosses the ABI.  Calls are re-entrant given distinct
+ *    workspaces; concurrent calls on one workspace are a caller error.
+ *  - Precision: fp32 everywhere (R23); decision quantities follow the fp32 recipe of
+ *    DESIGN.md so that binning and sort order are bit-exact to the CPU oracle.
+ */
+#ifndef GS_H
+#define GS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *gs_stream_t; /* identical to cudaStream_t */
+
+typedef enum {
+    GS_OK = 0,
+    GS_ERR_INVALID_ARG = 1,  /* NULL pointer, non-positive size, bad degree/level count      */
+    GS_ERR_SHAPE = 2,        /* DimensionMismatch, TooManyLevels, */
+                             /* views of different sizes, workspace too small                  */
+    GS_ERR_CAPACITY = 3,     /* (from gs_query_status) more tile pairs than the workspace holds */
+    GS_ERR_STALE_STATE = 4,  /* backward without a matching forward             */
+    GS_ERR_CUDA = 5,         /* kernel launch / CUDA runtime failure                           */
+    GS_ERR_NOT_SUPPORTED = 6 /* e.g. more than GS_MAX_VIEWS views in one call                 */
+} gs_status;
+
+#define GS_TILE 16      /* 16x16-pixel tiles */
+#define GS_MAX_VIEWS 64 /* views per call (keyframe batch on one GPU) */
+
+/* Pinhole camera of one keyframe view.  World->camera p_c = R P + t with R row-major
+   (SPEC.md:38); pixel (x, y) is centred at integer (x, y) (R12); at pyramid level l the
+   caller passes fx, fy, cx, cy scaled by 2^-l and the ceil-halved size (R12, R19).
+   znear: cull z_c <= znear (R14).  lim_x, lim_y: |x_c/z_c|, |y_c/z_c| clamp used inside the
+   EWA Jacobian (R15); +INF disables the clamp. */
+typedef struct {
+    float R[9];
+    float t[3];
+    float fx, fy, cx, cy;
+    int32_t width, height;
+    float znear, lim_x, lim_y;
+} gs_camera;
+
+/* Gaussian parameters (position P, rotation r, scaling s, density sigma, SH),
+   fp32 structure-of-arrays: row r occupies data[r*ld .. r*ld+n).  K = gs_param_rows(D):
+     rows 0..2   P (x, y, z)
+     rows 3..6   raw quaternion (w, x, y, z), normalised inside (R5)
+     rows 7..9   log scales (R4)
+     row  10     opacity logit (R3)
+     rows 11..   SH, coefficient-major: row 11 + 3*l + c, l = 0..(D+1)^2-1, c = R,G,B (R2)
+   ld >= n and ld % 4 == 0 (gs_param_ld gives the recommended value).  Gradients and the
+   Adam moments use the identical layout. */
+typedef struct {
+    float *data;
+    int64_t n;
+    int64_t ld;
+    int32_t sh_degree; /* 0..3 */
+} gs_params;
+
+/* Optimiser hyper-parameters (PAPER.md:568 fixed learning rate; R20).  lr per class:
+   [0] P, [1] quaternion, [2] log scale, [3] opacity logit, [4] SH DC (l = 0), [5] SH rest. */
+typedef struct {
+    float lr[6];
+    float beta1, beta2, eps;
+    int32_t sgd_mode; /* 1: p -= lr * g (no moments) */
+} gs_adam_hparams;
+
+/* Rows K of the parameter layout: 11 + 3 (D+1)^2 (14 at D = 0, 59 at D = 3). */
+int32_t gs_param_rows(int32_t sh_degree);
+/* Recommended leading dimension: n rounded up to a multiple of 64 floats (256-byte rows). */
+int64_t gs_param_ld(int64_t n);
+
+/* Bytes of the render workspace for n Gaussians, n_views views of width x height and a
+   capacity of pair_capacity (Gaussian, tile) pairs summed over the views (rounded up to a
+   multiple of 4096).  *bytes is host memory. */
+gs_status gs_workspace_size(int64_t n, int32_t n_views, int32_t width, int32_t height,
+                            int64_t pair_capacity, size_t *bytes);
+
+/* A1 + A2: per (view, Gaussian) projection, culling, EWA 2D covariance + 0.3 px^2 floor,
+   conic, radius r = ceil(3 sqrt(lambda_max)), tile rect, depth, SH colour and sigmoid
+   opacity; then the exclusive scan of tiles touched.
+   cams: host array [n_views]; all views must share width and height. */
+gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                        size_t ws_bytes, gs_stream_t stream);
+
+/* A3-A6: key duplication (key = (view*tiles + tile) << 32 | float_bits(depth), value =
+   Gaussian index), stable LSD radix sort, tile ranges and per-tile front-to-back alpha
+   compositing of Eq. 3: alpha = min(0.99, sigma e^power),
+   power cut at Mahalanobis^2 > 9 (R9), skip alpha < 1/255, stop when T (1 - alpha) < 1e-4
+   (R7, R8).  Requires gs_preprocess on the same params/cams/workspace first.
+   bg: host float[3] background (R16).  out_rgb [n_views][3][H][W], out_T [n_views][H][W]
+   (final transmittance; may be NULL). */
+gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                            size_t ws_bytes, const float bg[3], float *out_rgb, float *out_T,
+                            gs_stream_t stream);
+
+/* Workspace bytes for gs_photometric_loss on V images of H x W. */
+gs_status gs_loss_workspace_size(int32_t V, int32_t H, int32_t W, size_t *bytes);
+
+/* A7: Eq. 4 per view, L_v = (1 - lambda) mean|I_r - I_gt| + lambda (1 - mean SSIM) with an
+   11x11 Gaussian window (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, zero-padded 'same' (R17), and
+   its exact gradient (L1 subgradient 0 at 0).  render, gt, dL_drender:
+   [V][3][H][W]; loss: device float[V]. */
+gs_status gs_photometric_loss(const float *render, const float *gt, int32_t V, int32_t H, int32_t W,
+                              float lambda, float *loss, float *dL_drender, void *ws, size_t ws_bytes,
+                              gs_stream_t stream);
+
+/* A8 + A9: reverse-mode gradient of sum_v <dL_drgb_v, I_v> through the compositing of the
+   last gs_render_forward on this workspace and through the projection to P, quaternion,
+   log scale, opacity logit and SH, summed over views (R22).
+   grads (param layout, += accumulate), grad2d_norm_accum (float[n], += sum over views of
+   ||dL/dmean2d|| in pixels, R24; may be NULL).  Returns GS_ERR_STALE_STATE if the last
+   forward on ws used other params, n, views or cameras. */
+gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                             size_t ws_bytes, const float bg[3], const float *dL_drgb, float *grads,
+                             float *grad2d_norm_accum, gs_stream_t stream);
+
+/* A0: Gaussian pyramid (Eq. 5): level l+1 = even rows/cols of the level-l
+   image blurred by [1,4,6,4,1]/16 horizontally then vertically with a reflect-101 border
+   (R18); sizes ceil-halved.  img [n_images][C][H][W]; out = levels 1..n_levels concatenated,
+   level-major, each [n_images][C][H_l][W_l].  GS_ERR_SHAPE if min(H, W) <= 2^n_levels
+   (TooManyLevels). */
+gs_status gs_pyramid(const float *img, int32_t n_images, int32_t C, int32_t H, int32_t W, int32_t n_levels,
+                     float *out, gs_stream_t stream);
+
+/* A11: fused optimiser step over Gaussians [g_begin, g_end) of every row: bias-corrected
+   Adam with per-class lr (R20) or SGD, in place on params, m, v; step is 1-based; if
+   zero_grads, grads of the range are zeroed after use. */
+gs_status gs_adam_step(gs_params *params, float *grads, float *m, float *v, const gs_adam_hparams *hp,
+                       int64_t step, int64_t g_begin, int64_t g_end, int32_t zero_grads, gs_stream_t stream);
+
+/* Synchronises stream, then reads the workspace status: *flags (host) bit 0 = pair capacity
+   overflow; *pairs (host, may be NULL) = pair count of the last gs_preprocess.  Returns
+   GS_ERR_CAPACITY if bit 0 is set. */
+gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs);
+
+const char *gs_status_str(gs_status s);
+
+/* ---- test / benchmark entry points ------------------------------------------------------ */
+/* Stable LSD radix sort of n (key, value) pairs on key bits [0, key_bits) (8-bit digits,
+   one decoupled-look-back pass per digit).  Sorted in place in keys/vals; keys_alt/vals_alt
+   are ping-pong buffers of n entries; temp of gs_sort_temp_size bytes. */
+gs_status gs_sort_temp_size(int64_t n, int32_t key_bits, size_t *bytes);
+gs_status gs_debug_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt, uint32_t *vals_alt, int64_t n,
+                              int32_t key_bits, void *temp, size_t temp_bytes, gs_stream_t stream);
+
+/* Device pointers to the per-(view, Gaussian) and binning buffers of a workspace, for
+   bit-exact comparison with the oracle.  Valid after gs_preprocess / gs_render_forward. */
+typedef struct {
+    const float *rec0;            /* [n_views*n][4] (u, v, A, B): mean2d, conic A, B */
+    const float *rec1;            /* [n_views*n][4] (C, sigma, r, g)                 */
+    const float *rec2;            /* [n_views*n] b                                   */
+    const float *depth;           /* [n_views*n] view-space z                        */
+    const int32_t *radius;        /* [n_views*n] 0 = culled                          */
+    const int32_t *rect;          /* [n_views*n][4] tile x0, y0, x1, y1 (exclusive)  */
+    const uint32_t *tiles_touched; /* [n_views*n]                                    */
+    const uint32_t *offsets;       /* [n_views*n] exclusive scan of tiles_touched     */
+    const uint64_t *keys;          /* [capacity] sorted keys (after render_forward)   */
+    const uint32_t *vals;          /* [capacity] sorted values                        */
+    const uint32_t *ranges;        /* [n_views*tiles][2] [start, end) per tile        */
+    const uint32_t *n_contrib;     /* [n_views][H][W] list position of the last composited */
+    int64_t capacity;
+} gs_ws_view;
+gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t n_views, int32_t width,
+                                  int32_t height, gs_ws_view *out);
+/* (float)exp((double)s) exactly as the preprocess kernel evaluates it, for the exhaustive
+   check against the oracle (DESIGN.md fp32 recipe). */
+gs_status gs_debug_exp_scale(const float *s, float *out, int64_t n, gs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_H */

@@ -1,0 +1,325 @@
+// api.cu -- the extern "C" boundary of libgs.so (declared and documented in include/gs.h).
+// Argument validation, workspace layout, the forward/backward state token and kernel
+// sequencing live here; all arithmetic of the path runs in the kernels of this directory.
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "gs_internal.cuh"
+
+namespace gsk {
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
+    Layout L;
+    std::memset(&L, 0, sizeof(L));
+    L.n = n;
+    L.V = V;
+    L.W = W;
+    L.H = H;
+    L.M = (int64_t)V * n;
+    L.TX = (W + TILE - 1) / TILE;
+    L.TY = (H + TILE - 1) / TILE;
+    L.tiles = L.TX * L.TY;
+    L.cap = ((cap + SORT_TILE - 1) / SORT_TILE) * SORT_TILE;
+    L.scan_blocks = (L.M + SCAN_TILE - 1) / SCAN_TILE;
+    L.sort_blocks = L.cap / SORT_TILE;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o += al(bytes);
+        return r;
+    };
+    const size_t M = (size_t)L.M;
+    L.hdr = take(sizeof(WsHeader));
+    L.rec0 = take(M * sizeof(float4));
+    L.rec1 = take(M * sizeof(float4));
+    L.rec2 = take(M * sizeof(float));
+    L.depth = take(M * sizeof(float));
+    L.radius = take(M * sizeof(int32_t));
+    L.rect = take(M * sizeof(int4));
+    L.tiles_touched = take(M * sizeof(uint32_t));
+    L.offsets = take(M * sizeof(uint32_t));
+    L.grad2d = take(M * 3 * sizeof(float4));
+    L.scan_flags = take((size_t)std::max<int64_t>(L.scan_blocks, 1) * sizeof(uint64_t));
+    L.ranges = take((size_t)V * L.tiles * sizeof(uint2));
+    L.ncontrib = take((size_t)V * W * H * sizeof(uint32_t));
+    L.Tfinal = take((size_t)V * W * H * sizeof(float));
+    L.keys0 = take((size_t)L.cap * sizeof(uint64_t));
+    L.keys1 = take((size_t)L.cap * sizeof(uint64_t));
+    L.vals0 = take((size_t)L.cap * sizeof(uint32_t));
+    L.vals1 = take((size_t)L.cap * sizeof(uint32_t));
+    L.sort_look = take((size_t)SORT_MAX_PASSES * std::max<int64_t>(L.sort_blocks, 1) * SORT_RADIX * sizeof(uint32_t));
+    L.total = o;
+    return L;
+}
+
+bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out) {
+    Layout L0 = make_layout(n, V, W, H, 0);
+    if (L0.total > ws_bytes) return false;
+    // bytes per SORT_TILE pairs: 2 x (8 + 4) per pair + look-back words
+    size_t per_tile = (size_t)SORT_TILE * 24 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
+    int64_t tiles = (int64_t)((ws_bytes - L0.total) / per_tile) + 1;
+    for (; tiles >= 0; tiles--) {
+        Layout L = make_layout(n, V, W, H, tiles * SORT_TILE);
+        if (L.total <= ws_bytes) {
+            *out = L;
+            return true;
+        }
+    }
+    return false;
+}
+
+// ---- forward/backward state token (SPEC.md:355-359 StaleRenderState) ----
+struct Token {
+    const float *data;
+    int64_t n, ld;
+    int32_t D, V;
+    uint64_t cam_hash;
+    int stage;  // 1 = preprocessed, 2 = rendered
+};
+static std::mutex g_mu;
+static std::unordered_map<const void *, Token> g_tokens;
+
+static uint64_t hash_cams(const gs_camera *c, int V) {
+    uint64_t h = 1469598103934665603ull;
+    const unsigned char *p = reinterpret_cast<const unsigned char *>(c);
+    for (size_t k = 0; k < sizeof(gs_camera) * (size_t)V; k++) h = (h ^ p[k]) * 1099511628211ull;
+    return h;
+}
+static Token make_token(const gs_params *p, const gs_camera *c, int V, int stage) {
+    return Token{p->data, p->n, p->ld, p->sh_degree, V, hash_cams(c, V), stage};
+}
+static bool same(const Token &a, const Token &b) {
+    return a.data == b.data && a.n == b.n && a.ld == b.ld && a.D == b.D && a.V == b.V && a.cam_hash == b.cam_hash;
+}
+
+static gs_status check_params(const gs_params *p) {
+    if (!p || p->n < 0 || (p->n > 0 && !p->data)) return GS_ERR_INVALID_ARG;
+    if (p->sh_degree < 0 || p->sh_degree > 3) return GS_ERR_INVALID_ARG;
+    if (p->ld < p->n || p->ld % 4 != 0) return GS_ERR_SHAPE;
+    if (p->n >= (int64_t)1 << 31) return GS_ERR_NOT_SUPPORTED;
+    return GS_OK;
+}
+
+static gs_status check_views(const gs_camera *cams, int V, CamBatch *cb) {
+    if (!cams || V <= 0) return GS_ERR_INVALID_ARG;
+    if (V > GS_MAX_VIEWS) return GS_ERR_NOT_SUPPORTED;
+    for (int v = 0; v < V; v++) {
+        if (cams[v].width <= 0 || cams[v].height <= 0) return GS_ERR_INVALID_ARG;
+        if (cams[v].width != cams[0].width || cams[v].height != cams[0].height) return GS_ERR_SHAPE;
+        cb->c[v] = cams[v];
+    }
+    return GS_OK;
+}
+
+static gs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GS_OK : GS_ERR_CUDA; }
+
+}  // namespace gsk
+
+using namespace gsk;
+
+extern "C" {
+
+int32_t gs_param_rows(int32_t sh_degree) { return 11 + 3 * (sh_degree + 1) * (sh_degree + 1); }
+
+int64_t gs_param_ld(int64_t n) { return ((n + 63) / 64) * 64; }
+
+gs_status gs_workspace_size(int64_t n, int32_t n_views, int32_t width, int32_t height, int64_t pair_capacity,
+                            size_t *bytes) {
+    if (!bytes || n < 0 || n_views <= 0 || width <= 0 || height <= 0 || pair_capacity < 0) return GS_ERR_INVALID_ARG;
+    if (n_views > GS_MAX_VIEWS) return GS_ERR_NOT_SUPPORTED;
+    if (pair_capacity >= ((int64_t)1 << 30)) return GS_ERR_NOT_SUPPORTED;
+    *bytes = make_layout(n, n_views, width, height, pair_capacity).total;
+    return GS_OK;
+}
+
+gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws, size_t ws_bytes,
+                        gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    static thread_local CamBatch cb;
+    if ((st = check_views(cams, n_views, &cb))) return st;
+    if (!ws) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    cudaStream_t s = (cudaStream_t)stream;
+    WsHeader *hdr = at<WsHeader>(ws, L.hdr);
+    cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter
+    cudaMemsetAsync(at<char>(ws, L.scan_flags), 0, (size_t)std::max<int64_t>(L.scan_blocks, 1) * 8, s);
+    cudaError_t e = launch_preprocess(*params, cb, n_views, L, ws, s);
+    if (e == cudaSuccess) e = launch_scan(L, ws, s);
+    if (e != cudaSuccess) return GS_ERR_CUDA;
+    std::lock_guard<std::mutex> g(g_mu);
+    g_tokens[ws] = make_token(params, cams, n_views, 1);
+    return GS_OK;
+}
+
+gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                            size_t ws_bytes, const float bg[3], float *out_rgb, float *out_T, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    static thread_local CamBatch cb;
+    if ((st = check_views(cams, n_views, &cb))) return st;
+    if (!ws || !bg || !out_rgb) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        auto it = g_tokens.find(ws);
+        if (it == g_tokens.end() || !same(it->second, make_token(params, cams, n_views, 1)))
+            return GS_ERR_STALE_STATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    WsHeader *hdr = at<WsHeader>(ws, L.hdr);
+    int key_bits = 32 + std::max(1, hi_bits_for((int64_t)n_views * L.tiles));
+    cudaError_t e = launch_duplicate(L, ws, s);
+    if (e == cudaSuccess)
+        e = launch_sort(at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint64_t>(ws, L.keys1),
+                        at<uint32_t>(ws, L.vals1), &hdr->P, L.cap, key_bits, hdr, at<uint32_t>(ws, L.sort_look),
+                        L.sort_blocks, s);
+    if (e == cudaSuccess) e = launch_ranges(L, ws, s);
+    if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s);
+    if (e != cudaSuccess) return GS_ERR_CUDA;
+    std::lock_guard<std::mutex> g(g_mu);
+    g_tokens[ws] = make_token(params, cams, n_views, 2);
+    return GS_OK;
+}
+
+gs_status gs_loss_workspace_size(int32_t V, int32_t H, int32_t W, size_t *bytes) {
+    if (!bytes || V <= 0 || H <= 0 || W <= 0) return GS_ERR_INVALID_ARG;
+    *bytes = loss_ws_bytes(V, H, W);
+    return GS_OK;
+}
+
+gs_status gs_photometric_loss(const float *render, const float *gt, int32_t V, int32_t H, int32_t W, float lambda,
+                              float *loss, float *dL_drender, void *ws, size_t ws_bytes, gs_stream_t stream) {
+    if (!render || !gt || !loss || !ws || V <= 0 || H <= 0 || W <= 0) return GS_ERR_INVALID_ARG;
+    if (!(lambda >= 0.f && lambda <= 1.f)) return GS_ERR_INVALID_ARG;
+    if (ws_bytes < loss_ws_bytes(V, H, W)) return GS_ERR_SHAPE;
+    return cuda_status(launch_loss(render, gt, V, H, W, lambda, loss, dL_drender, ws, (cudaStream_t)stream));
+}
+
+gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                             size_t ws_bytes, const float bg[3], const float *dL_drgb, float *grads,
+                             float *grad2d_norm_accum, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    static thread_local CamBatch cb;
+    if ((st = check_views(cams, n_views, &cb))) return st;
+    if (!ws || !bg || !dL_drgb || !grads) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        auto it = g_tokens.find(ws);
+        if (it == g_tokens.end() || it->second.stage != 2 || !same(it->second, make_token(params, cams, n_views, 2)))
+            return GS_ERR_STALE_STATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = launch_raster_bwd(L, ws, bg, dL_drgb, s);
+    if (e == cudaSuccess) e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grads, grad2d_norm_accum, s);
+    return cuda_status(e);
+}
+
+gs_status gs_pyramid(const float *img, int32_t n_images, int32_t C, int32_t H, int32_t W, int32_t n_levels, float *out,
+                     gs_stream_t stream) {
+    if (!img || n_images <= 0 || C <= 0 || H <= 0 || W <= 0 || n_levels < 0) return GS_ERR_INVALID_ARG;
+    if (n_levels > 0 && (int64_t)std::min(H, W) <= ((int64_t)1 << n_levels)) return GS_ERR_SHAPE;
+    if (n_levels == 0) return GS_OK;
+    if (!out) return GS_ERR_INVALID_ARG;
+    return cuda_status(launch_pyramid(img, n_images, C, H, W, n_levels, out, (cudaStream_t)stream));
+}
+
+gs_status gs_adam_step(gs_params *params, float *grads, float *m, float *v, const gs_adam_hparams *hp, int64_t step,
+                       int64_t g_begin, int64_t g_end, int32_t zero_grads, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    if (!grads || !hp || step < 1 || g_begin < 0 || g_end > params->n || g_begin > g_end) return GS_ERR_INVALID_ARG;
+    if (!hp->sgd_mode && (!m || !v)) return GS_ERR_INVALID_ARG;
+    if (g_begin == g_end) return GS_OK;
+    return cuda_status(launch_adam(*params, grads, m, v, *hp, step, g_begin, g_end, zero_grads, (cudaStream_t)stream));
+}
+
+gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs) {
+    if (!ws || !flags || ws_bytes < sizeof(WsHeader)) return GS_ERR_INVALID_ARG;
+    WsHeader h;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return GS_ERR_CUDA;
+    if (cudaMemcpy(&h, ws, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost) != cudaSuccess) return GS_ERR_CUDA;
+    *flags = (int32_t)h.flags;
+    if (pairs) *pairs = h.P;
+    return (h.flags & 1u) ? GS_ERR_CAPACITY : GS_OK;
+}
+
+const char *gs_status_str(gs_status s) {
+    switch (s) {
+        case GS_OK: return "ok";
+        case GS_ERR_INVALID_ARG: return "invalid argument";
+        case GS_ERR_SHAPE: return "shape mismatch / too many levels / workspace too small";
+        case GS_ERR_CAPACITY: return "tile-pair capacity exceeded";
+        case GS_ERR_STALE_STATE: return "stale render state (backward without matching forward)";
+        case GS_ERR_CUDA: return "CUDA error";
+        case GS_ERR_NOT_SUPPORTED: return "not supported";
+    }
+    return "unknown status";
+}
+
+gs_status gs_sort_temp_size(int64_t n, int32_t key_bits, size_t *bytes) {
+    if (!bytes || n < 0 || key_bits <= 0 || key_bits > 64) return GS_ERR_INVALID_ARG;
+    if (n >= ((int64_t)1 << 30)) return GS_ERR_NOT_SUPPORTED;
+    int64_t blocks = (n + SORT_TILE - 1) / SORT_TILE;
+    *bytes = al(sizeof(WsHeader)) + al(sizeof(uint32_t)) +
+             al((size_t)SORT_MAX_PASSES * std::max<int64_t>(blocks, 1) * SORT_RADIX * sizeof(uint32_t));
+    return GS_OK;
+}
+
+gs_status gs_debug_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt, uint32_t *vals_alt, int64_t n,
+                              int32_t key_bits, void *temp, size_t temp_bytes, gs_stream_t stream) {
+    size_t need = 0;
+    gs_status st = gs_sort_temp_size(n, key_bits, &need);
+    if (st) return st;
+    if (!keys || !vals || !keys_alt || !vals_alt || !temp) return GS_ERR_INVALID_ARG;
+    if (temp_bytes < need) return GS_ERR_SHAPE;
+    if (n == 0) return GS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t blocks = (n + SORT_TILE - 1) / SORT_TILE;
+    WsHeader *hdr = at<WsHeader>(temp, 0);
+    uint32_t *count = at<uint32_t>(temp, al(sizeof(WsHeader)));
+    uint32_t *look = at<uint32_t>(temp, al(sizeof(WsHeader)) + al(sizeof(uint32_t)));
+    uint32_t nn = (uint32_t)n;
+    // count lives in device memory like the workspace pair count (captured as a memset node)
+    cudaMemsetAsync(count, 0, sizeof(uint32_t), s);
+    cudaMemcpyAsync(count, &nn, sizeof(uint32_t), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);  // &nn is a stack variable
+    return cuda_status(launch_sort(keys, vals, keys_alt, vals_alt, count, blocks * SORT_TILE, key_bits, hdr, look,
+                                   blocks, s));
+}
+
+gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t n_views, int32_t width,
+                                  int32_t height, gs_ws_view *out) {
+    if (!ws || !out || n < 0 || n_views <= 0 || width <= 0 || height <= 0) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(n, n_views, width, height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    out->rec0 = at<const float>(ws, L.rec0);
+    out->rec1 = at<const float>(ws, L.rec1);
+    out->rec2 = at<const float>(ws, L.rec2);
+    out->depth = at<const float>(ws, L.depth);
+    out->radius = at<const int32_t>(ws, L.radius);
+    out->rect = at<const int32_t>(ws, L.rect);
+    out->tiles_touched = at<const uint32_t>(ws, L.tiles_touched);
+    out->offsets = at<const uint32_t>(ws, L.offsets);
+    out->keys = at<const uint64_t>(ws, L.keys0);
+    out->vals = at<const uint32_t>(ws, L.vals0);
+    out->ranges = at<const uint32_t>(ws, L.ranges);
+    out->n_contrib = at<const uint32_t>(ws, L.ncontrib);
+    out->capacity = L.cap;
+    return GS_OK;
+}
+
+gs_status gs_debug_exp_scale(const float *s, float *out, int64_t n, gs_stream_t stream) {
+    if (!s || !out || n < 0) return GS_ERR_INVALID_ARG;
+    return cuda_status(launch_exp_scale(s, out, n, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// gs_internal.cuh -- shared declarations of the libgs.so kernels (CUDA path only; the CPU
+// oracle in oracle/ shares nothing with this tree).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gs.h"
+
+namespace gsk {
+
+constexpr int TILE = GS_TILE;               // 16x16 pixel tiles
+constexpr int BLOCK_PIX = TILE * TILE;      // one thread per pixel in the raster kernels
+
+// radix sort: 8-bit digits, one decoupled-look-back ("onesweep") pass per digit
+constexpr int SORT_BITS = 8;
+constexpr int SORT_RADIX = 1 << SORT_BITS;
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 4096 pairs per CTA
+constexpr int SORT_MAX_PASSES = 8;
+
+// decoupled-look-back exclusive scan of tiles_touched
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+struct CamBatch {
+    gs_camera c[GS_MAX_VIEWS];
+};
+
+// Device-side header at the start of every workspace.
+struct WsHeader {
+    uint32_t flags;        // bit 0: pair capacity overflow
+    uint32_t P;            // total pairs of the last preprocess (may exceed capacity)
+    uint32_t scan_ctr;     // dynamic CTA index of the scan
+    uint32_t hist_ctr;     // last-CTA detection of the sort histogram
+    uint32_t sort_ctr[SORT_MAX_PASSES];
+    int32_t sort_sel[SORT_MAX_PASSES + 1];  // source buffer of each pass (0 = primary)
+    uint32_t sort_hist[SORT_MAX_PASSES][SORT_RADIX];
+    uint32_t sort_start[SORT_MAX_PASSES][SORT_RADIX];
+};
+
+// Byte offsets of every buffer inside a render workspace (pure function of n, V, W, H, cap).
+struct Layout {
+    int64_t n, M, cap;  // M = V * n
+    int V, W, H, TX, TY, tiles;
+    int64_t scan_blocks, sort_blocks;
+    size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags;
+    size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, Tfinal, total;
+};
+
+Layout make_layout(int64_t n, int V, int W, int H, int64_t cap);
+// largest layout (capacity) fitting in ws_bytes; returns false if even cap = 0 does not fit
+bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out);
+
+template <typename T>
+__host__ __device__ inline T *at(void *ws, size_t off) {
+    return reinterpret_cast<T *>(reinterpret_cast<char *>(ws) + off);
+}
+
+int sort_passes(int key_bits);
+int hi_bits_for(int64_t count);
+
+// ---- launchers (each returns cudaGetLastError()) ----
+cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
+                              cudaStream_t s);
+cudaError_t launch_scan(const Layout &L, void *ws, cudaStream_t s);
+cudaError_t launch_duplicate(const Layout &L, void *ws, cudaStream_t s);
+// generic pair sort on the primary buffers of a workspace (or debug buffers)
+cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, const uint32_t *count,
+                        int64_t cap, int key_bits, WsHeader *hdr, uint32_t *lookback, int64_t sort_blocks,
+                        cudaStream_t s);
+cudaError_t launch_ranges(const Layout &L, void *ws, cudaStream_t s);
+cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
+                              cudaStream_t s);
+cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);
+cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
+                                  float *grads, float *grad2d_norm, cudaStream_t s);
+cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int W, float lambda, float *loss,
+                        float *dL, void *ws, cudaStream_t s);
+size_t loss_ws_bytes(int V, int H, int W);
+cudaError_t launch_pyramid(const float *img, int N, int C, int H, int W, int levels, float *out, cudaStream_t s);
+cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
+                        int64_t g0, int64_t g1, int zero, cudaStream_t s);
+cudaError_t launch_exp_scale(const float *s, float *out, int64_t n, cudaStream_t st);
+
+}  // namespace gsk

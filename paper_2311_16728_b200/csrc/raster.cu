@@ -1,0 +1,254 @@
+// raster.cu -- A6 (per-tile front-to-back alpha compositing, Eq. 3) and A8 (its backward).
+//
+// Eq. 3 with the reading prod_{j<i}(1 - alpha_j) (R1), evaluated per
+// pixel over the depth-sorted list of its tile (SPEC.md:348 (4)): power = -1/2 d^T Q d with
+// d = pixel - mean2d (fp32 recipe order, bit-exact to the oracle), cut at power < -4.5
+// (Mahalanobis^2 > 9, R9) or power > 0; alpha = min(0.99, sigma e^power) (R7); skip alpha
+// < 1/255; stop the pixel when T (1 - alpha) < 1e-4 (R8).  One 256-thread CTA per
+// (view, 16x16 tile), one thread per pixel; Gaussian records are staged in shared memory in
+// batches of 256 and the CTA leaves as soon as every pixel of the tile has stopped.
+//
+// The backward replays each pixel's list back to front: dL/dc, dL/dalpha
+// = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  The nine
+// per-pixel gradients of a Gaussian are reduced over the warp with shuffles and added to the
+// per-(view, Gaussian) buffer with one vector red.global.add.v4.f32 triple per warp.
+#include "gs_internal.cuh"
+
+namespace gsk {
+
+#define FMA __fmaf_rn
+#define MUL __fmul_rn
+#define SUB __fsub_rn
+
+constexpr float ALPHA_MAX = 0.99f;
+constexpr float ALPHA_MIN = 1.0f / 255.0f;
+constexpr float T_STOP = 1e-4f;
+constexpr float POWER_CUT = -4.5f;
+
+// power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order
+__device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float C, float &dx, float &dy) {
+    dx = SUB(px, g0.x);
+    dy = SUB(py, g0.y);
+    float qf = FMA(MUL(C, dy), dy, MUL(MUL(g0.z, dx), dx));
+    return FMA(-MUL(g0.w, dx), dy, MUL(-0.5f, qf));
+}
+
+__global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restrict__ ranges,
+                                                          const uint32_t *__restrict__ vals,
+                                                          const float4 *__restrict__ rec0,
+                                                          const float4 *__restrict__ rec1,
+                                                          const float *__restrict__ rec2, int64_t n, int W, int H,
+                                                          int TX, int tiles, float bg0, float bg1, float bg2,
+                                                          float *__restrict__ out_rgb, float *__restrict__ out_T,
+                                                          float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib) {
+    __shared__ float4 s0[BLOCK_PIX];
+    __shared__ float4 s1[BLOCK_PIX];
+    __shared__ float s2[BLOCK_PIX];
+    const int view = blockIdx.z;
+    const int tile = blockIdx.y * TX + blockIdx.x;
+    const int tid = threadIdx.x;
+    const int px = blockIdx.x * TILE + (tid & (TILE - 1));
+    const int py = blockIdx.y * TILE + (tid >> 4);
+    const bool inside = px < W && py < H;
+    const uint2 range = ranges[(int64_t)view * tiles + tile];
+    const int todo_all = (int)(range.y - range.x);
+    const float fx = (float)px, fy = (float)py;
+    const int64_t vbase = (int64_t)view * n;
+    float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    uint32_t contributor = 0, last = 0;
+    bool done = !inside;
+    for (int b0 = 0; b0 < todo_all; b0 += BLOCK_PIX) {
+        if (__syncthreads_count(done) == BLOCK_PIX) break;
+        int idx = b0 + tid;
+        if (idx < todo_all) {
+            int64_t m = vbase + vals[range.x + idx];
+            s0[tid] = rec0[m];
+            s1[tid] = rec1[m];
+            s2[tid] = rec2[m];
+        }
+        __syncthreads();
+        int cnt = min(BLOCK_PIX, todo_all - b0);
+        for (int j = 0; j < cnt && !done; j++) {
+            contributor++;
+            float4 g0 = s0[j];
+            float4 g1 = s1[j];
+            float dx, dy;
+            float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
+            if (power > 0.0f || power < POWER_CUT) continue;
+            float alpha = fminf(ALPHA_MAX, g1.y * __expf(power));
+            if (alpha < ALPHA_MIN) continue;
+            float test_T = T * (1.0f - alpha);
+            if (test_T < T_STOP) {
+                done = true;
+                continue;
+            }
+            float w = alpha * T;
+            c0 += g1.z * w;
+            c1 += g1.w * w;
+            c2 += s2[j] * w;
+            T = test_T;
+            last = contributor;
+        }
+    }
+    if (inside) {
+        int64_t HW = (int64_t)H * W;
+        int64_t pix = (int64_t)py * W + px;
+        float *o = out_rgb + (int64_t)view * 3 * HW + pix;
+        o[0] = c0 + T * bg0;
+        o[HW] = c1 + T * bg1;
+        o[2 * HW] = c2 + T * bg2;
+        if (out_T) out_T[(int64_t)view * HW + pix] = T;
+        T_keep[(int64_t)view * HW + pix] = T;
+        ncontrib[(int64_t)view * HW + pix] = last;
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restrict__ ranges,
+                                                          const uint32_t *__restrict__ vals,
+                                                          const float4 *__restrict__ rec0,
+                                                          const float4 *__restrict__ rec1,
+                                                          const float *__restrict__ rec2, int64_t n, int W, int H,
+                                                          int TX, int tiles, float bg0, float bg1, float bg2,
+                                                          const float *__restrict__ dL_drgb,
+                                                          const float *__restrict__ T_keep,
+                                                          const uint32_t *__restrict__ ncontrib,
+                                                          float4 *__restrict__ g2d) {
+    __shared__ float4 s0[BLOCK_PIX];
+    __shared__ float4 s1[BLOCK_PIX];
+    __shared__ float s2[BLOCK_PIX];
+    __shared__ uint32_t sid[BLOCK_PIX];
+    __shared__ uint32_t s_maxlast;
+    const int view = blockIdx.z;
+    const int tile = blockIdx.y * TX + blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int px = blockIdx.x * TILE + (tid & (TILE - 1));
+    const int py = blockIdx.y * TILE + (tid >> 4);
+    const bool inside = px < W && py < H;
+    const uint2 range = ranges[(int64_t)view * tiles + tile];
+    const float fx = (float)px, fy = (float)py;
+    const int64_t vbase = (int64_t)view * n;
+    const int64_t HW = (int64_t)H * W;
+    const int64_t pix = (int64_t)py * W + px;
+    float T = 1.f, g_0 = 0.f, g_1 = 0.f, g_2 = 0.f;
+    uint32_t last = 0;
+    if (inside) {
+        T = T_keep[(int64_t)view * HW + pix];
+        last = ncontrib[(int64_t)view * HW + pix];
+        const float *g = dL_drgb + (int64_t)view * 3 * HW + pix;
+        g_0 = g[0];
+        g_1 = g[HW];
+        g_2 = g[2 * HW];
+    }
+    if (tid == 0) s_maxlast = 0;
+    __syncthreads();
+    atomicMax(&s_maxlast, last);
+    __syncthreads();
+    // only the list prefix that some pixel composited matters
+    const int todo_all = (int)s_maxlast;
+    float acc0 = bg0, acc1 = bg1, acc2 = bg2;
+    // process positions todo_all-1 .. 0 (0-based within the tile range), batches from the back
+    for (int b_end = todo_all; b_end > 0; b_end -= BLOCK_PIX) {
+        int b_start = max(0, b_end - BLOCK_PIX);
+        int cnt = b_end - b_start;
+        __syncthreads();
+        if (tid < cnt) {
+            int pos = b_end - 1 - tid;  // s[tid] holds position b_end-1-tid (back to front)
+            uint32_t gi = vals[range.x + pos];
+            int64_t m = vbase + gi;
+            sid[tid] = (uint32_t)gi;
+            s0[tid] = rec0[m];
+            s1[tid] = rec1[m];
+            s2[tid] = rec2[m];
+        }
+        __syncthreads();
+        for (int j = 0; j < cnt; j++) {
+            uint32_t position = (uint32_t)(b_end - j);  // 1-based position in the tile list
+            float4 g0 = s0[j];
+            float4 g1 = s1[j];
+            float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
+            float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
+            bool contrib = false;
+            if (position <= last) {
+                float dx, dy;
+                float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
+                if (!(power > 0.0f || power < POWER_CUT)) {
+                    float e = __expf(power);
+                    float a_raw = g1.y * e;
+                    float alpha = fminf(ALPHA_MAX, a_raw);
+                    if (alpha >= ALPHA_MIN) {
+                        contrib = true;
+                        T = T / (1.0f - alpha);  // transmittance before this Gaussian
+                        float w = alpha * T;
+                        dLdr = g_0 * w;
+                        dLdg = g_1 * w;
+                        dLdb = g_2 * w;
+                        float cr = g1.z, cg = g1.w, cb = s2[j];
+                        float dLda = T * (g_0 * (cr - acc0) + g_1 * (cg - acc1) + g_2 * (cb - acc2));
+                        acc0 = alpha * cr + (1.f - alpha) * acc0;
+                        acc1 = alpha * cg + (1.f - alpha) * acc1;
+                        acc2 = alpha * cb + (1.f - alpha) * acc2;
+                        if (!(a_raw > ALPHA_MAX)) {
+                            dLdsig = e * dLda;
+                            float dLdp = alpha * dLda;
+                            float A = g0.z, B = g0.w, C = g1.x;
+                            dLdu = dLdp * (A * dx + B * dy);
+                            dLdv = dLdp * (C * dy + B * dx);
+                            dLdA = -0.5f * dx * dx * dLdp;
+                            dLdB = -dx * dy * dLdp;
+                            dLdC = -0.5f * dy * dy * dLdp;
+                        }
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+                dLdu = warp_sum(dLdu);
+                dLdv = warp_sum(dLdv);
+                dLdA = warp_sum(dLdA);
+                dLdB = warp_sum(dLdB);
+                dLdC = warp_sum(dLdC);
+                dLdsig = warp_sum(dLdsig);
+                dLdr = warp_sum(dLdr);
+                dLdg = warp_sum(dLdg);
+                dLdb = warp_sum(dLdb);
+                if (lane == 0) {
+                    float4 *dst = g2d + 3 * (vbase + sid[j]);
+                    red_add_v4(dst, dLdu, dLdv, dLdA, dLdB);
+                    red_add_v4(dst + 1, dLdC, dLdsig, dLdr, dLdg);
+                    red_add_v4(dst + 2, dLdb, 0.f, 0.f, 0.f);
+                }
+            }
+        }
+    }
+}
+
+cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
+                              cudaStream_t s) {
+    dim3 grid(L.TX, L.TY, L.V);
+    k_raster_fwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
+                                            at<float4>(ws, L.rec1), at<float>(ws, L.rec2), L.n, L.W, L.H, L.TX,
+                                            L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
+                                            at<uint32_t>(ws, L.ncontrib));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
+    dim3 grid(L.TX, L.TY, L.V);
+    k_raster_bwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
+                                            at<float4>(ws, L.rec1), at<float>(ws, L.rec2), L.n, L.W, L.H, L.TX,
+                                            L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
+                                            at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
+    return cudaGetLastError();
+}
+
+}  // namespace gsk

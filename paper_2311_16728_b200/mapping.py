@@ -1,0 +1,127 @@
+"""Photorealistic-mapping driver: Gaussian-pyramid schedule (Eq. 5), one mapping iteration
+per level (render -> loss -> backward -> [all-reduce] -> Adam), keyframe-batch data
+parallelism over torch.distributed (NCCL).  Host logic only; every stage is a libgs.so call.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from synth import scaled_camera
+
+from .core import Adam, AdamConfig, PhotometricLoss, Renderer, gaussian_pyramid, level_shapes, pack_params
+
+
+def gp_level(iteration: int, n_levels: int, iters_per_level: int) -> int:
+    """Eq. 5: start at the top level n, step down every iters_per_level
+    iterations, stay at 0 (SPEC.md:443-451 gp_level; R21/R26)."""
+    if iteration < 0 or n_levels < 0 or iters_per_level <= 0:
+        raise ValueError("gp_level: iteration >= 0, n >= 0, iters_per_level > 0")
+    return max(0, n_levels - iteration // iters_per_level)
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Keyframe-batch partition: rank g takes views g, g+G, ..."""
+    return list(range(rank, n_views, world))
+
+
+def reduce_gradients(grads: torch.Tensor, group=None) -> torch.Tensor:
+    """A10: sum of the per-rank gradients (R22) -- the only exchange step of the path."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
+    return grads
+
+
+class MappingEngine:
+    """Optimises one Gaussian map against the keyframes of this rank.
+
+    scene: synth.Scene (initial parameters); cams: this rank's keyframe cameras (level 0);
+    gts: [V, 3, H, W] level-0 targets (numpy or torch); n_levels: top pyramid level n (n=2,
+    PAPER.md:568)."""
+
+    def __init__(self, scene, cams, gts, n_levels: int = 2, lam: float = 0.2, adam: AdamConfig | None = None,
+                 device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0)):
+        self.device = device
+        self.n = scene.means.shape[0]
+        self.D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
+        self.params = pack_params(scene, device)
+        self.grads = torch.zeros_like(self.params)
+        self.grad2d_norm = torch.zeros(self.n, dtype=torch.float32, device=device)
+        self.adam = Adam(self.params, self.n, self.D, adam)
+        self.cams0 = list(cams)
+        self.V = len(self.cams0)
+        self.n_levels = n_levels
+        self.lam = lam
+        self.bg = bg
+        self.group = group
+        H, W = self.cams0[0].height, self.cams0[0].width
+        self.shapes = level_shapes(H, W, n_levels)
+        self.cams = [[scaled_camera(c, l) for c in self.cams0] for l in range(n_levels + 1)]
+        self.gt0 = torch.empty((self.V, 3, H, W), dtype=torch.float32, device=device)
+        self.set_keyframes(gts)
+        self.losses = [PhotometricLoss(self.V, h, w, lam, device) for (h, w) in self.shapes]
+        self.renderers = [None] * (n_levels + 1)
+        self.margin = capacity_margin
+        self.calibrate()
+
+    # ------------------------------------------------------------------ keyframes / A0
+    def set_keyframes(self, gts):
+        g = torch.as_tensor(np.asarray(gts, np.float32) if not torch.is_tensor(gts) else gts)
+        self.gt0.copy_(g.to(self.device, non_blocking=True).view_as(self.gt0))
+        self.build_pyramids()
+
+    def build_pyramids(self):
+        """A0: GP^l(I_gt), l = 1..n, once per keyframe."""
+        self.pyr = gaussian_pyramid(self.gt0, self.n_levels)
+
+    # ------------------------------------------------------------------ capacity
+    def calibrate(self, min_capacity: int = 1 << 16):
+        """Size each level's pair capacity from a measured pair count (one sync, setup only)."""
+        for l, (h, w) in enumerate(self.shapes):
+            r = self.renderers[l]
+            if r is None:
+                r = Renderer(self.n, self.D, self.V, w, h, min_capacity, self.device)
+            r.forward(self.params, self.cams[l], self.bg)
+            st, flags, pairs = r.ws.status()
+            need = int(pairs * self.margin) + 4096
+            if need > r.ws.capacity or r.ws.capacity > 4 * need:
+                r = Renderer(self.n, self.D, self.V, w, h, max(need, min_capacity), self.device)
+            self.renderers[l] = r
+
+    def check(self):
+        """Synchronises; raises if any level overflowed its pair capacity (then re-calibrate)."""
+        for r in self.renderers:
+            st, flags, pairs = r.ws.status()
+            if flags & 1:
+                raise RuntimeError(f"pair capacity exceeded ({pairs} > {r.ws.capacity})")
+
+    # ------------------------------------------------------------------ iteration
+    def render(self, level: int = 0):
+        return self.renderers[level].forward(self.params, self.cams[level], self.bg)
+
+    def iteration(self, level: int) -> torch.Tensor:
+        """One optimiser step at pyramid level `level` (Eq. 4 against GP^level, R19)."""
+        r = self.renderers[level]
+        cams = self.cams[level]
+        rgb, _ = r.forward(self.params, cams, self.bg)                       # A1-A6
+        loss, dL = self.losses[level](rgb, self.pyr[level])                  # A7
+        r.backward(self.params, cams, dL, self.grads, self.grad2d_norm, self.bg)  # A8-A9
+        reduce_gradients(self.grads, self.group)                             # A10
+        self.adam.step(self.grads, zero_grads=True)                          # A11
+        return loss
+
+    def step(self) -> list:
+        """One pass of the Eq. 5 schedule: iterations at levels n, n-1, ..., 0."""
+        return [self.iteration(l) for l in range(self.n_levels, -1, -1)]
+
+    def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor):
+        """End-to-end public API: new keyframe targets from pinned host memory (H2D), A0,
+        the Eq. 5 pass, per-level losses back to pinned host memory (D2H)."""
+        self.gt0.copy_(gts_pinned, non_blocking=True)
+        self.build_pyramids()
+        losses = self.step()
+        out_pinned.copy_(torch.stack(losses), non_blocking=True)
+        return out_pinned

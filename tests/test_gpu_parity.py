@@ -1,0 +1,353 @@
+"""GPU parity of the CUDA path (libgs.so through the C ABI) against the CPU oracle, on the same
+seeded synthetic inputs (SURVEY §8(c) parity contract):
+
+1. decision quantities (cull, radius, rect, tiles, depth, mean2d, conic): bit-exact;
+2. binning keys, values, ranges: bit-exact;
+3. colour and final T: |d| <= 1e-4 on pixels outside the oracle's ambiguity band; flagged
+   pixels <= 1e-3 of all and each within 1.1e-2;
+4. last contributor equal on non-flagged pixels;
+5. gradients: |d| <= 1e-3 max(|g_ref|, 1e-2 RMS_class(g_ref)) outside Gaussians touching
+   flagged pixels; loss rel <= 1e-5;
+6. pyramid |d| <= 1e-6; Adam rel <= 1e-6 after one step.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle.oracle as orc
+from paper_2311_16728_b200 import _lib as L
+from paper_2311_16728_b200.core import (Adam, AdamConfig, PhotometricLoss, Renderer, gaussian_pyramid, pack_params,
+                                        unpack)
+from paper_2311_16728_b200.mapping import MappingEngine
+from synth import make_cameras, make_scene, noise_image, perturb, scaled_camera
+
+pytestmark = pytest.mark.gpu
+
+CLASSES = ["means", "quats", "log_scales", "opacity_logits", "sh"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2311_16728_b200.build import build
+    build()
+    L.lib()
+
+
+def _renderer(scene, cams, cap=None):
+    n = scene.means.shape[0]
+    D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
+    params = pack_params(scene)
+    if cap is None:
+        _, _, _, tt = orc.bin_pairs(scene, cams)
+        cap = int(tt.sum()) + 4096
+    r = Renderer(n, D, len(cams), cams[0].width, cams[0].height, cap)
+    return r, params, D
+
+
+def _sample_pixels(V, H, W, k, seed):
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(V * H * W, size=min(k, V * H * W), replace=False)
+    v, rem = np.divmod(idx, H * W)
+    y, x = np.divmod(rem, W)
+    return np.stack([v, y, x], 1).astype(np.int32)
+
+
+# ------------------------------------------------------------------------------ recipe pieces
+def test_exp_scale_bit_exact():
+    """The recipe's e = (float)exp((double)s) on the GPU equals the oracle's, over every 7th
+    fp32 bit pattern of log-scales in [-12, 3] (DESIGN.md fp32 recipe)."""
+    lo = np.array([-12.0], np.float32).view(np.uint32)[0]
+    hi = np.array([3.0], np.float32).view(np.uint32)[0]
+    neg = np.arange(np.array([-0.0], np.float32).view(np.uint32)[0], lo, 7, dtype=np.uint32)
+    pos = np.arange(0, hi, 7, dtype=np.uint32)
+    for chunk in (neg, pos):
+        s = chunk.view(np.float32)
+        ref = orc.exp_scale_f32(s)
+        st = torch.from_numpy(s).cuda()
+        out = torch.empty_like(st)
+        L.gs_debug_exp_scale(st, out)
+        got = out.cpu().numpy()
+        bad = np.nonzero(got.view(np.uint32) != ref.view(np.uint32))[0]
+        assert bad.size == 0, (bad.size, s[bad[:5]])
+
+
+@pytest.mark.parametrize("cfg,n,views,level", [("tiny", None, 1, 0), ("tum", 60000, 1, 0), ("tum", 60000, 3, 2),
+                                               ("replica", 40000, 2, 1)])
+def test_preprocess_and_binning_bit_exact(cfg, n, views, level):
+    scene = make_scene(cfg, n=n)
+    cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    torch.cuda.synchronize()
+    v = r.ws.views()
+    N = scene.means.shape[0]
+    for k, cam in enumerate(cams):
+        o = orc.project(scene, cam, "recipe")
+        sl = slice(k * N, (k + 1) * N)
+        rad = v["radius"][sl].cpu().numpy()
+        np.testing.assert_array_equal(rad, o["radius"])
+        vis = o["radius"] > 0
+        np.testing.assert_array_equal(v["rect"][sl].cpu().numpy()[vis], o["rect"][vis])
+        np.testing.assert_array_equal(v["depth"][sl].cpu().numpy()[vis].view(np.uint32), o["depth_bits"][vis])
+        np.testing.assert_array_equal(v["mean2d"][sl].cpu().numpy()[vis].view(np.uint32),
+                                      o["mean2d_f"][vis].view(np.uint32))
+        np.testing.assert_array_equal(v["conic"][sl].cpu().numpy()[vis].view(np.uint32),
+                                      o["conic_f"][vis].view(np.uint32))
+    keys, vals, ranges, tt = orc.bin_pairs(scene, cams)
+    st, flags, P = r.ws.status()
+    assert st == L.GS_OK and flags == 0 and P == keys.size
+    np.testing.assert_array_equal(v["tiles_touched"].cpu().numpy(), tt.reshape(-1))
+    np.testing.assert_array_equal(v["keys"][:P].cpu().numpy().view(np.uint64), keys)
+    np.testing.assert_array_equal(v["vals"][:P].cpu().numpy().view(np.uint32), vals)
+    np.testing.assert_array_equal(v["ranges"].cpu().numpy().view(np.uint32), ranges)
+
+
+@pytest.mark.parametrize("n,bits,kind", [(1, 40, "rand"), (4095, 44, "depth"), (4096, 44, "rand"),
+                                         (4097, 48, "depth"), (300_001, 44, "depth"), (1_000_003, 64, "rand"),
+                                         (2_000_000, 12, "rand")])
+def test_radix_sort_stable(n, bits, kind):
+    rng = np.random.default_rng(n)
+    if bits > 32:
+        hi = rng.integers(0, 1 << (bits - 32), size=n, dtype=np.uint64)
+        if kind == "depth":  # float bits of depths in [0.5, 8): constant top bits (skipped passes)
+            lo = np.sort(rng.uniform(0.5, 8.0, size=n).astype(np.float32)).view(np.uint32).astype(np.uint64)
+        else:
+            lo = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+        keys = (hi << np.uint64(32)) | lo
+    else:
+        keys = rng.integers(0, 1 << bits, size=n, dtype=np.uint64)
+    if n > 10:
+        keys[rng.integers(0, n, size=n // 10)] = keys[0]  # many ties
+    vals = np.arange(n, dtype=np.uint32)
+    k = torch.from_numpy(keys.view(np.int64)).cuda()
+    v = torch.from_numpy(vals.view(np.int32)).cuda()
+    k2, v2 = torch.empty_like(k), torch.empty_like(v)
+    temp = torch.empty(L.gs_sort_temp_size(n, bits), dtype=torch.uint8, device="cuda")
+    L.gs_debug_sort_pairs(k, v, k2, v2, bits, temp)
+    order = np.argsort(keys, kind="stable")
+    np.testing.assert_array_equal(k.cpu().numpy().view(np.uint64), keys[order])
+    np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), vals[order])
+
+
+# ------------------------------------------------------------------------------ forward
+def _check_colour(got_rgb, got_T, ref, pixels_mask=None):
+    flag = ref["flag"].astype(bool)
+    d = np.abs(got_rgb - ref["rgb"]).max(axis=-1 if got_rgb.ndim == 2 else 1)
+    dT = np.abs(got_T - ref["T"])
+    ok = ~flag
+    assert flag.mean() <= 1e-3 + 1e-9, flag.mean()
+    assert d[ok].max(initial=0) <= 1e-4, d[ok].max()
+    assert dT[ok].max(initial=0) <= 1e-4, dT[ok].max()
+    assert d[flag].max(initial=0) <= 1.1e-2
+
+
+def test_forward_parity_tiny_full_image():
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, _ = _renderer(scene, cams)
+    rgb, T = r.forward(params, cams)
+    ref = orc.render(scene, cams, "recipe")
+    _check_colour(rgb.cpu().numpy(), T.cpu().numpy(), ref)
+    # last contributor (Gaussian id) equal on non-flagged pixels
+    v = r.ws.views()
+    nc = v["n_contrib"].cpu().numpy().reshape(1, cams[0].height, cams[0].width)
+    ranges = v["ranges"].cpu().numpy()
+    vals = v["vals"].cpu().numpy()
+    TX = r.ws.tiles_x
+    ys, xs = np.mgrid[0:cams[0].height, 0:cams[0].width]
+    tile = (ys // 16) * TX + xs // 16
+    last = np.where(nc[0] > 0, vals[np.clip(ranges[tile, 0] + nc[0] - 1, 0, None)], -1)
+    ok = ref["flag"][0] == 0
+    np.testing.assert_array_equal(last[ok], ref["last"][0][ok])
+    assert (ref["ncomp"] > 0).mean() > 0.3
+
+
+@pytest.mark.parametrize("cfg,views,level", [("tum", 1, 0), ("tum", 1, 2), ("euroc", 4, 1), ("replica", 1, 0)])
+def test_forward_parity_full_size_sampled(cfg, views, level):
+    scene = make_scene(cfg)
+    cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
+    r, params, _ = _renderer(scene, cams, cap=None)
+    rgb, T = r.forward(params, cams)
+    H, W = cams[0].height, cams[0].width
+    pix = _sample_pixels(views, H, W, 4096, 7)
+    ref = orc.render(scene, cams, "recipe", pixels=pix)
+    g = rgb.cpu().numpy()[pix[:, 0], :, pix[:, 1], pix[:, 2]]
+    gT = T.cpu().numpy()[pix[:, 0], pix[:, 1], pix[:, 2]]
+    _check_colour(g, gT, ref)
+
+
+def test_forward_deterministic_and_empty():
+    scene = make_scene("tum", n=50000)
+    cams = make_cameras("tum", 1)
+    r, params, _ = _renderer(scene, cams)
+    a = r.forward(params, cams)[0].clone()
+    b = r.forward(params, cams)[0].clone()
+    assert torch.equal(a, b)
+    # all Gaussians behind the camera: empty image, T = 1
+    s2 = scene.copy()
+    s2.means[:] = cams[0].centre() - 5 * cams[0].R[2]
+    r2, p2, _ = _renderer(s2, cams, cap=4096)
+    rgb, T = r2.forward(p2, cams)
+    assert rgb.abs().max().item() == 0 and T.min().item() == 1.0
+
+
+def test_capacity_overflow_flag_and_stale_state():
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, D = _renderer(scene, cams, cap=1)  # rounds up to 4096 pairs
+    s2 = scene.copy()
+    s2.log_scales += 2.5  # huge footprints: far more than 4096 pairs
+    p2 = pack_params(s2)
+    r.forward(p2, cams)
+    st, flags, P = r.ws.status()
+    assert st == L.GS_ERR_CAPACITY and flags & 1 and P > 4096
+    # backward with other cameras than the last forward -> StaleRenderState
+    import dataclasses
+    cam2 = [dataclasses.replace(cams[0], t=cams[0].t + np.float32(0.01))]
+    grads = torch.zeros_like(p2)
+    dL = torch.zeros((1, 3, cams[0].height, cams[0].width), device="cuda")
+    with pytest.raises(L.GsError) as e:
+        r.backward(p2, cam2, dL, grads)
+    assert e.value.status == L.GS_ERR_STALE_STATE
+
+
+# ------------------------------------------------------------------------------ loss / pyramid / adam
+@pytest.mark.parametrize("V,H,W", [(1, 16, 16), (2, 45, 61), (1, 120, 160)])
+def test_loss_parity(V, H, W):
+    rng = np.random.default_rng(H * W)
+    x = rng.uniform(0, 1, size=(V, 3, H, W)).astype(np.float32)
+    y = rng.uniform(0, 1, size=(V, 3, H, W)).astype(np.float32)
+    y[:, :, : H // 3] = x[:, :, : H // 3]  # some exactly equal pixels (L1 subgradient 0)
+    pl = PhotometricLoss(V, H, W, 0.2)
+    loss, dL = pl(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    loss, dL = loss.cpu().numpy(), dL.cpu().numpy()
+    for v in range(V):
+        l_ref, _, d_ref = orc.loss(x[v], y[v], 0.2)
+        assert loss[v] == pytest.approx(l_ref, rel=1e-5)
+        np.testing.assert_allclose(dL[v], d_ref, rtol=1e-3, atol=1e-3 * np.abs(d_ref).max())
+
+
+def test_pyramid_parity():
+    rng = np.random.default_rng(0)
+    img = rng.uniform(size=(2, 3, 37, 50)).astype(np.float32)
+    lv = gaussian_pyramid(torch.from_numpy(img).cuda(), 2)
+    for k in range(2):
+        ref = orc.pyramid(img[k], 2)
+        for l in range(3):
+            np.testing.assert_allclose(lv[l][k].cpu().numpy(), ref[l], atol=1e-6, rtol=0)
+    with pytest.raises(L.GsError):
+        gaussian_pyramid(torch.zeros((1, 3, 8, 8), device="cuda"), 3)
+
+
+@pytest.mark.parametrize("sgd", [False, True])
+def test_adam_parity(sgd):
+    rng = np.random.default_rng(3)
+    scene = make_scene("tiny", n=777)
+    D = 0
+    n = scene.means.shape[0]
+    params = pack_params(scene)
+    cfg = AdamConfig(sgd=sgd, lr_means=1e-2)
+    opt = Adam(params, n, D, cfg)
+    g = torch.from_numpy(rng.normal(size=tuple(params.shape)).astype(np.float32)).cuda()
+    g[:, n:] = 0
+    p0 = params.cpu().numpy().astype(np.float64)
+    m = np.zeros_like(p0)
+    v = np.zeros_like(p0)
+    for step in (1, 2, 3):
+        gg = g.clone()
+        opt.step(gg, zero_grads=True)
+        assert gg.abs().max().item() == 0
+        lrs = cfg.struct().lr
+        rows_lr = [lrs[0]] * 3 + [lrs[1]] * 4 + [lrs[2]] * 3 + [lrs[3]] + [lrs[4]] * 3 + [lrs[5]] * (params.shape[0] - 14)
+        gn = g.cpu().numpy().astype(np.float64)
+        for row, lr in enumerate(rows_lr):
+            p0[row], m[row], v[row] = orc.adam(p0[row], gn[row], m[row], v[row], lr=np.float32(lr).item(),
+                                               eps=1e-15, step=step, sgd_mode=sgd)
+        got = params.cpu().numpy()
+        ulp = np.spacing(np.abs(got).astype(np.float32)).astype(np.float64)
+        assert (np.abs(got - p0) <= 4 * ulp + 1e-6 * np.abs(p0 - got + 1e-30)).all()
+        if not sgd:
+            np.testing.assert_allclose(opt.m.cpu().numpy(), m, rtol=1e-6, atol=1e-12)
+            np.testing.assert_allclose(opt.v.cpu().numpy(), v, rtol=1e-5, atol=1e-15)
+
+
+# ------------------------------------------------------------------------------ backward
+def _check_grads(got, ref, flagged):
+    keep = flagged == 0
+    for c in CLASSES:
+        a, b = got[c][keep], ref[c][keep]
+        rms = math.sqrt(float((ref[c] ** 2).mean())) + 1e-30
+        tol = 1e-3 * np.maximum(np.abs(b), 1e-2 * rms)
+        bad = np.abs(a - b) > tol
+        assert bad.sum() == 0, (c, int(bad.sum()), float(np.abs(a - b)[bad].max()), rms)
+
+
+def test_backward_parity_tiny():
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    H, W = cams[0].height, cams[0].width
+    G = np.random.default_rng(1).normal(size=(1, 3, H, W)).astype(np.float32)
+    grads = torch.zeros_like(params)
+    gn = torch.zeros(scene.means.shape[0], device="cuda")
+    r.backward(params, cams, torch.from_numpy(G).cuda(), grads, gn)
+    got = unpack(grads, scene.means.shape[0], D)
+    ref = orc.backward(scene, cams, G, "recipe")
+    _check_grads(got, ref, ref["flagged"])
+    keep = ref["flagged"] == 0
+    np.testing.assert_allclose(gn.cpu().numpy()[keep], ref["grad2d_norm"][keep], rtol=1e-3,
+                               atol=1e-5 * ref["grad2d_norm"].max())
+
+
+@pytest.mark.parametrize("cfg,views,level,D", [("tum", 1, 0, 3), ("tum", 1, 2, 3), ("euroc", 3, 1, 3)])
+def test_backward_parity_sampled(cfg, views, level, D):
+    """dL/dI masked to 4096 sampled pixels on both sides (SURVEY §8(d) 'Parity runs')."""
+    scene = make_scene(cfg)
+    cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    H, W = cams[0].height, cams[0].width
+    pix = _sample_pixels(views, H, W, 4096, 3)
+    gp = np.random.default_rng(2).normal(size=(pix.shape[0], 3)).astype(np.float32)
+    G = np.zeros((views, 3, H, W), np.float32)
+    G[pix[:, 0], :, pix[:, 1], pix[:, 2]] = gp
+    grads = torch.zeros_like(params)
+    r.backward(params, cams, torch.from_numpy(G).cuda(), grads)
+    got = unpack(grads, scene.means.shape[0], D)
+    ref = orc.backward(scene, cams, gp, "recipe", pixels=pix)
+    _check_grads(got, ref, ref["flagged"])
+
+
+def test_backward_accumulates_and_zero_upstream():
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    grads = torch.zeros_like(params)
+    r.backward(params, cams, torch.zeros((1, 3, 48, 64), device="cuda"), grads)
+    assert grads.abs().max().item() == 0
+    G = torch.randn((1, 3, 48, 64), device="cuda")
+    r.backward(params, cams, G, grads)
+    one = grads.clone()
+    r.backward(params, cams, G, grads)
+    torch.testing.assert_close(grads, 2 * one, rtol=1e-5, atol=1e-7)
+
+
+# ------------------------------------------------------------------------------ mapping loop
+def test_mapping_engine_reduces_loss():
+    """A few Eq. 5 passes on the tiny config reduce the photometric loss (SPEC.md:460 trend)."""
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, _ = _renderer(scene, cams)
+    gt = r.forward(params, cams)[0].clone()
+    eng = MappingEngine(perturb(scene, 9), cams, gt, n_levels=1, adam=AdamConfig(lr_means=1e-3))
+    first = torch.stack(eng.step()).cpu().numpy()
+    for _ in range(60):
+        last = torch.stack(eng.step()).cpu().numpy()
+    eng.check()
+    assert last[-1] < 0.7 * first[-1], (first, last)
