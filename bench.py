@@ -223,6 +223,15 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     eng.check()
+    if args.launch_list:
+        # exactly one step inside a cudaProfilerStart/Stop range (ncu --profile-from-start off)
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        if rank == 0:
+            print(json.dumps({"launch_list": True, "config": args.config}), flush=True)
+        return 0
 
     # ---- per-stage breakdown (separate instrumented pass; not the headline)
     stage = {k: 0.0 for k in ("pyramid", "preprocess", "render_fwd", "loss", "backward", "allreduce", "adam")}
@@ -385,6 +394,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-pixels", type=int, default=4096)
+    ap.add_argument("--launch-list", action="store_true", help="profile exactly one step (ncu range)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -168,7 +168,7 @@ gs_status gs_debug_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt
 typedef struct {
     const float *rec0;            /* [n_views*n][4] (u, v, A, B): mean2d, conic A, B */
     const float *rec1;            /* [n_views*n][4] (C, sigma, r, g)                 */
-    const float *rec2;            /* [n_views*n] b                                   */
+    const float *rec2;            /* [n_views*n][4] (b, 3-sigma x/y extents, -)      */
     const float *depth;           /* [n_views*n] view-space z                        */
     const int32_t *radius;        /* [n_views*n] 0 = culled                          */
     const int32_t *rect;          /* [n_views*n][4] tile x0, y0, x1, y1 (exclusive)  */

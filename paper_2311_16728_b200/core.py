@@ -65,9 +65,9 @@ class Workspace:
         tiles = self.tiles_x * self.tiles_y * self.V
         rec0 = self._slice(v.rec0, 4 * M, torch.float32).view(M, 4)
         rec1 = self._slice(v.rec1, 4 * M, torch.float32).view(M, 4)
-        rec2 = self._slice(v.rec2, M, torch.float32)
+        rec2 = self._slice(v.rec2, 4 * M, torch.float32).view(M, 4)
         return dict(mean2d=rec0[:, 0:2], conic=torch.stack([rec0[:, 2], rec0[:, 3], rec1[:, 0]], 1),
-                    sigma=rec1[:, 1], rgb=torch.stack([rec1[:, 2], rec1[:, 3], rec2], 1),
+                    sigma=rec1[:, 1], rgb=torch.stack([rec1[:, 2], rec1[:, 3], rec2[:, 0]], 1), extent=rec2[:, 1:3],
                     depth=self._slice(v.depth, M, torch.float32),
                     radius=self._slice(v.radius, M, torch.int32),
                     rect=self._slice(v.rect, 4 * M, torch.int32).view(M, 4),

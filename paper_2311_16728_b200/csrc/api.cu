@@ -35,7 +35,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.hdr = take(sizeof(WsHeader));
     L.rec0 = take(M * sizeof(float4));
     L.rec1 = take(M * sizeof(float4));
-    L.rec2 = take(M * sizeof(float));
+    L.rec2 = take(M * sizeof(float4));
     L.depth = take(M * sizeof(float));
     L.radius = take(M * sizeof(int32_t));
     L.rect = take(M * sizeof(int4));
@@ -43,6 +43,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.offsets = take(M * sizeof(uint32_t));
     L.grad2d = take(M * 3 * sizeof(float4));
     L.scan_flags = take((size_t)std::max<int64_t>(L.scan_blocks, 1) * sizeof(uint64_t));
+    L.vis_list = take((size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t));
     L.ranges = take((size_t)V * L.tiles * sizeof(uint2));
     L.ncontrib = take((size_t)V * W * H * sizeof(uint32_t));
     L.Tfinal = take((size_t)V * W * H * sizeof(float));
@@ -146,7 +147,7 @@ gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t 
     if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
     cudaStream_t s = (cudaStream_t)stream;
     WsHeader *hdr = at<WsHeader>(ws, L.hdr);
-    cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter
+    cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter, visible count
     cudaMemsetAsync(at<char>(ws, L.scan_flags), 0, (size_t)std::max<int64_t>(L.scan_blocks, 1) * 8, s);
     cudaError_t e = launch_preprocess(*params, cb, n_views, L, ws, s);
     if (e == cudaSuccess) e = launch_scan(L, ws, s);

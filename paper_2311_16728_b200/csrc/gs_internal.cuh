@@ -33,6 +33,7 @@ struct WsHeader {
     uint32_t flags;        // bit 0: pair capacity overflow
     uint32_t P;            // total pairs of the last preprocess (may exceed capacity)
     uint32_t scan_ctr;     // dynamic CTA index of the scan
+    uint32_t vis_count;    // Gaussians visible in at least one view (compacted list length)
     uint32_t hist_ctr;     // last-CTA detection of the sort histogram
     uint32_t sort_ctr[SORT_MAX_PASSES];
     int32_t sort_sel[SORT_MAX_PASSES + 1];  // source buffer of each pass (0 = primary)
@@ -45,7 +46,7 @@ struct Layout {
     int64_t n, M, cap;  // M = V * n
     int V, W, H, TX, TY, tiles;
     int64_t scan_blocks, sort_blocks;
-    size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags;
+    size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, Tfinal, total;
 };
 

@@ -219,12 +219,13 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
     float sigma = 1.0f / (1.0f + expf(-op));
     float4 *rec0 = at<float4>(ws, L.rec0);
     float4 *rec1 = at<float4>(ws, L.rec1);
-    float *rec2 = at<float>(ws, L.rec2);
+    float4 *rec2 = at<float4>(ws, L.rec2);
     float *depth = at<float>(ws, L.depth);
     int32_t *radius = at<int32_t>(ws, L.radius);
     int4 *rect = at<int4>(ws, L.rect);
     uint32_t *tt = at<uint32_t>(ws, L.tiles_touched);
     float4 *g2d = at<float4>(ws, L.grad2d);
+    bool any_vis = false;
     for (int v = 0; v < V; v++) {
         const gs_camera &cam = cams.c[v];
         int64_t m = (int64_t)v * n + i;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
             tt[m] = 0;
             continue;
         }
+        any_vis = true;
         // SH colour, dir = normalize(P - C_cam) (R6)
         float Cc[3];
         cam_centre(cam, Cc);
@@ -251,7 +253,9 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
         }
         rec0[m] = make_float4(p.u, p.v, p.A, p.B);
         rec1[m] = make_float4(p.C, sigma, rgb[0], rgb[1]);
-        rec2[m] = rgb[2];
+        // padded exact 3-sigma extents of the ellipse d^T Q d <= 9 (Q^-1 = Sigma2' = [[a, b], [b, c]]):
+        // used by the raster kernels for a conservative warp-level skip test
+        rec2[m] = make_float4(rgb[2], 3.0f * sqrtf(p.a) * 1.0001f + 1e-3f, 3.0f * sqrtf(p.c) * 1.0001f + 1e-3f, 0.f);
         depth[m] = p.z;
         radius[m] = p.r;
         rect[m] = make_int4(p.x0, p.y0, p.x1, p.y1);
@@ -260,6 +264,18 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
         g2d[3 * m] = zero;
         g2d[3 * m + 1] = zero;
         g2d[3 * m + 2] = zero;
+    }
+    // compacted list of Gaussians visible in some view (warp-aggregated append) so that the
+    // backward chain runs on full warps of visible Gaussians only
+    unsigned active = __activemask();
+    unsigned mask = __ballot_sync(active, any_vis);
+    if (mask) {
+        int lane = threadIdx.x & 31;
+        int leader = __ffs(mask) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&at<WsHeader>(ws, L.hdr)->vis_count, (uint32_t)__popc(mask));
+        base = __shfl_sync(active, base, leader);
+        if (any_vis) at<uint32_t>(ws, L.vis_list)[base + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)i;
     }
 }
 
@@ -270,29 +286,22 @@ template <int D>
 __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict__ P, int64_t n, int64_t ld,
                                                         const CamBatch cams, int V, Layout L, const char *ws,
                                                         float *__restrict__ G, float *__restrict__ gnorm) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     constexpr int NC = (D + 1) * (D + 1);
-    const int32_t *radius = at<const int32_t>(const_cast<char *>(ws), L.radius);
-    bool any = false;
-    for (int v = 0; v < V; v++) any |= radius[(int64_t)v * n + i] > 0;
-    if (!any) return;
-    const float4 *g2d = at<const float4>(const_cast<char *>(ws), L.grad2d);
+    char *w = const_cast<char *>(ws);
+    const uint32_t nvis = at<WsHeader>(w, L.hdr)->vis_count;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nvis) return;
+    const int64_t i = at<const uint32_t>(w, L.vis_list)[t];
+    const int32_t *radius = at<const int32_t>(w, L.radius);
+    float4 *g2d = at<float4>(w, L.grad2d);
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
-    float q[4] = {P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i]};
-    Cov3 cv = cov3_recipe(q[0], q[1], q[2], q[3], P[7 * ld + i], P[8 * ld + i], P[9 * ld + i]);
+    Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
+                          P[9 * ld + i]);
     float op = P[10 * ld + i];
     float sig = 1.0f / (1.0f + expf(-op));
-    float sh[3][NC];
-#pragma unroll
-    for (int l = 0; l < NC; l++)
-#pragma unroll
-        for (int ch = 0; ch < 3; ch++) sh[ch][l] = P[(11 + 3 * l + ch) * ld + i];
-    float gP[3] = {0.f, 0.f, 0.f}, gR[9], gs[3] = {0.f, 0.f, 0.f}, gop = 0.f, gsh[3][NC];
+    float gP[3] = {0.f, 0.f, 0.f}, gR[9], gs[3] = {0.f, 0.f, 0.f}, gop = 0.f;
 #pragma unroll
     for (int k = 0; k < 9; k++) gR[k] = 0.f;
-#pragma unroll
-    for (int l = 0; l < NC; l++) gsh[0][l] = gsh[1][l] = gsh[2][l] = 0.f;
     float norm_acc = 0.f;
     const float S3[9] = {cv.S00, cv.S01, cv.S02, cv.S01, cv.S11, cv.S12, cv.S02, cv.S12, cv.S22};
     for (int v = 0; v < V; v++) {
@@ -301,6 +310,8 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         const gs_camera &cam = cams.c[v];
         Proj p = project_recipe(cam, px, py, pz, cv, L.TX, L.TY);
         float4 ga = g2d[3 * m], gb = g2d[3 * m + 1], gc = g2d[3 * m + 2];
+        // consumed: reset so that a repeated backward on the same forward state starts from 0
+        g2d[3 * m] = g2d[3 * m + 1] = g2d[3 * m + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
         float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gsig = gb.y;
         float gcol[3] = {gb.z, gb.w, gc.x};
         norm_acc += sqrtf(gu * gu + gv * gv);
@@ -319,7 +330,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
             HT0[c] = H00 * p.T0[c] + H01 * p.T1[c];
             HT1[c] = H01 * p.T0[c] + H11 * p.T1[c];
         }
-        // dL/dSigma3 = T^T H T (symmetric), accumulated into dL/dM = 2 GS3 M later
+        // dL/dSigma3 = T^T H T (symmetric)
         float GS3[9];
 #pragma unroll
         for (int r = 0; r < 3; r++)
@@ -371,7 +382,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
                 gR[3 * r + j] += gm * cv.e[j];
             }
         gop += gsig;
-        // SH colour
+        // SH colour, one channel at a time (coefficients re-read through L1)
         float Cc[3];
         cam_centre(cam, Cc);
         float dx = px - Cc[0], dy = py - Cc[1], dz = pz - Cc[2];
@@ -380,17 +391,21 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         float Y[16];
         sh_basis<D>(dir[0], dir[1], dir[2], Y);
         float gdir[3] = {0.f, 0.f, 0.f};
-#pragma unroll
+#pragma unroll 1
         for (int ch = 0; ch < 3; ch++) {
+            float c[16];
             float acc = 0.5f;
 #pragma unroll
-            for (int l = 0; l < NC; l++) acc += sh[ch][l] * Y[l];
+            for (int l = 0; l < NC; l++) {
+                c[l] = P[(11 + 3 * l + ch) * ld + i];
+                acc += c[l] * Y[l];
+            }
             if (acc < 0.f) continue;  // clamped channel: zero gradient (R6)
 #pragma unroll
-            for (int l = 0; l < NC; l++) gsh[ch][l] += Y[l] * gcol[ch];
+            for (int l = 0; l < NC; l++) G[(11 + 3 * l + ch) * ld + i] += Y[l] * gcol[ch];
             if (D > 0) {
                 float gd[3];
-                sh_grad_dir<D>(dir[0], dir[1], dir[2], sh[ch], gd);
+                sh_grad_dir<D>(dir[0], dir[1], dir[2], c, gd);
                 gdir[0] += gcol[ch] * gd[0];
                 gdir[1] += gcol[ch] * gd[1];
                 gdir[2] += gcol[ch] * gd[2];
@@ -403,21 +418,21 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         }
     }
     // quaternion: dL/dq_hat from dL/dRq, then through the normalisation
-    float w = cv.qn[0], qx = cv.qn[1], qy = cv.qn[2], qz = cv.qn[3];
+    float w_ = cv.qn[0], qx = cv.qn[1], qy = cv.qn[2], qz = cv.qn[3];
     const float *g = gR;
     float gq0 = 2.f * (-qz * g[1] + qy * g[2] + qz * g[3] - qx * g[5] - qy * g[6] + qx * g[7]);
-    float gq1 = 2.f * (qy * g[1] + qz * g[2] + qy * g[3] - 2.f * qx * g[4] - w * g[5] + qz * g[6] + w * g[7] -
+    float gq1 = 2.f * (qy * g[1] + qz * g[2] + qy * g[3] - 2.f * qx * g[4] - w_ * g[5] + qz * g[6] + w_ * g[7] -
                        2.f * qx * g[8]);
-    float gq2 = 2.f * (-2.f * qy * g[0] + qx * g[1] + w * g[2] + qx * g[3] + qz * g[5] - w * g[6] + qz * g[7] -
+    float gq2 = 2.f * (-2.f * qy * g[0] + qx * g[1] + w_ * g[2] + qx * g[3] + qz * g[5] - w_ * g[6] + qz * g[7] -
                        2.f * qy * g[8]);
-    float gq3 = 2.f * (-2.f * qz * g[0] - w * g[1] + qx * g[2] + w * g[3] - 2.f * qz * g[4] + qy * g[5] + qx * g[6] +
+    float gq3 = 2.f * (-2.f * qz * g[0] - w_ * g[1] + qx * g[2] + w_ * g[3] - 2.f * qz * g[4] + qy * g[5] + qx * g[6] +
                        qy * g[7]);
-    float dotg = w * gq0 + qx * gq1 + qy * gq2 + qz * gq3;
+    float dotg = w_ * gq0 + qx * gq1 + qy * gq2 + qz * gq3;
     float in = cv.inv_norm;
     G[i] += gP[0];
     G[ld + i] += gP[1];
     G[2 * ld + i] += gP[2];
-    G[3 * ld + i] += (gq0 - w * dotg) * in;
+    G[3 * ld + i] += (gq0 - w_ * dotg) * in;
     G[4 * ld + i] += (gq1 - qx * dotg) * in;
     G[5 * ld + i] += (gq2 - qy * dotg) * in;
     G[6 * ld + i] += (gq3 - qz * dotg) * in;
@@ -425,10 +440,6 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     G[8 * ld + i] += gs[1];
     G[9 * ld + i] += gs[2];
     G[10 * ld + i] += sig * (1.f - sig) * gop;
-#pragma unroll
-    for (int l = 0; l < NC; l++)
-#pragma unroll
-        for (int ch = 0; ch < 3; ch++) G[(11 + 3 * l + ch) * ld + i] += gsh[ch][l];
     if (gnorm) gnorm[i] += norm_acc;
 }
 

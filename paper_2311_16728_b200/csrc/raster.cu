@@ -4,14 +4,21 @@
 // pixel over the depth-sorted list of its tile (SPEC.md:348 (4)): power = -1/2 d^T Q d with
 // d = pixel - mean2d (fp32 recipe order, bit-exact to the oracle), cut at power < -4.5
 // (Mahalanobis^2 > 9, R9) or power > 0; alpha = min(0.99, sigma e^power) (R7); skip alpha
-// < 1/255; stop the pixel when T (1 - alpha) < 1e-4 (R8).  One 256-thread CTA per
-// (view, 16x16 tile), one thread per pixel; Gaussian records are staged in shared memory in
-// batches of 256 and the CTA leaves as soon as every pixel of the tile has stopped.
+// < 1/255; stop the pixel when T (1 - alpha) < 1e-4 (R8).
+//
+// Layout: one 256-thread CTA per (view, 16x16 tile), one thread per pixel; each warp owns an
+// 8x4 pixel block (2 x 4 blocks per tile).  Gaussian records are staged in shared memory in
+// batches of 256; before evaluating a Gaussian a warp tests its 3-sigma bounding box (exact
+// ellipse extents 3 sqrt(Sigma2_xx), 3 sqrt(Sigma2_yy), padded so the test is conservative)
+// against the warp's block and skips it with one uniform branch -- no pixel result changes,
+// but most (warp, Gaussian) pairs of small splats are never evaluated.  The CTA leaves as
+// soon as every pixel of the tile has stopped.
 //
 // The backward replays each pixel's list back to front: dL/dc, dL/dalpha
 // = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  The nine
-// per-pixel gradients of a Gaussian are reduced over the warp with shuffles and added to the
-// per-(view, Gaussian) buffer with one vector red.global.add.v4.f32 triple per warp.
+// per-pixel gradients of a Gaussian are summed over the warp with a transposing butterfly
+// (9 + 5 shuffles instead of 45) and added to the per-(view, Gaussian) record by nine lanes
+// with one scalar red.global.add each.
 #include "gs_internal.cuh"
 
 namespace gsk {
@@ -33,30 +40,49 @@ __device__ __forceinline__ float pixel_power(float px, float py, const float4 g0
     return FMA(-MUL(g0.w, dx), dy, MUL(-0.5f, qf));
 }
 
+// thread -> pixel: warp w covers the 8x4 block (w & 1, w >> 1) of the tile
+__device__ __forceinline__ void pixel_of(int tid, int &lx, int &ly) {
+    int w = tid >> 5, l = tid & 31;
+    lx = (w & 1) * 8 + (l & 7);
+    ly = (w >> 1) * 4 + (l >> 3);
+}
+
+// warp-uniform: does the Gaussian's padded 3-sigma box miss the warp's 8x4 block?
+__device__ __forceinline__ bool warp_misses(const float4 g0, const float4 g2, float wx0, float wy0) {
+    return g0.x + g2.y < wx0 || g0.x - g2.y > wx0 + 7.f || g0.y + g2.z < wy0 || g0.y - g2.z > wy0 + 3.f;
+}
+
 __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restrict__ ranges,
                                                           const uint32_t *__restrict__ vals,
                                                           const float4 *__restrict__ rec0,
                                                           const float4 *__restrict__ rec1,
-                                                          const float *__restrict__ rec2, int64_t n, int W, int H,
+                                                          const float4 *__restrict__ rec2, int64_t n, int W, int H,
                                                           int TX, int tiles, float bg0, float bg1, float bg2,
                                                           float *__restrict__ out_rgb, float *__restrict__ out_T,
                                                           float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib) {
     __shared__ float4 s0[BLOCK_PIX];
     __shared__ float4 s1[BLOCK_PIX];
-    __shared__ float s2[BLOCK_PIX];
+    __shared__ float4 s2[BLOCK_PIX];
+    __shared__ uint8_t wl[BLOCK_PIX / 32][BLOCK_PIX];
     const int view = blockIdx.z;
     const int tile = blockIdx.y * TX + blockIdx.x;
     const int tid = threadIdx.x;
-    const int px = blockIdx.x * TILE + (tid & (TILE - 1));
-    const int py = blockIdx.y * TILE + (tid >> 4);
+    int lx, ly;
+    pixel_of(tid, lx, ly);
+    const int px = blockIdx.x * TILE + lx;
+    const int py = blockIdx.y * TILE + ly;
+    const float wx0 = (float)(blockIdx.x * TILE + ((tid >> 5) & 1) * 8);
+    const float wy0 = (float)(blockIdx.y * TILE + (tid >> 6) * 4);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const int todo_all = (int)(range.y - range.x);
     const float fx = (float)px, fy = (float)py;
     const int64_t vbase = (int64_t)view * n;
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    uint32_t contributor = 0, last = 0;
+    uint32_t last = 0;
     bool done = !inside;
+    const int warp = tid >> 5, lane = tid & 31;
+    const unsigned lt = (1u << lane) - 1u;
     for (int b0 = 0; b0 < todo_all; b0 += BLOCK_PIX) {
         if (__syncthreads_count(done) == BLOCK_PIX) break;
         int idx = b0 + tid;
@@ -67,14 +93,28 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
             s2[tid] = rec2[m];
         }
         __syncthreads();
-        int cnt = min(BLOCK_PIX, todo_all - b0);
-        for (int j = 0; j < cnt && !done; j++) {
-            contributor++;
+        const int cnt = min(BLOCK_PIX, todo_all - b0);
+        // phase 1 (parallel over the batch): ordered list of the Gaussians whose padded
+        // 3-sigma box meets this warp's 8x4 block
+        int nsel = 0;
+        for (int k = 0; k < cnt; k += 32) {
+            int j = k + lane;
+            bool hit = j < cnt && !warp_misses(s0[j], s2[j], wx0, wy0);
+            unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
+            nsel += __popc(b);
+        }
+        __syncwarp();
+        // phase 2 (sequential per pixel): composite the warp's list front to back
+        for (int t = 0; t < nsel; t++) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const int j = wl[warp][t];
             float4 g0 = s0[j];
             float4 g1 = s1[j];
+            float4 g2 = s2[j];
             float dx, dy;
             float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
-            if (power > 0.0f || power < POWER_CUT) continue;
+            if (done || power > 0.0f || power < POWER_CUT) continue;
             float alpha = fminf(ALPHA_MAX, g1.y * __expf(power));
             if (alpha < ALPHA_MIN) continue;
             float test_T = T * (1.0f - alpha);
@@ -85,9 +125,9 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
             float w = alpha * T;
             c0 += g1.z * w;
             c1 += g1.w * w;
-            c2 += s2[j] * w;
+            c2 += g2.x * w;
             T = test_T;
-            last = contributor;
+            last = (uint32_t)(b0 + j + 1);  // 1-based list position of the last composited
         }
     }
     if (inside) {
@@ -109,16 +149,38 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-__device__ __forceinline__ void red_add_v4(float4 *addr, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
+// Warp sum of eight values with a transposing butterfly: at offsets 16, 8, 4 every lane keeps
+// half of its values and receives the partner's other half (4 + 2 + 1 shuffles), then two
+// plain xor steps finish the sum.  Lane l ends with the total of value index
+// ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); 9 shuffles instead of 40.
+__device__ __forceinline__ float warp_sum8_transposed(float a[8], int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    float h[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        float send = b4 ? a[k] : a[k + 4];
+        float keep = b4 ? a[k + 4] : a[k];
+        h[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float q[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        float send = b3 ? h[k] : h[k + 2];
+        float keep = b3 ? h[k + 2] : h[k];
+        q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float send = b2 ? q[0] : q[1];
+    float r = (b2 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
 }
 
 __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restrict__ ranges,
                                                           const uint32_t *__restrict__ vals,
                                                           const float4 *__restrict__ rec0,
                                                           const float4 *__restrict__ rec1,
-                                                          const float *__restrict__ rec2, int64_t n, int W, int H,
+                                                          const float4 *__restrict__ rec2, int64_t n, int W, int H,
                                                           int TX, int tiles, float bg0, float bg1, float bg2,
                                                           const float *__restrict__ dL_drgb,
                                                           const float *__restrict__ T_keep,
@@ -126,14 +188,19 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                                                           float4 *__restrict__ g2d) {
     __shared__ float4 s0[BLOCK_PIX];
     __shared__ float4 s1[BLOCK_PIX];
-    __shared__ float s2[BLOCK_PIX];
+    __shared__ float4 s2[BLOCK_PIX];
     __shared__ uint32_t sid[BLOCK_PIX];
+    __shared__ uint8_t wl[BLOCK_PIX / 32][BLOCK_PIX];
     __shared__ uint32_t s_maxlast;
     const int view = blockIdx.z;
     const int tile = blockIdx.y * TX + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int px = blockIdx.x * TILE + (tid & (TILE - 1));
-    const int py = blockIdx.y * TILE + (tid >> 4);
+    int lx, ly;
+    pixel_of(tid, lx, ly);
+    const int px = blockIdx.x * TILE + lx;
+    const int py = blockIdx.y * TILE + ly;
+    const float wx0 = (float)(blockIdx.x * TILE + ((tid >> 5) & 1) * 8);
+    const float wy0 = (float)(blockIdx.y * TILE + (tid >> 6) * 4);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const float fx = (float)px, fy = (float)py;
@@ -152,29 +219,48 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
     }
     if (tid == 0) s_maxlast = 0;
     __syncthreads();
-    atomicMax(&s_maxlast, last);
+    // the warp's own furthest composited position bounds its work; the CTA's bounds the batches
+    uint32_t wlast = last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (lane == 0) atomicMax(&s_maxlast, wlast);
     __syncthreads();
-    // only the list prefix that some pixel composited matters
     const int todo_all = (int)s_maxlast;
     float acc0 = bg0, acc1 = bg1, acc2 = bg2;
-    // process positions todo_all-1 .. 0 (0-based within the tile range), batches from the back
+    // process positions todo_all .. 1 (1-based within the tile range), batches from the back
     for (int b_end = todo_all; b_end > 0; b_end -= BLOCK_PIX) {
         int b_start = max(0, b_end - BLOCK_PIX);
         int cnt = b_end - b_start;
         __syncthreads();
         if (tid < cnt) {
-            int pos = b_end - 1 - tid;  // s[tid] holds position b_end-1-tid (back to front)
+            int pos = b_end - 1 - tid;  // s[tid] holds 0-based position b_end-1-tid (back to front)
             uint32_t gi = vals[range.x + pos];
             int64_t m = vbase + gi;
-            sid[tid] = (uint32_t)gi;
+            sid[tid] = gi;
             s0[tid] = rec0[m];
             s1[tid] = rec1[m];
             s2[tid] = rec2[m];
         }
         __syncthreads();
-        for (int j = 0; j < cnt; j++) {
-            uint32_t position = (uint32_t)(b_end - j);  // 1-based position in the tile list
+        // phase 1: ordered (back to front) list of the batch entries this warp must replay --
+        // at or before its furthest composited position and with a box meeting its block
+        const int warp = tid >> 5;
+        const unsigned lt = (1u << lane) - 1u;
+        const int j0 = (uint32_t)b_end > wlast ? (int)((uint32_t)b_end - wlast) : 0;
+        int nsel = 0;
+        for (int k = 0; k < cnt; k += 32) {
+            int j = k + lane;
+            bool hit = j < cnt && j >= j0 && !warp_misses(s0[j], s2[j], wx0, wy0);
+            unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
+            nsel += __popc(b);
+        }
+        __syncwarp();
+        for (int t = 0; t < nsel; t++) {
+            const int j = wl[warp][t];
+            const uint32_t position = (uint32_t)(b_end - j);  // 1-based position in the tile list
             float4 g0 = s0[j];
+            float4 g2 = s2[j];
             float4 g1 = s1[j];
             float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
             float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
@@ -193,7 +279,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                         dLdr = g_0 * w;
                         dLdg = g_1 * w;
                         dLdb = g_2 * w;
-                        float cr = g1.z, cg = g1.w, cb = s2[j];
+                        float cr = g1.z, cg = g1.w, cb = g2.x;
                         float dLda = T * (g_0 * (cr - acc0) + g_1 * (cg - acc1) + g_2 * (cb - acc2));
                         acc0 = alpha * cr + (1.f - alpha) * acc0;
                         acc1 = alpha * cg + (1.f - alpha) * acc1;
@@ -212,21 +298,14 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                 }
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                dLdu = warp_sum(dLdu);
-                dLdv = warp_sum(dLdv);
-                dLdA = warp_sum(dLdA);
-                dLdB = warp_sum(dLdB);
-                dLdC = warp_sum(dLdC);
-                dLdsig = warp_sum(dLdsig);
-                dLdr = warp_sum(dLdr);
-                dLdg = warp_sum(dLdg);
-                dLdb = warp_sum(dLdb);
-                if (lane == 0) {
-                    float4 *dst = g2d + 3 * (vbase + sid[j]);
-                    red_add_v4(dst, dLdu, dLdv, dLdA, dLdB);
-                    red_add_v4(dst + 1, dLdC, dLdsig, dLdr, dLdg);
-                    red_add_v4(dst + 2, dLdb, 0.f, 0.f, 0.f);
-                }
+                // per-(view, Gaussian) record: [u, v, A, B | C, sigma, r, g | b, -, -, -]
+                float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
+                float mine = warp_sum8_transposed(vals8, lane);
+                float bsum = warp_sum(dLdb);
+                float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + sid[j]));
+                if ((lane & 3) == 0)
+                    atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
+                if (lane == 1) atomicAdd(dst + 8, bsum);
             }
         }
     }
@@ -236,7 +315,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
                               cudaStream_t s) {
     dim3 grid(L.TX, L.TY, L.V);
     k_raster_fwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
-                                            at<float4>(ws, L.rec1), at<float>(ws, L.rec2), L.n, L.W, L.H, L.TX,
+                                            at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
                                             L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
                                             at<uint32_t>(ws, L.ncontrib));
     return cudaGetLastError();
@@ -245,7 +324,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     dim3 grid(L.TX, L.TY, L.V);
     k_raster_bwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
-                                            at<float4>(ws, L.rec1), at<float>(ws, L.rec2), L.n, L.W, L.H, L.TX,
+                                            at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
                                             L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
                                             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
     return cudaGetLastError();

@@ -120,13 +120,13 @@ __global__ void __launch_bounds__(256) k_duplicate(const int4 *__restrict__ rect
                                                    WsHeader *hdr) {
     int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
+    if ((int64_t)hdr->P > cap) {  // capacity overflow: flag it, emit nothing
+        if (m == 0) atomicOr(&hdr->flags, 1u);
+        return;
+    }
     uint32_t cnt = tt[m];
     if (cnt == 0) return;
     int64_t o = off[m];
-    if (o + cnt > cap) {
-        atomicOr(&hdr->flags, 1u);
-        return;
-    }
     int64_t view = m / n;
     uint32_t gi = (uint32_t)(m - view * n);
     int4 r = rect[m];
@@ -149,9 +149,11 @@ cudaError_t launch_duplicate(const Layout &L, void *ws, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------ radix sort
+// Pair count seen by the sort / ranges / raster: 0 after a capacity overflow (the outputs of
+// that call are invalid and flagged; nothing reads or writes beyond the buffers).
 __device__ __forceinline__ uint32_t count_of(const uint32_t *count, int64_t cap) {
     uint32_t c = *count;
-    return c > cap ? (uint32_t)cap : c;
+    return c > cap ? 0u : c;
 }
 
 // One pass over all keys: histogram of every digit; the last CTA scans them and decides which
