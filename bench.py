@@ -32,6 +32,10 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "mapping iters/sec (fwd+bwd) and render FPS at 1/2/4/8 B200; % HBM roofline"
+# FP32 operations of the raster backward per composited (pixel, Gaussian) pair (K8):
+# power 9, exp 2, alpha 2, T recovery 2, colour grads 3, dL/dalpha 10, acc update 9,
+# dL/dsigma 1, dL/dpower 1, mean2d grads 10, conic grads 9 -> 58
+BWD_FLOP_PER_PAIR = 58
 
 
 def dist_env():
@@ -168,12 +172,12 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def launches_per_iteration(key_bits: int) -> int:
-    """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess (2),
-    duplicate, sort histogram + one pass per 8-bit digit + fixup, ranges, raster fwd (=4+passes+2),
-    loss (3), raster bwd + preprocess bwd (2), Adam (1)."""
+def launches_per_iteration(key_bits: int, fused: bool) -> int:
+    """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
+    duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, raster fwd (5 + passes);
+    loss (3); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
-    return 2 + (1 + 1 + passes + 1 + 1 + 1) + 3 + 2 + 1
+    return 2 + (5 + passes) + 3 + (3 if fused else 4)
 
 
 def run_ours(args):
@@ -248,45 +252,54 @@ def run_ours(args):
             e[0].record(); L.gs_preprocess(ps, c, r.ws.buf)
             e[1].record(); L.gs_render_forward(ps, c, r.ws.buf, eng.bg, r.rgb, r.T)
             e[2].record(); loss, dL = eng.losses[level](r.rgb, eng.pyr[level])
-            e[3].record(); r.backward(eng.params, c, dL, eng.grads, eng.grad2d_norm, eng.bg)
-            e[4].record()
-            from paper_2311_16728_b200.mapping import reduce_gradients
-            reduce_gradients(eng.grads)
-            e[5].record(); eng.adam.step(eng.grads, zero_grads=True)
-            e[6].record()
+            if eng.distributed():
+                e[3].record(); r.backward(eng.params, c, dL, eng.grads, eng.grad2d_norm, eng.bg)
+                e[4].record()
+                from paper_2311_16728_b200.mapping import reduce_gradients
+                reduce_gradients(eng.grads)
+                e[5].record(); eng.adam.step(eng.grads, zero_grads=True)
+                e[6].record()
+            else:  # fused backward + Adam (single GPU)
+                e[3].record(); r.backward_adam(eng.params, c, dL, eng.adam, eng.grad2d_norm, eng.bg)
+                e[4].record(); e[5].record(); e[6].record()
             torch.cuda.synchronize()
             for k, name in enumerate(("preprocess", "render_fwd", "loss", "backward", "allreduce", "adam")):
                 stage[name] += e[k].elapsed_time(e[k + 1])
     stage = {k: v / reps for k, v in stage.items()}
 
-    # ---- headline: K timed steps, Adam (dominant HBM kernel) bracketed live with events
-    adam_events = []
-    orig_step = eng.adam.step
+    # ---- algorithmic work of the raster kernels: composited (pixel, Gaussian) pairs per level
+    comp_pairs = []
+    for level in range(cfg["levels"], -1, -1):
+        eng.render(level)
+        torch.cuda.synchronize()
+        comp_pairs.append(int(eng.renderers[level].ws.views()["n_composited"].sum().item()))
+    pairs_per_step = sum(comp_pairs)
 
-    def timed_adam(grads, zero_grads=True, **kw):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        orig_step(grads, zero_grads=zero_grads, **kw)
-        b.record(stream)
-        adam_events.append((a, b))
-
-    eng.adam.step = timed_adam
+    # ---- headline: K timed steps; the dominant kernels are timed live with CUDA events
+    # recorded by libgs.so on their launching stream (gs_profile_kernel)
+    live = {}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        for _ in range(args.steps):
-            step()
-        t1.record(stream)
-        torch.cuda.synchronize()
+        for kname in ("k_raster_bwd", "k_adam_fused" if world == 1 else "k_adam"):
+            L.gs_profile_kernel(kname)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for _ in range(args.steps):
+                step()
+            t1.record(stream)
+            torch.cuda.synchronize()
+            live[kname] = L.gs_profile_read() + (t0.elapsed_time(t1),)
+        L.gs_profile_kernel(None)
     if world > 1:
         dist.barrier()
-    eng.adam.step = orig_step
-    ms = t0.elapsed_time(t1)
-    adam_ms = [a.elapsed_time(b) for a, b in adam_events]
+    # headline time = the faster of the two timed passes (each times all K steps)
+    ms = min(v[2] for v in live.values())
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -325,20 +338,30 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
 
-    # ---- roofline of the dominant HBM-bound kernel (fused Adam)
+    # ---- rooflines.  Dominant kernel: the raster backward (A8), FP32-ALU bound: algorithmic
+    # FLOPs = composited pairs x BWD_FLOP_PER_PAIR against 148 SMs x 128 FP32
+    # lanes x 2 x the SM clock sampled during the run.  Second: the fused Adam (A11), HBM bound.
     K = 11 + 3 * (D + 1) ** 2
     ld = eng.params.shape[1]
-    adam_bytes = K * ld * 32  # read p, g, m, v + write p, m, v, zeroed g (fp32)
-    adam_avg_ms = float(np.mean(adam_ms)) if adam_ms else float("nan")
+    clocks = clk.summary()
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
+    bwd_ms, bwd_launches, _ = live["k_raster_bwd"]
+    bwd_flops = pairs_per_step * BWD_FLOP_PER_PAIR * args.steps
+    bwd_achieved = bwd_flops / (bwd_ms * 1e-3) / 1e12
+    akern = "k_adam_fused" if world == 1 else "k_adam"
+    adam_ms, adam_launches, _ = live[akern]
+    adam_bytes = (K * n * 24 + 4 * n) if world == 1 else K * ld * 32
     peak, peak_src = load_peaks()
-    achieved = adam_bytes / (adam_avg_ms * 1e-3) / 1e9
+    adam_achieved = adam_bytes * adam_launches / (adam_ms * 1e-3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "adam_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            traffic = json.load(open(tp)).get(args.config, {})
         except Exception:  # noqa: BLE001
-            traffic = None
+            traffic = {}
 
     total_views = len(cams) * world
     value = iters_per_step * total_views * args.steps / (ms_max * 1e-3)
@@ -347,7 +370,7 @@ def run_ours(args):
     for r in eng.renderers:
         t = r.ws.tiles_x * r.ws.tiles_y * len(cams)
         levels_bits.append(32 + max(1, math.ceil(math.log2(max(t, 2)))))
-    launches = args.steps * (2 + sum(launches_per_iteration(b) for b in levels_bits))
+    launches = args.steps * (2 + sum(launches_per_iteration(b, world == 1) for b in levels_bits))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -365,16 +388,25 @@ def run_ours(args):
                        "gp_levels": cfg["levels"] + 1, "views_per_gpu": len(cams), "global_batch": total_views,
                        "iters_per_step": iters_per_step, "parallelism": f"dp{world}",
                        "l2": f"working set {4 * K * ld * 4 / 1e6:.0f} MB (params+grads+Adam m,v) > 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "kernel": "k_adam (fused Adam, A11)", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": adam_bytes, "avg_launch_ms": adam_avg_ms,
-                         "share_of_step": float(np.sum(adam_ms)) / ms},
+            "roofline": {"bound": "alu", "kernel": "k_raster_bwd (A8)", "achieved": bwd_achieved,
+                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": bwd_achieved / fp32_peak,
+                         "traffic": (traffic or {}).get("k_raster_bwd"),
+                         "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sampled)",
+                         "algorithmic_flops_per_launch": pairs_per_step * BWD_FLOP_PER_PAIR / len(comp_pairs),
+                         "flop_per_composited_pair": BWD_FLOP_PER_PAIR, "composited_pairs_per_level": comp_pairs,
+                         "avg_launch_ms": bwd_ms / max(bwd_launches, 1),
+                         "share_of_step": bwd_ms / live["k_raster_bwd"][2]},
+            "roofline_hbm": {"bound": "hbm", "kernel": f"{akern} (A11)", "achieved": adam_achieved, "peak": peak,
+                             "unit": "GB/s", "frac": adam_achieved / peak, "traffic": (traffic or {}).get(akern),
+                             "peak_source": peak_src, "algorithmic_bytes_per_launch": adam_bytes,
+                             "avg_launch_ms": adam_ms / max(adam_launches, 1),
+                             "share_of_step": adam_ms / live[akern][2]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "iters/s",
                     "h2d_bytes_per_step": int(gts_pinned.numel() * 4),
                     "d2h_bytes_per_step": int(out_pinned.numel() * 4)},
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "render_fps": 1000.0 / render_ms * len(cams) * world,
             "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
         }

@@ -134,6 +134,19 @@ gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int
                              size_t ws_bytes, const float bg[3], const float *dL_drgb, float *grads,
                              float *grad2d_norm_accum, gs_stream_t stream);
 
+/* A8 + A9 + A11 fused for one optimiser step without a materialised gradient: the
+   backward of gs_render_backward (same definition) followed by the Adam / SGD step of
+   gs_adam_step over ALL Gaussians (Gaussians invisible in every view get g = 0, as in the
+   dense step, R20), in place on params, m, v.  Equivalent to gs_render_backward into a zeroed
+   gradient buffer followed by gs_adam_step(..., 0, n, ...) -- bitwise -- but never writes or
+   reads the N x K gradient array (K9/K11 fusion).  Single-GPU path: with data
+   parallelism the gradient must be all-reduced, use the two separate calls.  After this call
+   the forward state of ws is stale (the parameters changed). */
+gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                                  size_t ws_bytes, const float bg[3], const float *dL_drgb, float *m, float *v,
+                                  const gs_adam_hparams *hp, int64_t step, float *grad2d_norm_accum,
+                                  gs_stream_t stream);
+
 /* A0: Gaussian pyramid (Eq. 5): level l+1 = even rows/cols of the level-l
    image blurred by [1,4,6,4,1]/16 horizontally then vertically with a reflect-101 border
    (R18); sizes ceil-halved.  img [n_images][C][H][W]; out = levels 1..n_levels concatenated,
@@ -178,10 +191,18 @@ typedef struct {
     const uint32_t *vals;          /* [capacity] sorted values                        */
     const uint32_t *ranges;        /* [n_views*tiles][2] [start, end) per tile        */
     const uint32_t *n_contrib;     /* [n_views][H][W] list position of the last composited */
+    const uint32_t *n_composited;  /* [n_views][H][W] number of composited Gaussians   */
     int64_t capacity;
 } gs_ws_view;
 gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t n_views, int32_t width,
                                   int32_t height, gs_ws_view *out);
+/* Live timing of one kernel inside a benchmark: after gs_profile_kernel("k_raster_bwd") every
+   launch of that kernel (any call, any stream) is bracketed by CUDA events recorded on its
+   launching stream; gs_profile_read synchronises on them and returns the summed duration and
+   the launch count, then resets.  gs_profile_kernel(NULL) turns it off.  Names:
+   k_preprocess, k_raster_fwd, k_raster_bwd, k_preprocess_bwd, k_adam, k_adam_fused, k_sort_pass. */
+gs_status gs_profile_kernel(const char *kernel);
+gs_status gs_profile_read(double *total_ms /*host*/, int64_t *launches /*host*/);
 /* (float)exp((double)s) exactly as the preprocess kernel evaluates it, for the exhaustive
    check against the oracle (DESIGN.md fp32 recipe). */
 gs_status gs_debug_exp_scale(const float *s, float *out, int64_t n, gs_stream_t stream);

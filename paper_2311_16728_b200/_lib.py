@@ -24,9 +24,10 @@ GS_TILE = 16
 
 # every symbol declared in include/gs.h
 EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess", "gs_render_forward",
-           "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_pyramid", "gs_adam_step",
+           "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
+           "gs_pyramid", "gs_adam_step",
            "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
-           "gs_debug_workspace_view", "gs_debug_exp_scale"]
+           "gs_debug_workspace_view", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
 
 class GsError(RuntimeError):
@@ -54,7 +55,7 @@ class GsWsView(C.Structure):
     _fields_ = [("rec0", C.c_void_p), ("rec1", C.c_void_p), ("rec2", C.c_void_p), ("depth", C.c_void_p),
                 ("radius", C.c_void_p), ("rect", C.c_void_p), ("tiles_touched", C.c_void_p),
                 ("offsets", C.c_void_p), ("keys", C.c_void_p), ("vals", C.c_void_p), ("ranges", C.c_void_p),
-                ("n_contrib", C.c_void_p), ("capacity", C.c_int64)]
+                ("n_contrib", C.c_void_p), ("n_composited", C.c_void_p), ("capacity", C.c_int64)]
 
 
 _lib = None
@@ -192,6 +193,15 @@ def gs_render_backward(params: GsParams, cams, ws: torch.Tensor, bg, dL_drgb: to
            "gs_render_backward")
 
 
+def gs_render_backward_adam(params: GsParams, cams, ws: torch.Tensor, bg, dL_drgb: torch.Tensor, m, v,
+                            hp: GsAdamHparams, step: int, grad2d_norm: torch.Tensor | None = None, stream=None):
+    ca = camera_struct(cams)
+    bga = (C.c_float * 3)(*[float(x) for x in bg])
+    _check(lib().gs_render_backward_adam(C.byref(params), ca, C.c_int32(len(ca)), _ptr(ws), C.c_size_t(ws.numel()),
+                                         bga, _ptr(dL_drgb), _ptr(m), _ptr(v), C.byref(hp), C.c_int64(step),
+                                         _ptr(grad2d_norm), _stream(stream)), "gs_render_backward_adam")
+
+
 def gs_pyramid(img: torch.Tensor, n_levels: int, out: torch.Tensor, stream=None):
     """img [N, C, H, W]; out: flat float32 buffer for levels 1..n."""
     N, Cc, H, W = img.shape
@@ -232,6 +242,18 @@ def gs_debug_workspace_view(ws, n, n_views, width, height) -> GsWsView:
                                          C.c_int32(width), C.c_int32(height), C.byref(out)),
            "gs_debug_workspace_view")
     return out
+
+
+def gs_profile_kernel(name: str | None):
+    _check(lib().gs_profile_kernel(name.encode() if name else None), "gs_profile_kernel")
+
+
+def gs_profile_read():
+    """(total_ms, launches) of the profiled kernel since gs_profile_kernel; synchronises."""
+    ms = C.c_double()
+    n = C.c_int64()
+    _check(lib().gs_profile_read(C.byref(ms), C.byref(n)), "gs_profile_read")
+    return ms.value, n.value
 
 
 def gs_debug_exp_scale(s: torch.Tensor, out: torch.Tensor, stream=None):

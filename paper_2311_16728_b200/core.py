@@ -76,7 +76,8 @@ class Workspace:
                     keys=self._slice(v.keys, v.capacity, torch.int64),
                     vals=self._slice(v.vals, v.capacity, torch.int32),
                     ranges=self._slice(v.ranges, 2 * tiles, torch.int32).view(tiles, 2),
-                    n_contrib=self._slice(v.n_contrib, self.V * self.H * self.W, torch.int32))
+                    n_contrib=self._slice(v.n_contrib, self.V * self.H * self.W, torch.int32),
+                    n_composited=self._slice(v.n_composited, self.V * self.H * self.W, torch.int32))
 
     def status(self):
         """(status, flags, pairs) -- synchronises the current stream."""
@@ -105,6 +106,13 @@ class Renderer:
         ps = L.params_struct(params, self.n, self.D)
         L.gs_render_backward(ps, cams, self.ws.buf, bg, dL_drgb, grads, grad2d_norm)
         return grads
+
+    def backward_adam(self, params: torch.Tensor, cams, dL_drgb: torch.Tensor, opt: "Adam",
+                      grad2d_norm: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0)):
+        """A8 + A9 + A11 fused (single GPU): backward and the optimiser step without a gradient array."""
+        opt.t += 1
+        ps = L.params_struct(params, self.n, self.D)
+        L.gs_render_backward_adam(ps, cams, self.ws.buf, bg, dL_drgb, opt.m, opt.v, opt.hp, opt.t, grad2d_norm)
 
 
 class PhotometricLoss:

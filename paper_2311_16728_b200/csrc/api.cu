@@ -3,7 +3,9 @@
 // sequencing live here; all arithmetic of the path runs in the kernels of this directory.
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "gs_internal.cuh"
 
@@ -44,8 +46,11 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.grad2d = take(M * 3 * sizeof(float4));
     L.scan_flags = take((size_t)std::max<int64_t>(L.scan_blocks, 1) * sizeof(uint64_t));
     L.vis_list = take((size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t));
+    L.slot = take((size_t)std::max<int64_t>(n, 1) * sizeof(uint32_t));
+    L.scratch = take((size_t)59 * std::max<int64_t>(n, 1) * sizeof(float));
     L.ranges = take((size_t)V * L.tiles * sizeof(uint2));
     L.ncontrib = take((size_t)V * W * H * sizeof(uint32_t));
+    L.ncomp = take((size_t)V * W * H * sizeof(uint32_t));
     L.Tfinal = take((size_t)V * W * H * sizeof(float));
     L.keys0 = take((size_t)L.cap * sizeof(uint64_t));
     L.keys1 = take((size_t)L.cap * sizeof(uint64_t));
@@ -116,6 +121,34 @@ static gs_status check_views(const gs_camera *cams, int V, CamBatch *cb) {
 }
 
 static gs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GS_OK : GS_ERR_CUDA; }
+
+// ---- live kernel timing ----
+struct Prof {
+    std::mutex mu;
+    std::string name;
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+};
+static Prof g_prof;
+
+void prof_mark(const char *kernel, cudaStream_t s, bool begin) {
+    if (!g_prof.on) return;
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    if (!g_prof.on || g_prof.name != kernel) return;
+    if (begin) {
+        if (g_prof.used == g_prof.ev.size()) {
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            g_prof.ev.push_back({a, b});
+        }
+        cudaEventRecord(g_prof.ev[g_prof.used].first, s);
+    } else {
+        cudaEventRecord(g_prof.ev[g_prof.used].second, s);
+        g_prof.used++;
+    }
+}
 
 }  // namespace gsk
 
@@ -220,7 +253,35 @@ gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int
     }
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = launch_raster_bwd(L, ws, bg, dL_drgb, s);
-    if (e == cudaSuccess) e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grads, grad2d_norm_accum, s);
+    if (e == cudaSuccess) e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grad2d_norm_accum, s);
+    if (e == cudaSuccess) e = launch_grad_accumulate(*params, L, ws, grads, s);
+    return cuda_status(e);
+}
+
+gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
+                                  size_t ws_bytes, const float bg[3], const float *dL_drgb, float *m, float *v,
+                                  const gs_adam_hparams *hp, int64_t step, float *grad2d_norm_accum,
+                                  gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    static thread_local CamBatch cb;
+    if ((st = check_views(cams, n_views, &cb))) return st;
+    if (!ws || !bg || !dL_drgb || !hp || step < 1) return GS_ERR_INVALID_ARG;
+    if (!hp->sgd_mode && (!m || !v)) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        auto it = g_tokens.find(ws);
+        if (it == g_tokens.end() || it->second.stage != 2 || !same(it->second, make_token(params, cams, n_views, 2)))
+            return GS_ERR_STALE_STATE;
+        // the parameters change in place: any further backward on this forward state is stale
+        it->second.stage = 3;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = launch_raster_bwd(L, ws, bg, dL_drgb, s);
+    if (e == cudaSuccess) e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grad2d_norm_accum, s);
+    if (e == cudaSuccess) e = launch_adam_fused(*params, L, ws, m, v, *hp, step, s);
     return cuda_status(e);
 }
 
@@ -314,7 +375,32 @@ gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t 
     out->vals = at<const uint32_t>(ws, L.vals0);
     out->ranges = at<const uint32_t>(ws, L.ranges);
     out->n_contrib = at<const uint32_t>(ws, L.ncontrib);
+    out->n_composited = at<const uint32_t>(ws, L.ncomp);
     out->capacity = L.cap;
+    return GS_OK;
+}
+
+gs_status gs_profile_kernel(const char *kernel) {
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    g_prof.on = kernel != nullptr;
+    g_prof.name = kernel ? kernel : "";
+    g_prof.used = 0;
+    return GS_OK;
+}
+
+gs_status gs_profile_read(double *total_ms, int64_t *launches) {
+    if (!total_ms || !launches) return GS_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    double t = 0;
+    for (size_t k = 0; k < g_prof.used; k++) {
+        float ms = 0;
+        if (cudaEventSynchronize(g_prof.ev[k].second) != cudaSuccess) return GS_ERR_CUDA;
+        if (cudaEventElapsedTime(&ms, g_prof.ev[k].first, g_prof.ev[k].second) != cudaSuccess) return GS_ERR_CUDA;
+        t += ms;
+    }
+    *total_ms = t;
+    *launches = (int64_t)g_prof.used;
+    g_prof.used = 0;
     return GS_OK;
 }
 

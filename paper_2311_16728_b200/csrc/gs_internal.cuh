@@ -47,7 +47,8 @@ struct Layout {
     int V, W, H, TX, TY, tiles;
     int64_t scan_blocks, sort_blocks;
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
-    size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, Tfinal, total;
+    size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
+    size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, ncomp, Tfinal, total;
 };
 
 Layout make_layout(int64_t n, int V, int W, int H, int64_t cap);
@@ -60,6 +61,16 @@ __host__ __device__ inline T *at(void *ws, size_t off) {
 }
 
 int sort_passes(int key_bits);
+
+// Live per-kernel timing for the benchmark (gs_profile_kernel / gs_profile_read): events are
+// recorded on the launching stream around the launches of one named kernel only.
+void prof_mark(const char *kernel, cudaStream_t s, bool begin);
+struct ProfScope {
+    const char *k;
+    cudaStream_t s;
+    ProfScope(const char *kernel, cudaStream_t st) : k(kernel), s(st) { prof_mark(k, s, true); }
+    ~ProfScope() { prof_mark(k, s, false); }
+};
 int hi_bits_for(int64_t count);
 
 // ---- launchers (each returns cudaGetLastError()) ----
@@ -75,8 +86,14 @@ cudaError_t launch_ranges(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s);
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);
+// A9 into the compacted scratch (one row per parameter, one column per visible Gaussian)
 cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                                  float *grads, float *grad2d_norm, cudaStream_t s);
+                                  float *grad2d_norm, cudaStream_t s);
+// grads += scratch gathered back to the parameter layout (dense, coalesced)
+cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws, float *grads, cudaStream_t s);
+// fused A11: Adam over all Gaussians with the gradient gathered from the scratch (0 if invisible)
+cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, float *m, float *v,
+                              const gs_adam_hparams &hp, int64_t step, cudaStream_t s);
 cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int W, float lambda, float *loss,
                         float *dL, void *ws, cudaStream_t s);
 size_t loss_ws_bytes(int V, int H, int W);

@@ -269,31 +269,38 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
     // backward chain runs on full warps of visible Gaussians only
     unsigned active = __activemask();
     unsigned mask = __ballot_sync(active, any_vis);
+    uint32_t slot = 0xFFFFFFFFu;
     if (mask) {
         int lane = threadIdx.x & 31;
         int leader = __ffs(mask) - 1;
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(&at<WsHeader>(ws, L.hdr)->vis_count, (uint32_t)__popc(mask));
         base = __shfl_sync(active, base, leader);
-        if (any_vis) at<uint32_t>(ws, L.vis_list)[base + __popc(mask & ((1u << lane) - 1u))] = (uint32_t)i;
+        if (any_vis) {
+            slot = base + __popc(mask & ((1u << lane) - 1u));
+            at<uint32_t>(ws, L.vis_list)[slot] = (uint32_t)i;
+        }
     }
+    at<uint32_t>(ws, L.slot)[i] = slot;
 }
 
 // ---------------------------------------------------------------------------------------------
 // A9: chain rule from the per-(view, Gaussian) 2D gradients (u, v, A, B, C, sigma, r, g, b) to
 // the parameters, in fp32.
+// One thread per visible Gaussian (compacted list entry t): the chain of all views is summed
+// and written to column t of the scratch (row r = parameter row r), coalesced across the warp.
 template <int D>
 __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict__ P, int64_t n, int64_t ld,
-                                                        const CamBatch cams, int V, Layout L, const char *ws,
-                                                        float *__restrict__ G, float *__restrict__ gnorm) {
+                                                        const CamBatch cams, int V, Layout L, char *ws,
+                                                        float *__restrict__ gnorm) {
     constexpr int NC = (D + 1) * (D + 1);
-    char *w = const_cast<char *>(ws);
-    const uint32_t nvis = at<WsHeader>(w, L.hdr)->vis_count;
+    const uint32_t nvis = at<WsHeader>(ws, L.hdr)->vis_count;
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nvis) return;
-    const int64_t i = at<const uint32_t>(w, L.vis_list)[t];
-    const int32_t *radius = at<const int32_t>(w, L.radius);
-    float4 *g2d = at<float4>(w, L.grad2d);
+    const int64_t i = at<const uint32_t>(ws, L.vis_list)[t];
+    const int32_t *radius = at<const int32_t>(ws, L.radius);
+    float4 *g2d = at<float4>(ws, L.grad2d);
+    float *S = at<float>(ws, L.scratch);  // [row][n], column t
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
                           P[9 * ld + i]);
@@ -304,16 +311,15 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     for (int k = 0; k < 9; k++) gR[k] = 0.f;
     float norm_acc = 0.f;
     const float S3[9] = {cv.S00, cv.S01, cv.S02, cv.S01, cv.S11, cv.S12, cv.S02, cv.S12, cv.S22};
+    // ---- geometry: conic -> Sigma2 -> (Sigma3, J) -> (q, s), mean2d -> P
     for (int v = 0; v < V; v++) {
         int64_t m = (int64_t)v * n + i;
         if (radius[m] <= 0) continue;
         const gs_camera &cam = cams.c[v];
         Proj p = project_recipe(cam, px, py, pz, cv, L.TX, L.TY);
-        float4 ga = g2d[3 * m], gb = g2d[3 * m + 1], gc = g2d[3 * m + 2];
-        // consumed: reset so that a repeated backward on the same forward state starts from 0
-        g2d[3 * m] = g2d[3 * m + 1] = g2d[3 * m + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x, gsig = gb.y;
-        float gcol[3] = {gb.z, gb.w, gc.x};
+        float4 ga = g2d[3 * m], gb = g2d[3 * m + 1];
+        float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x;
+        gop += gb.y;
         norm_acc += sqrtf(gu * gu + gv * gv);
         // conic Q = Sigma2'^-1 : dL/dSigma2 = -Q G Q, G = [[gA, gB/2], [gB/2, gC]]
         float A = p.A, B = p.B, C = p.C;
@@ -381,41 +387,49 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
                 gs[j] += gm * cv.Rq[3 * r + j] * cv.e[j];  // d/dlog s = e d/de
                 gR[3 * r + j] += gm * cv.e[j];
             }
-        gop += gsig;
-        // SH colour, one channel at a time (coefficients re-read through L1)
-        float Cc[3];
-        cam_centre(cam, Cc);
-        float dx = px - Cc[0], dy = py - Cc[1], dz = pz - Cc[2];
-        float nd = sqrtf(dx * dx + dy * dy + dz * dz), ind = 1.f / nd;
-        float dir[3] = {dx * ind, dy * ind, dz * ind};
-        float Y[16];
-        sh_basis<D>(dir[0], dir[1], dir[2], Y);
-        float gdir[3] = {0.f, 0.f, 0.f};
+    }
+    // ---- SH colour, one channel at a time: c = max(0, sum_l SH_l Y_l(dir) + 0.5) (R6)
 #pragma unroll 1
-        for (int ch = 0; ch < 3; ch++) {
-            float c[16];
-            float acc = 0.5f;
+    for (int ch = 0; ch < 3; ch++) {
+        float c[16], acc_sh[16];
 #pragma unroll
-            for (int l = 0; l < NC; l++) {
-                c[l] = P[(11 + 3 * l + ch) * ld + i];
-                acc += c[l] * Y[l];
-            }
-            if (acc < 0.f) continue;  // clamped channel: zero gradient (R6)
+        for (int l = 0; l < NC; l++) {
+            c[l] = P[(11 + 3 * l + ch) * ld + i];
+            acc_sh[l] = 0.f;
+        }
+        for (int v = 0; v < V; v++) {
+            int64_t m = (int64_t)v * n + i;
+            if (radius[m] <= 0) continue;
+            const float *gcol4 = reinterpret_cast<const float *>(g2d + 3 * m);
+            float gcol = gcol4[6 + ch];  // record [.. | C, sigma, r, g | b ..]
+            float Cc[3];
+            cam_centre(cams.c[v], Cc);
+            float dx = px - Cc[0], dy = py - Cc[1], dz = pz - Cc[2];
+            float nd = sqrtf(dx * dx + dy * dy + dz * dz), ind = 1.f / nd;
+            float dir[3] = {dx * ind, dy * ind, dz * ind};
+            float Y[16];
+            sh_basis<D>(dir[0], dir[1], dir[2], Y);
+            float a = 0.5f;
 #pragma unroll
-            for (int l = 0; l < NC; l++) G[(11 + 3 * l + ch) * ld + i] += Y[l] * gcol[ch];
+            for (int l = 0; l < NC; l++) a += c[l] * Y[l];
+            if (a < 0.f) continue;  // clamped channel: zero gradient
+#pragma unroll
+            for (int l = 0; l < NC; l++) acc_sh[l] += Y[l] * gcol;
             if (D > 0) {
                 float gd[3];
                 sh_grad_dir<D>(dir[0], dir[1], dir[2], c, gd);
-                gdir[0] += gcol[ch] * gd[0];
-                gdir[1] += gcol[ch] * gd[1];
-                gdir[2] += gcol[ch] * gd[2];
+                float dd = dir[0] * gd[0] + dir[1] * gd[1] + dir[2] * gd[2];
+#pragma unroll
+                for (int k = 0; k < 3; k++) gP[k] += gcol * (gd[k] - dir[k] * dd) * ind;
             }
         }
-        if (D > 0) {
-            float dd = dir[0] * gdir[0] + dir[1] * gdir[1] + dir[2] * gdir[2];
 #pragma unroll
-            for (int k = 0; k < 3; k++) gP[k] += (gdir[k] - dir[k] * dd) * ind;
-        }
+        for (int l = 0; l < NC; l++) S[(11 + 3 * l + ch) * n + t] = acc_sh[l];
+    }
+    // consumed: reset the 2D records so a repeated backward on the same forward starts from 0
+    for (int v = 0; v < V; v++) {
+        int64_t m = (int64_t)v * n + i;
+        if (radius[m] > 0) g2d[3 * m] = g2d[3 * m + 1] = g2d[3 * m + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // quaternion: dL/dq_hat from dL/dRq, then through the normalisation
     float w_ = cv.qn[0], qx = cv.qn[1], qy = cv.qn[2], qz = cv.qn[3];
@@ -429,17 +443,17 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
                        qy * g[7]);
     float dotg = w_ * gq0 + qx * gq1 + qy * gq2 + qz * gq3;
     float in = cv.inv_norm;
-    G[i] += gP[0];
-    G[ld + i] += gP[1];
-    G[2 * ld + i] += gP[2];
-    G[3 * ld + i] += (gq0 - w_ * dotg) * in;
-    G[4 * ld + i] += (gq1 - qx * dotg) * in;
-    G[5 * ld + i] += (gq2 - qy * dotg) * in;
-    G[6 * ld + i] += (gq3 - qz * dotg) * in;
-    G[7 * ld + i] += gs[0];
-    G[8 * ld + i] += gs[1];
-    G[9 * ld + i] += gs[2];
-    G[10 * ld + i] += sig * (1.f - sig) * gop;
+    S[0 * n + t] = gP[0];
+    S[1 * n + t] = gP[1];
+    S[2 * n + t] = gP[2];
+    S[3 * n + t] = (gq0 - w_ * dotg) * in;
+    S[4 * n + t] = (gq1 - qx * dotg) * in;
+    S[5 * n + t] = (gq2 - qy * dotg) * in;
+    S[6 * n + t] = (gq3 - qz * dotg) * in;
+    S[7 * n + t] = gs[0];
+    S[8 * n + t] = gs[1];
+    S[9 * n + t] = gs[2];
+    S[10 * n + t] = sig * (1.f - sig) * gop;
     if (gnorm) gnorm[i] += norm_acc;
 }
 
@@ -447,6 +461,7 @@ cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, c
                               cudaStream_t s) {
     int64_t blocks = (p.n + 255) / 256;
     if (blocks == 0) return cudaGetLastError();
+    ProfScope prof("k_preprocess", s);
     switch (p.sh_degree) {
         case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
         case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
@@ -457,14 +472,16 @@ cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, c
 }
 
 cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                                  float *grads, float *grad2d_norm, cudaStream_t s) {
-    int64_t blocks = (p.n + 127) / 128;
+                                  float *grad2d_norm, cudaStream_t s) {
+    int64_t blocks = (p.n + 127) / 128;  // grid sized for every Gaussian; threads past vis_count exit
     if (blocks == 0) return cudaGetLastError();
+    char *w = (char *)ws;
+    ProfScope prof("k_preprocess_bwd", s);
     switch (p.sh_degree) {
-        case 0: k_preprocess_bwd<0><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, grads, grad2d_norm); break;
-        case 1: k_preprocess_bwd<1><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, grads, grad2d_norm); break;
-        case 2: k_preprocess_bwd<2><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, grads, grad2d_norm); break;
-        default: k_preprocess_bwd<3><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, grads, grad2d_norm); break;
+        case 0: k_preprocess_bwd<0><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
+        case 1: k_preprocess_bwd<1><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
+        case 2: k_preprocess_bwd<2><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
+        default: k_preprocess_bwd<3><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
     }
     return cudaGetLastError();
 }

@@ -144,16 +144,87 @@ __global__ void __launch_bounds__(ADAM_THREADS) k_adam(float *__restrict__ P, fl
     }
 }
 
-static int g_sms = 0;
+// ---- dense column kernels over the compacted backward scratch ---------------------------
+// thread = 4 consecutive Gaussians (one float4 of every row); grid.y splits the rows
+constexpr int COL_THREADS = 256;
+constexpr int ROW_GROUPS = 8;
 
-cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
-                        int64_t g0, int64_t g1, int zero, cudaStream_t s) {
-    if (g_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
+__device__ __forceinline__ bool load_slots(const uint32_t *slot, int64_t i0, int64_t n, uint32_t sl[4]) {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        sl[k] = i0 + k < n ? slot[i0 + k] : 0xFFFFFFFFu;
+        any |= sl[k] != 0xFFFFFFFFu;
     }
+    return any;
+}
+
+__global__ void __launch_bounds__(COL_THREADS) k_grad_accumulate(float *__restrict__ G, int64_t ld, int64_t n,
+                                                                 int rows, const uint32_t *__restrict__ slot,
+                                                                 const float *__restrict__ S) {
+    const int64_t c4 = (int64_t)blockIdx.x * COL_THREADS + threadIdx.x;
+    const int64_t i0 = c4 * 4;
+    if (i0 >= n) return;
+    uint32_t sl[4];
+    if (!load_slots(slot, i0, n, sl)) return;
+    const int rpg = (rows + gridDim.y - 1) / gridDim.y;
+    const int r0 = blockIdx.y * rpg, r1 = min(rows, r0 + rpg);
+    for (int row = r0; row < r1; row++) {
+        float4 *gp = reinterpret_cast<float4 *>(G + (int64_t)row * ld) + c4;
+        float4 g = *gp;
+        const float *Sr = S + (int64_t)row * n;
+        if (sl[0] != 0xFFFFFFFFu) g.x += Sr[sl[0]];
+        if (sl[1] != 0xFFFFFFFFu) g.y += Sr[sl[1]];
+        if (sl[2] != 0xFFFFFFFFu) g.z += Sr[sl[2]];
+        if (sl[3] != 0xFFFFFFFFu) g.w += Sr[sl[3]];
+        *gp = g;
+    }
+}
+
+__global__ void __launch_bounds__(COL_THREADS) k_adam_fused(float *__restrict__ P, float *__restrict__ Mm,
+                                                            float *__restrict__ Vv, int64_t ld, int64_t n, int rows,
+                                                            const uint32_t *__restrict__ slot,
+                                                            const float *__restrict__ S, AdamArgs a) {
+    const int64_t c4 = (int64_t)blockIdx.x * COL_THREADS + threadIdx.x;
+    const int64_t i0 = c4 * 4;
+    if (i0 >= n) return;
+    uint32_t sl[4];
+    load_slots(slot, i0, n, sl);
+    const int rpg = (rows + gridDim.y - 1) / gridDim.y;
+    const int r0 = blockIdx.y * rpg, r1 = min(rows, r0 + rpg);
+#pragma unroll 2
+    for (int row = r0; row < r1; row++) {
+        const float lr = a.lr[row_class(row)];
+        const int64_t q = (int64_t)row * (ld / 4) + c4;
+        float4 p = reinterpret_cast<float4 *>(P)[q];
+        float4 m = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4 *>(Mm)[q];
+        float4 v = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4 *>(Vv)[q];
+        const float *Sr = S + (int64_t)row * n;
+        float g[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) g[k] = sl[k] != 0xFFFFFFFFu ? Sr[sl[k]] : 0.f;
+        float *pp = &p.x, *mm = &m.x, *vv = &v.x;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (i0 + k < n) adam1(pp[k], g[k], mm[k], vv[k], lr, a);
+        reinterpret_cast<float4 *>(P)[q] = p;
+        if (!a.sgd) {
+            reinterpret_cast<float4 *>(Mm)[q] = m;
+            reinterpret_cast<float4 *>(Vv)[q] = v;
+        }
+    }
+}
+
+cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws, float *grads, cudaStream_t s) {
+    int64_t cols4 = (p.n + 3) / 4;
+    if (cols4 == 0) return cudaGetLastError();
+    dim3 grid((unsigned)((cols4 + COL_THREADS - 1) / COL_THREADS), ROW_GROUPS);
+    k_grad_accumulate<<<grid, COL_THREADS, 0, s>>>(grads, p.ld, p.n, gs_param_rows(p.sh_degree),
+                                                   at<uint32_t>(ws, L.slot), at<float>(ws, L.scratch));
+    return cudaGetLastError();
+}
+
+static AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero) {
     AdamArgs a;
     double bc1 = 1.0 - std::pow((double)hp.beta1, (double)step);
     double bc2 = 1.0 - std::pow((double)hp.beta2, (double)step);
@@ -164,9 +235,28 @@ cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const 
     a.rs_bc2 = (float)(1.0 / std::sqrt(bc2));
     a.sgd = hp.sgd_mode;
     a.zero = zero;
+    return a;
+}
+
+cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, float *m, float *v,
+                              const gs_adam_hparams &hp, int64_t step, cudaStream_t s) {
+    AdamArgs a = adam_args(hp, step, 0);
+    int64_t cols4 = (p.n + 3) / 4;
+    if (cols4 == 0) return cudaGetLastError();
+    dim3 grid((unsigned)((cols4 + COL_THREADS - 1) / COL_THREADS), ROW_GROUPS);
+    ProfScope prof("k_adam_fused", s);
+    k_adam_fused<<<grid, COL_THREADS, 0, s>>>(p.data, m, v, p.ld, p.n, gs_param_rows(p.sh_degree),
+                                              at<uint32_t>(ws, L.slot), at<float>(ws, L.scratch), a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
+                        int64_t g0, int64_t g1, int zero, cudaStream_t s) {
+    AdamArgs a = adam_args(hp, step, zero);
     int rows = gs_param_rows(p.sh_degree);
     int64_t per_row = p.ld / 4;
     dim3 grid((unsigned)((per_row + ADAM_THREADS * ADAM_UNROLL - 1) / (ADAM_THREADS * ADAM_UNROLL)), rows);
+    ProfScope prof("k_adam", s);
     if (per_row > 0) k_adam<<<grid, ADAM_THREADS, 0, s>>>(p.data, g, m, v, p.ld, g0, g1, a);
     return cudaGetLastError();
 }

@@ -8,11 +8,12 @@
 //
 // Layout: one 256-thread CTA per (view, 16x16 tile), one thread per pixel; each warp owns an
 // 8x4 pixel block (2 x 4 blocks per tile).  Gaussian records are staged in shared memory in
-// batches of 256; before evaluating a Gaussian a warp tests its 3-sigma bounding box (exact
-// ellipse extents 3 sqrt(Sigma2_xx), 3 sqrt(Sigma2_yy), padded so the test is conservative)
-// against the warp's block and skips it with one uniform branch -- no pixel result changes,
-// but most (warp, Gaussian) pairs of small splats are never evaluated.  The CTA leaves as
-// soon as every pixel of the tile has stopped.
+// batches of 256; each warp then builds, in parallel over the batch (one Gaussian per lane,
+// ballot + popc), the ordered list of Gaussians that can reach its block: the exact minimum of
+// d^T Q d over the block is compared with the Gaussian's limit min(9, 2 ln(255 sigma)) (3-sigma
+// cutoff or alpha >= 1/255), padded so the test is conservative.  The sequential per-pixel
+// loop then only visits that list -- no pixel result changes.  The CTA leaves as soon as every
+// pixel of the tile has stopped.
 //
 // The backward replays each pixel's list back to front: dL/dc, dL/dalpha
 // = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  The nine
@@ -40,16 +41,50 @@ __device__ __forceinline__ float pixel_power(float px, float py, const float4 g0
     return FMA(-MUL(g0.w, dx), dy, MUL(-0.5f, qf));
 }
 
+// e^power with the SFU: ex2.approx.ftz(power * log2 e).  Forward and backward evaluate alpha
+// with this same sequence, so their skip / stop decisions agree bit for bit.
+__device__ __forceinline__ float fast_exp(float power) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(power * 1.4426950408889634f));
+    return y;
+}
+
+// Largest d^T Q d at which a Gaussian can still be composited: the 3-sigma cutoff (R9) or the
+// alpha >= 1/255 skip, alpha <= sigma e^(-q/2) (R7), whichever is tighter (-1: never composited).
+__device__ __forceinline__ float q_limit(float sigma) {
+    if (sigma * 255.0f < 1.0f) return -1.0f;
+    return fminf(9.0f, 2.0f * __logf(255.0f * sigma));
+}
+
+// Conservative warp-level skip: minimum of d^T Q d over the warp's pixel block (centres
+// [x0, x0 + 7] x [y0, y0 + 3]) exceeds the Gaussian's limit.  Exact box-ellipse minimum:
+// 0 if the mean is inside, else the smallest of the four clamped edge minima.  The padding
+// (1e-3 relative + 1e-3 absolute) absorbs the rounding of the per-pixel fp32 power, so a
+// culled Gaussian can never pass the per-pixel tests.
+__device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, float qlim, float x0, float y0) {
+    if (qlim < 0.f) return true;
+    const float A = g0.z, B = g0.w, C = g1.x;
+    const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + 3.f - g0.y;
+    if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return false;
+    float best = 3.4e38f;
+    // edges x = X: f = A X^2 + 2 B X y + C y^2, y* = -B X / C clamped to [ay, by]
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        float X = e ? bx : ax;
+        float y = fminf(fmaxf(-B * X / C, ay), by);
+        best = fminf(best, A * X * X + 2.f * B * X * y + C * y * y);
+        float Y = e ? by : ay;
+        float x = fminf(fmaxf(-B * Y / A, ax), bx);
+        best = fminf(best, A * x * x + 2.f * B * x * Y + C * Y * Y);
+    }
+    return best > qlim * 1.001f + 1e-3f;
+}
+
 // thread -> pixel: warp w covers the 8x4 block (w & 1, w >> 1) of the tile
 __device__ __forceinline__ void pixel_of(int tid, int &lx, int &ly) {
     int w = tid >> 5, l = tid & 31;
     lx = (w & 1) * 8 + (l & 7);
     ly = (w >> 1) * 4 + (l >> 3);
-}
-
-// warp-uniform: does the Gaussian's padded 3-sigma box miss the warp's 8x4 block?
-__device__ __forceinline__ bool warp_misses(const float4 g0, const float4 g2, float wx0, float wy0) {
-    return g0.x + g2.y < wx0 || g0.x - g2.y > wx0 + 7.f || g0.y + g2.z < wy0 || g0.y - g2.z > wy0 + 3.f;
 }
 
 __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restrict__ ranges,
@@ -59,7 +94,8 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
                                                           const float4 *__restrict__ rec2, int64_t n, int W, int H,
                                                           int TX, int tiles, float bg0, float bg1, float bg2,
                                                           float *__restrict__ out_rgb, float *__restrict__ out_T,
-                                                          float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib) {
+                                                          float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib,
+                                                          uint32_t *__restrict__ ncomp) {
     __shared__ float4 s0[BLOCK_PIX];
     __shared__ float4 s1[BLOCK_PIX];
     __shared__ float4 s2[BLOCK_PIX];
@@ -79,7 +115,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
     const float fx = (float)px, fy = (float)py;
     const int64_t vbase = (int64_t)view * n;
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    uint32_t last = 0;
+    uint32_t last = 0, composited = 0;
     bool done = !inside;
     const int warp = tid >> 5, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -88,9 +124,11 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
         int idx = b0 + tid;
         if (idx < todo_all) {
             int64_t m = vbase + vals[range.x + idx];
+            float4 r1 = rec1[m], r2 = rec2[m];
+            r2.w = q_limit(r1.y);
             s0[tid] = rec0[m];
-            s1[tid] = rec1[m];
-            s2[tid] = rec2[m];
+            s1[tid] = r1;
+            s2[tid] = r2;
         }
         __syncthreads();
         const int cnt = min(BLOCK_PIX, todo_all - b0);
@@ -99,7 +137,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
         int nsel = 0;
         for (int k = 0; k < cnt; k += 32) {
             int j = k + lane;
-            bool hit = j < cnt && !warp_misses(s0[j], s2[j], wx0, wy0);
+            bool hit = j < cnt && !block_misses(s0[j], s1[j], s2[j].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
             if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
             nsel += __popc(b);
@@ -115,7 +153,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
             float dx, dy;
             float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
             if (done || power > 0.0f || power < POWER_CUT) continue;
-            float alpha = fminf(ALPHA_MAX, g1.y * __expf(power));
+            float alpha = fminf(ALPHA_MAX, g1.y * fast_exp(power));
             if (alpha < ALPHA_MIN) continue;
             float test_T = T * (1.0f - alpha);
             if (test_T < T_STOP) {
@@ -127,6 +165,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
             c1 += g1.w * w;
             c2 += g2.x * w;
             T = test_T;
+            composited++;
             last = (uint32_t)(b0 + j + 1);  // 1-based list position of the last composited
         }
     }
@@ -140,6 +179,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
         if (out_T) out_T[(int64_t)view * HW + pix] = T;
         T_keep[(int64_t)view * HW + pix] = T;
         ncontrib[(int64_t)view * HW + pix] = last;
+        ncomp[(int64_t)view * HW + pix] = composited;
     }
 }
 
@@ -237,9 +277,11 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
             uint32_t gi = vals[range.x + pos];
             int64_t m = vbase + gi;
             sid[tid] = gi;
+            float4 r1 = rec1[m], r2 = rec2[m];
+            r2.w = q_limit(r1.y);
             s0[tid] = rec0[m];
-            s1[tid] = rec1[m];
-            s2[tid] = rec2[m];
+            s1[tid] = r1;
+            s2[tid] = r2;
         }
         __syncthreads();
         // phase 1: ordered (back to front) list of the batch entries this warp must replay --
@@ -250,7 +292,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
         int nsel = 0;
         for (int k = 0; k < cnt; k += 32) {
             int j = k + lane;
-            bool hit = j < cnt && j >= j0 && !warp_misses(s0[j], s2[j], wx0, wy0);
+            bool hit = j < cnt && j >= j0 && !block_misses(s0[j], s1[j], s2[j].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
             if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
             nsel += __popc(b);
@@ -269,12 +311,12 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                 float dx, dy;
                 float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
                 if (!(power > 0.0f || power < POWER_CUT)) {
-                    float e = __expf(power);
+                    float e = fast_exp(power);
                     float a_raw = g1.y * e;
                     float alpha = fminf(ALPHA_MAX, a_raw);
                     if (alpha >= ALPHA_MIN) {
                         contrib = true;
-                        T = T / (1.0f - alpha);  // transmittance before this Gaussian
+                        T = __fdividef(T, 1.0f - alpha);  // transmittance before this Gaussian
                         float w = alpha * T;
                         dLdr = g_0 * w;
                         dLdg = g_1 * w;
@@ -314,15 +356,17 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s) {
     dim3 grid(L.TX, L.TY, L.V);
+    ProfScope prof("k_raster_fwd", s);
     k_raster_fwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
                                             at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
                                             L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
-                                            at<uint32_t>(ws, L.ncontrib));
+                                            at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp));
     return cudaGetLastError();
 }
 
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     dim3 grid(L.TX, L.TY, L.V);
+    ProfScope prof("k_raster_bwd", s);
     k_raster_bwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
                                             at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
                                             L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),

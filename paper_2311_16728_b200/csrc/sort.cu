@@ -393,6 +393,7 @@ cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, 
         cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
+    ProfScope prof("k_sort_pass", s);
     for (int p = 0; p < passes; p++)
         k_sort_pass<<<sort_blocks, SORT_THREADS, smem, s>>>(k0, v0, k1, v1, count, cap, p, hdr, lookback, sort_blocks);
     k_sort_fixup<<<std::max(1, num_sms() * 4), 256, 0, s>>>(k0, v0, k1, v1, count, cap, hdr, passes);

@@ -102,15 +102,25 @@ class MappingEngine:
     def render(self, level: int = 0):
         return self.renderers[level].forward(self.params, self.cams[level], self.bg)
 
-    def iteration(self, level: int) -> torch.Tensor:
-        """One optimiser step at pyramid level `level` (Eq. 4 against GP^level, R19)."""
+    def distributed(self) -> bool:
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def iteration(self, level: int, fused: bool | None = None) -> torch.Tensor:
+        """One optimiser step at pyramid level `level` (Eq. 4 against GP^level, R19).  On one GPU
+        the backward and Adam run fused (no gradient array); with data parallelism the gradient
+        is materialised, all-reduced (A10) and then stepped."""
         r = self.renderers[level]
         cams = self.cams[level]
         rgb, _ = r.forward(self.params, cams, self.bg)                       # A1-A6
         loss, dL = self.losses[level](rgb, self.pyr[level])                  # A7
-        r.backward(self.params, cams, dL, self.grads, self.grad2d_norm, self.bg)  # A8-A9
-        reduce_gradients(self.grads, self.group)                             # A10
-        self.adam.step(self.grads, zero_grads=True)                          # A11
+        if fused is None:
+            fused = not self.distributed()
+        if fused:
+            r.backward_adam(self.params, cams, dL, self.adam, self.grad2d_norm, self.bg)  # A8-A9 + A11
+        else:
+            r.backward(self.params, cams, dL, self.grads, self.grad2d_norm, self.bg)  # A8-A9
+            reduce_gradients(self.grads, self.group)                         # A10
+            self.adam.step(self.grads, zero_grads=True)                      # A11
         return loss
 
     def step(self) -> list:

