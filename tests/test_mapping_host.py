@@ -1,0 +1,49 @@
+"""Host-side logic of the mapping driver (no GPU): the Gaussian-pyramid schedule of Eq. 5
+(SPEC.md:443-451), level geometry (R12/R19), parameter packing (include/gs.h layout) and the
+bench's launch accounting."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2311_16728_b200.core import level_shapes, pack_params, param_rows, unpack
+from paper_2311_16728_b200.mapping import gp_level
+from synth import make_cameras, make_scene, scaled_camera
+
+
+def test_gp_level_schedule():
+    # level(0) = n; non-increasing; terminal 0; n = 0 -> always 0
+    assert gp_level(0, 2, 100) == 2
+    seq = [gp_level(i, 2, 100) for i in range(500)]
+    assert all(a >= b for a, b in zip(seq, seq[1:]))
+    assert seq[-1] == 0 and seq[199] == 1 and seq[200] == 0
+    assert all(gp_level(i, 0, 10) == 0 for i in range(50))
+    with pytest.raises(ValueError):
+        gp_level(-1, 2, 10)
+
+
+def test_level_shapes_and_cameras():
+    assert level_shapes(480, 640, 2) == [(480, 640), (240, 320), (120, 160)]
+    assert level_shapes(33, 47, 2) == [(33, 47), (17, 24), (9, 12)]
+    cam = make_cameras("tum", 1)[0]
+    c2 = scaled_camera(cam, 2)
+    assert (c2.width, c2.height) == (160, 120)
+    assert c2.fx == pytest.approx(cam.fx / 4) and c2.cx == pytest.approx(cam.cx / 4)
+    assert scaled_camera(cam, 0) is cam
+
+
+def test_pack_unpack_roundtrip():
+    s = make_scene("tum", n=1000)
+    t = pack_params(s, device="cpu")
+    assert tuple(t.shape) == (param_rows(3), 1024)
+    back = unpack(t, 1000, 3)
+    for k in ("means", "quats", "log_scales", "opacity_logits", "sh"):
+        assert np.array_equal(back[k], getattr(s, k))
+    assert (t[:, 1000:] == 0).all()
+
+
+def test_launch_accounting_matches_design():
+    import bench
+    # 43 key bits -> 6 digit passes
+    assert bench.launches_per_iteration(43, True) == 2 + 5 + 6 + 3 + 3
+    assert bench.launches_per_iteration(43, False) == bench.launches_per_iteration(43, True) + 1
