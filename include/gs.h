@@ -196,11 +196,19 @@ typedef struct {
 } gs_ws_view;
 gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t n_views, int32_t width,
                                   int32_t height, gs_ws_view *out);
+/* Binning path for subsequent gs_preprocess / gs_render_forward calls (process-wide):
+   0 (default) = per-(view, tile) pair counts in A1, scan to tile ranges, scatter into tile
+   buckets and an in-tile bitonic sort by (depth bits, id) in shared memory (MSD radix on the
+   tile digit); 1 = key duplication + the global onesweep LSD radix sort + range extraction.
+   Both produce the identical keys, values and ranges (bit-exact to the oracle). */
+gs_status gs_set_binning(int32_t mode);
+
 /* Live timing of one kernel inside a benchmark: after gs_profile_kernel("k_raster_bwd") every
    launch of that kernel (any call, any stream) is bracketed by CUDA events recorded on its
    launching stream; gs_profile_read synchronises on them and returns the summed duration and
    the launch count, then resets.  gs_profile_kernel(NULL) turns it off.  Names:
-   k_preprocess, k_raster_fwd, k_raster_bwd, k_preprocess_bwd, k_adam, k_adam_fused, k_sort_pass. */
+   k_preprocess, k_raster_fwd, k_raster_bwd, k_preprocess_bwd, k_adam, k_adam_fused, k_sort_pass,
+   k_tile_sort. */
 gs_status gs_profile_kernel(const char *kernel);
 gs_status gs_profile_read(double *total_ms /*host*/, int64_t *launches /*host*/);
 /* (float)exp((double)s) exactly as the preprocess kernel evaluates it, for the exhaustive

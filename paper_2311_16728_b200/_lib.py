@@ -27,7 +27,7 @@ EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
            "gs_pyramid", "gs_adam_step",
            "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
-           "gs_debug_workspace_view", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
+           "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
 
 class GsError(RuntimeError):
@@ -242,6 +242,11 @@ def gs_debug_workspace_view(ws, n, n_views, width, height) -> GsWsView:
                                          C.c_int32(width), C.c_int32(height), C.byref(out)),
            "gs_debug_workspace_view")
     return out
+
+
+def gs_set_binning(mode: int):
+    """0 = tile buckets + in-tile sort (default), 1 = global onesweep LSD radix sort."""
+    _check(lib().gs_set_binning(C.c_int32(mode)), "gs_set_binning")
 
 
 def gs_profile_kernel(name: str | None):

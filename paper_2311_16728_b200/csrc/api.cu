@@ -25,7 +25,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.TY = (H + TILE - 1) / TILE;
     L.tiles = L.TX * L.TY;
     L.cap = ((cap + SORT_TILE - 1) / SORT_TILE) * SORT_TILE;
-    L.scan_blocks = (L.M + SCAN_TILE - 1) / SCAN_TILE;
+    L.scan_blocks = (std::max<int64_t>(L.M, (int64_t)V * L.tiles) + SCAN_TILE - 1) / SCAN_TILE;
     L.sort_blocks = L.cap / SORT_TILE;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -56,6 +56,10 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.keys1 = take((size_t)L.cap * sizeof(uint64_t));
     L.vals0 = take((size_t)L.cap * sizeof(uint32_t));
     L.vals1 = take((size_t)L.cap * sizeof(uint32_t));
+    L.tile_count = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
+    L.tile_start = take((size_t)V * L.tiles * sizeof(uint32_t));
+    L.tile_cursor = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
+    L.bin_big = take((size_t)2 * L.cap * sizeof(uint64_t));
     L.sort_look = take((size_t)SORT_MAX_PASSES * std::max<int64_t>(L.sort_blocks, 1) * SORT_RADIX * sizeof(uint32_t));
     L.total = o;
     return L;
@@ -64,8 +68,8 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
 bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out) {
     Layout L0 = make_layout(n, V, W, H, 0);
     if (L0.total > ws_bytes) return false;
-    // bytes per SORT_TILE pairs: 2 x (8 + 4) per pair + look-back words
-    size_t per_tile = (size_t)SORT_TILE * 24 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
+    // bytes per SORT_TILE pairs: 2 x (8 + 4) + 16 (bucket overflow) per pair + look-back words
+    size_t per_tile = (size_t)SORT_TILE * 40 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
     int64_t tiles = (int64_t)((ws_bytes - L0.total) / per_tile) + 1;
     for (; tiles >= 0; tiles--) {
         Layout L = make_layout(n, V, W, H, tiles * SORT_TILE);
@@ -83,7 +87,8 @@ struct Token {
     int64_t n, ld;
     int32_t D, V;
     uint64_t cam_hash;
-    int stage;  // 1 = preprocessed, 2 = rendered
+    int stage;  // 1 = preprocessed, 2 = rendered, 3 = parameters stepped in place
+    int mode;   // binning mode of the preprocess
 };
 static std::mutex g_mu;
 static std::unordered_map<const void *, Token> g_tokens;
@@ -94,8 +99,9 @@ static uint64_t hash_cams(const gs_camera *c, int V) {
     for (size_t k = 0; k < sizeof(gs_camera) * (size_t)V; k++) h = (h ^ p[k]) * 1099511628211ull;
     return h;
 }
+static int g_binning_mode_decl();
 static Token make_token(const gs_params *p, const gs_camera *c, int V, int stage) {
-    return Token{p->data, p->n, p->ld, p->sh_degree, V, hash_cams(c, V), stage};
+    return Token{p->data, p->n, p->ld, p->sh_degree, V, hash_cams(c, V), stage, g_binning_mode_decl()};
 }
 static bool same(const Token &a, const Token &b) {
     return a.data == b.data && a.n == b.n && a.ld == b.ld && a.D == b.D && a.V == b.V && a.cam_hash == b.cam_hash;
@@ -121,6 +127,16 @@ static gs_status check_views(const gs_camera *cams, int V, CamBatch *cb) {
 }
 
 static gs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GS_OK : GS_ERR_CUDA; }
+
+static int g_binning_mode = 0;
+int binning_mode() { return g_binning_mode; }
+static int g_binning_mode_decl() { return g_binning_mode; }
+// binning mode recorded by the preprocess of this workspace
+static int it_mode(const void *ws) {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_tokens.find(ws);
+    return it == g_tokens.end() ? g_binning_mode : it->second.mode;
+}
 
 // ---- live kernel timing ----
 struct Prof {
@@ -182,8 +198,18 @@ gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t 
     WsHeader *hdr = at<WsHeader>(ws, L.hdr);
     cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter, visible count
     cudaMemsetAsync(at<char>(ws, L.scan_flags), 0, (size_t)std::max<int64_t>(L.scan_blocks, 1) * 8, s);
-    cudaError_t e = launch_preprocess(*params, cb, n_views, L, ws, s);
-    if (e == cudaSuccess) e = launch_scan(L, ws, s);
+    const bool buckets = binning_mode() == 0;
+    if (buckets)
+        cudaMemsetAsync(at<char>(ws, L.tile_count), 0, (size_t)n_views * L.tiles * CNT_STRIDE * sizeof(uint32_t), s);
+    cudaError_t e = launch_preprocess(*params, cb, n_views, L, ws, buckets, s);
+    if (e == cudaSuccess) {
+        if (buckets)  // tile ranges straight from the per-tile counts
+            e = launch_scan_u32(at<uint32_t>(ws, L.tile_count), at<uint32_t>(ws, L.tile_start),
+                                (int64_t)n_views * L.tiles, at<uint64_t>(ws, L.scan_flags), hdr, s, CNT_STRIDE);
+        else  // pair offsets of every (view, Gaussian) for key duplication
+            e = launch_scan_u32(at<uint32_t>(ws, L.tiles_touched), at<uint32_t>(ws, L.offsets), L.M,
+                                at<uint64_t>(ws, L.scan_flags), hdr, s);
+    }
     if (e != cudaSuccess) return GS_ERR_CUDA;
     std::lock_guard<std::mutex> g(g_mu);
     g_tokens[ws] = make_token(params, cams, n_views, 1);
@@ -207,13 +233,18 @@ gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int3
     }
     cudaStream_t s = (cudaStream_t)stream;
     WsHeader *hdr = at<WsHeader>(ws, L.hdr);
-    int key_bits = 32 + std::max(1, hi_bits_for((int64_t)n_views * L.tiles));
-    cudaError_t e = launch_duplicate(L, ws, s);
-    if (e == cudaSuccess)
-        e = launch_sort(at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint64_t>(ws, L.keys1),
-                        at<uint32_t>(ws, L.vals1), &hdr->P, L.cap, key_bits, hdr, at<uint32_t>(ws, L.sort_look),
-                        L.sort_blocks, s);
-    if (e == cudaSuccess) e = launch_ranges(L, ws, s);
+    cudaError_t e;
+    if (it_mode(ws) == 0) {
+        e = launch_bin(L, ws, s);
+    } else {
+        int key_bits = 32 + std::max(1, hi_bits_for((int64_t)n_views * L.tiles));
+        e = launch_duplicate(L, ws, s);
+        if (e == cudaSuccess)
+            e = launch_sort(at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint64_t>(ws, L.keys1),
+                            at<uint32_t>(ws, L.vals1), &hdr->P, L.cap, key_bits, hdr,
+                            at<uint32_t>(ws, L.sort_look), L.sort_blocks, s);
+        if (e == cudaSuccess) e = launch_ranges(L, ws, s);
+    }
     if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s);
     if (e != cudaSuccess) return GS_ERR_CUDA;
     std::lock_guard<std::mutex> g(g_mu);
@@ -377,6 +408,12 @@ gs_status gs_debug_workspace_view(void *ws, size_t ws_bytes, int64_t n, int32_t 
     out->n_contrib = at<const uint32_t>(ws, L.ncontrib);
     out->n_composited = at<const uint32_t>(ws, L.ncomp);
     out->capacity = L.cap;
+    return GS_OK;
+}
+
+gs_status gs_set_binning(int32_t mode) {
+    if (mode != 0 && mode != 1) return GS_ERR_INVALID_ARG;
+    g_binning_mode = mode;
     return GS_OK;
 }
 

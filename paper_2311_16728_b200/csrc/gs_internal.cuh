@@ -19,6 +19,11 @@ constexpr int SORT_ITEMS = 16;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 4096 pairs per CTA
 constexpr int SORT_MAX_PASSES = 8;
 
+// bucket binning: per-(view, tile) counters are padded to 256 B (one L2 slice each) and
+// aggregated in shared memory when the table fits
+constexpr int CNT_STRIDE = 64;         // u32 words between two counters
+constexpr int SMEM_BINS = 6144;         // max V*tiles aggregated in shared memory
+
 // decoupled-look-back exclusive scan of tiles_touched
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
@@ -48,6 +53,7 @@ struct Layout {
     int64_t scan_blocks, sort_blocks;
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
+    size_t tile_count, tile_start, tile_cursor, bin_big;  // bucket binning (bin.cu)
     size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, ncomp, Tfinal, total;
 };
 
@@ -75,8 +81,13 @@ int hi_bits_for(int64_t count);
 
 // ---- launchers (each returns cudaGetLastError()) ----
 cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                              cudaStream_t s);
-cudaError_t launch_scan(const Layout &L, void *ws, cudaStream_t s);
+                              bool count_tiles, cudaStream_t s);
+// exclusive scan of `count` u32 (decoupled look-back); writes the total to hdr->P
+cudaError_t launch_scan_u32(const uint32_t *in, uint32_t *out, int64_t count, uint64_t *flags, WsHeader *hdr,
+                            cudaStream_t s, int in_stride = 1);
+// binning mode: 0 = tile buckets + in-tile sort (bin.cu), 1 = global onesweep LSD radix sort
+int binning_mode();
+cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_duplicate(const Layout &L, void *ws, cudaStream_t s);
 // generic pair sort on the primary buffers of a workspace (or debug buffers)
 cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, const uint32_t *count,

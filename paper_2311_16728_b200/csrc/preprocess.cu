@@ -207,10 +207,9 @@ __device__ __forceinline__ void cam_centre(const gs_camera &cam, float C[3]) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P, int64_t n, int64_t ld,
-                                                    const CamBatch cams, int V, Layout L, char *ws) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+__device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int64_t n, int64_t ld,
+                                               const CamBatch &cams, int V, const Layout &L, char *ws,
+                                               bool count_tiles, bool smem_cnt, uint32_t *s_cnt, int64_t i) {
     constexpr int NC = (D + 1) * (D + 1);
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
@@ -260,6 +259,16 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
         radius[m] = p.r;
         rect[m] = make_int4(p.x0, p.y0, p.x1, p.y1);
         tt[m] = (uint32_t)((p.x1 - p.x0) * (p.y1 - p.y0));
+        if (count_tiles) {  // per-(view, tile) pair counts for the bucket binning (bin.cu)
+            const int tb = v * L.tiles;
+            uint32_t *tc = at<uint32_t>(ws, L.tile_count);
+            for (int ty = p.y0; ty < p.y1; ty++)
+                for (int tx = p.x0; tx < p.x1; tx++) {
+                    int b = tb + ty * L.TX + tx;
+                    if (smem_cnt) atomicAdd(&s_cnt[b], 1u);
+                    else atomicAdd(&tc[(size_t)b * CNT_STRIDE], 1u);
+                }
+        }
         float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
         g2d[3 * m] = zero;
         g2d[3 * m + 1] = zero;
@@ -283,6 +292,30 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
     }
     at<uint32_t>(ws, L.slot)[i] = slot;
 }
+
+template <int D>
+__global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P, int64_t n, int64_t ld,
+                                                    const CamBatch cams, int V, Layout L, char *ws,
+                                                    bool count_tiles) {
+    __shared__ uint32_t s_cnt[SMEM_BINS];
+    const int VT = V * L.tiles;
+    const bool smem_cnt = count_tiles && VT <= SMEM_BINS;  // uniform
+    if (smem_cnt) {
+        for (int b = threadIdx.x; b < VT; b += blockDim.x) s_cnt[b] = 0;
+        __syncthreads();
+    }
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) preprocess_one<D>(P, n, ld, cams, V, L, ws, count_tiles, smem_cnt, s_cnt, i);
+    if (smem_cnt) {  // one global add per (CTA, tile) into the padded counters
+        __syncthreads();
+        uint32_t *tc = at<uint32_t>(ws, L.tile_count);
+        for (int b = threadIdx.x; b < VT; b += blockDim.x) {
+            uint32_t c = s_cnt[b];
+            if (c) atomicAdd(&tc[(size_t)b * CNT_STRIDE], c);
+        }
+    }
+}
+
 
 // ---------------------------------------------------------------------------------------------
 // A9: chain rule from the per-(view, Gaussian) 2D gradients (u, v, A, B, C, sigma, r, g, b) to
@@ -458,15 +491,15 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
 }
 
 cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                              cudaStream_t s) {
+                              bool count_tiles, cudaStream_t s) {
     int64_t blocks = (p.n + 255) / 256;
     if (blocks == 0) return cudaGetLastError();
     ProfScope prof("k_preprocess", s);
     switch (p.sh_degree) {
-        case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
-        case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
-        case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
-        default: k_preprocess<3><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws); break;
+        case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        default: k_preprocess<3><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
     }
     return cudaGetLastError();
 }

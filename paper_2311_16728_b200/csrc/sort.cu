@@ -38,7 +38,7 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
-                                                       int64_t M, uint64_t *flags, WsHeader *hdr) {
+                                                       int64_t M, uint64_t *flags, WsHeader *hdr, int stride) {
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_warp[SCAN_THREADS / 32];
     __shared__ uint64_t s_prefix;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const uint32_t *__restric
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; k++) {
         int64_t idx = base + k;
-        v[k] = idx < M ? in[idx] : 0u;
+        v[k] = idx < M ? in[idx * stride] : 0u;
         sum += v[k];
     }
     // block exclusive scan of per-thread sums
@@ -105,10 +105,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const uint32_t *__restric
     }
 }
 
-cudaError_t launch_scan(const Layout &L, void *ws, cudaStream_t s) {
-    if (L.M == 0) return cudaGetLastError();
-    k_scan<<<L.scan_blocks, SCAN_THREADS, 0, s>>>(at<uint32_t>(ws, L.tiles_touched), at<uint32_t>(ws, L.offsets),
-                                                  L.M, at<uint64_t>(ws, L.scan_flags), at<WsHeader>(ws, L.hdr));
+cudaError_t launch_scan_u32(const uint32_t *in, uint32_t *out, int64_t count, uint64_t *flags, WsHeader *hdr,
+                            cudaStream_t s, int in_stride) {
+    if (count == 0) return cudaGetLastError();
+    k_scan<<<(unsigned)((count + SCAN_TILE - 1) / SCAN_TILE), SCAN_THREADS, 0, s>>>(in, out, count, flags, hdr,
+                                                                                    in_stride);
     return cudaGetLastError();
 }
 

@@ -76,9 +76,18 @@ def test_exp_scale_bit_exact():
         assert bad.size == 0, (bad.size, s[bad[:5]])
 
 
+@pytest.fixture(params=[0, 1], ids=["buckets", "radix"])
+def binning(request):
+    L.gs_set_binning(request.param)
+    yield request.param
+    L.gs_set_binning(0)
+
+
 @pytest.mark.parametrize("cfg,n,views,level", [("tiny", None, 1, 0), ("tum", 60000, 1, 0), ("tum", 60000, 3, 2),
-                                               ("replica", 40000, 2, 1)])
-def test_preprocess_and_binning_bit_exact(cfg, n, views, level):
+                                               ("replica", 40000, 2, 1), ("tum", None, 1, 2)])
+def test_preprocess_and_binning_bit_exact(cfg, n, views, level, binning):
+    """Both binning paths (tile buckets + in-tile sort; global onesweep radix sort) give the
+    oracle's keys, values and ranges bit for bit (SURVEY §8(c) contract item 2)."""
     scene = make_scene(cfg, n=n)
     cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
     r, params, D = _renderer(scene, cams)
@@ -144,6 +153,29 @@ def _check_colour(got_rgb, got_T, ref, pixels_mask=None):
     assert d[ok].max(initial=0) <= 1e-4, d[ok].max()
     assert dT[ok].max(initial=0) <= 1e-4, dT[ok].max()
     assert d[flag].max(initial=0) <= 1.1e-2
+
+
+def test_long_tile_bucket_global_fallback():
+    """A tile list longer than the in-tile shared-memory sort (4096 pairs) takes the global-memory
+    network; it must still match the oracle's binning exactly."""
+    from tests.helpers import camera, scene_of
+    rng = np.random.default_rng(5)
+    n = 6000
+    means = np.stack([rng.uniform(-0.02, 0.02, n), rng.uniform(-0.02, 0.02, n), rng.uniform(1.0, 3.0, n)], 1)
+    scene = scene_of(means, log_scales=np.full((n, 3), np.log(0.002)), D=0)
+    scene.depth_ties = None
+    cams = [camera(width=64, height=48, cx=32, cy=24, fx=60, fy=60)]
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    torch.cuda.synchronize()
+    keys, vals, ranges, tt = orc.bin_pairs(scene, cams)
+    assert (ranges[:, 1] - ranges[:, 0]).max() > 4096
+    v = r.ws.views()
+    st, flags, P = r.ws.status()
+    assert P == keys.size
+    np.testing.assert_array_equal(v["keys"][:P].cpu().numpy().view(np.uint64), keys)
+    np.testing.assert_array_equal(v["vals"][:P].cpu().numpy().view(np.uint32), vals)
+    np.testing.assert_array_equal(v["ranges"].cpu().numpy().view(np.uint32), ranges)
 
 
 def test_forward_parity_tiny_full_image():
