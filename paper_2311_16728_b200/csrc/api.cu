@@ -60,6 +60,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.tile_start = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.tile_cursor = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
     L.bin_big = take((size_t)2 * L.cap * sizeof(uint64_t));
+    L.prec = take((size_t)3 * L.cap * sizeof(float4));
     L.sort_look = take((size_t)SORT_MAX_PASSES * std::max<int64_t>(L.sort_blocks, 1) * SORT_RADIX * sizeof(uint32_t));
     L.total = o;
     return L;
@@ -68,8 +69,9 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
 bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out) {
     Layout L0 = make_layout(n, V, W, H, 0);
     if (L0.total > ws_bytes) return false;
-    // bytes per SORT_TILE pairs: 2 x (8 + 4) + 16 (bucket overflow) per pair + look-back words
-    size_t per_tile = (size_t)SORT_TILE * 40 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
+    // bytes per SORT_TILE pairs: 2 x (8 + 4) + 16 (bucket overflow) + 48 (pair record) per pair
+    // + look-back words
+    size_t per_tile = (size_t)SORT_TILE * 88 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
     int64_t tiles = (int64_t)((ws_bytes - L0.total) / per_tile) + 1;
     for (; tiles >= 0; tiles--) {
         Layout L = make_layout(n, V, W, H, tiles * SORT_TILE);
@@ -245,6 +247,7 @@ gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int3
                             at<uint32_t>(ws, L.sort_look), L.sort_blocks, s);
         if (e == cudaSuccess) e = launch_ranges(L, ws, s);
     }
+    if (e == cudaSuccess) e = launch_gather_pairs(L, ws, s);
     if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s);
     if (e != cudaSuccess) return GS_ERR_CUDA;
     std::lock_guard<std::mutex> g(g_mu);

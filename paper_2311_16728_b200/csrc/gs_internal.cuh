@@ -54,6 +54,7 @@ struct Layout {
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
     size_t tile_count, tile_start, tile_cursor, bin_big;  // bucket binning (bin.cu)
+    size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
     size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, ncomp, Tfinal, total;
 };
 
@@ -94,6 +95,7 @@ cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, 
                         int64_t cap, int key_bits, WsHeader *hdr, uint32_t *lookback, int64_t sort_blocks,
                         cudaStream_t s);
 cudaError_t launch_ranges(const Layout &L, void *ws, cudaStream_t s);
+cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s);
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);

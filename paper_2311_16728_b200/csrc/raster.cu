@@ -6,14 +6,21 @@
 // (Mahalanobis^2 > 9, R9) or power > 0; alpha = min(0.99, sigma e^power) (R7); skip alpha
 // < 1/255; stop the pixel when T (1 - alpha) < 1e-4 (R8).
 //
-// Layout: one 256-thread CTA per (view, 16x16 tile), one thread per pixel; each warp owns an
-// 8x4 pixel block (2 x 4 blocks per tile).  Gaussian records are staged in shared memory in
-// batches of 256; each warp then builds, in parallel over the batch (one Gaussian per lane,
-// ballot + popc), the ordered list of Gaussians that can reach its block: the exact minimum of
-// d^T Q d over the block is compared with the Gaussian's limit min(9, 2 ln(255 sigma)) (3-sigma
+// Data movement: after binning, k_gather_pairs writes one 48-byte record per (tile, Gaussian)
+// pair in sorted order -- (u, v, A, B), (C, sigma, r, g), (b, id, -, q_limit) -- so a tile's
+// list is one contiguous range.  The raster kernels stream it into shared memory with TMA
+// bulk copies (cp.async.bulk + mbarrier complete_tx), double-buffered: the copy of batch b+1
+// is in flight while batch b is composited, and no thread waits on dependent gathers.
+//
+// Layout: one thread per pixel; each warp owns an 8x4 pixel block (2 x 4 blocks per 16x16
+// tile); a CTA holds 8 warps (a whole tile) or, at pyramid levels with fewer tiles than
+// 4 x SMs, 2 or 1 warps (several CTAs per tile) so that every SM gets work.  For every batch
+// of 256 records each warp builds, in parallel over the batch (one record per lane, ballot +
+// popc), the ordered list of Gaussians that can reach its block: the exact minimum of d^T Q d
+// over the block is compared with the Gaussian's limit min(9, 2 ln(255 sigma)) (3-sigma
 // cutoff or alpha >= 1/255), padded so the test is conservative.  The sequential per-pixel
-// loop then only visits that list -- no pixel result changes.  The CTA leaves as soon as every
-// pixel of the tile has stopped.
+// loop only visits that list -- no pixel result changes.  A CTA leaves as soon as all of its
+// pixels have stopped.
 //
 // The backward replays each pixel's list back to front: dL/dc, dL/dalpha
 // = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  The nine
@@ -32,6 +39,7 @@ constexpr float ALPHA_MAX = 0.99f;
 constexpr float ALPHA_MIN = 1.0f / 255.0f;
 constexpr float T_STOP = 1e-4f;
 constexpr float POWER_CUT = -4.5f;
+constexpr int BATCH = 256;  // records per staged batch (list indices fit in a byte)
 
 // power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order
 __device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float C, float &dx, float &dy) {
@@ -80,64 +88,133 @@ __device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, f
     return best > qlim * 1.001f + 1e-3f;
 }
 
-// thread -> pixel: warp w covers the 8x4 block (w & 1, w >> 1) of the tile
-__device__ __forceinline__ void pixel_of(int tid, int &lx, int &ly) {
-    int w = tid >> 5, l = tid & 31;
-    lx = (w & 1) * 8 + (l & 7);
-    ly = (w >> 1) * 4 + (l >> 3);
+// ---------------------------------------------------------------- per-pair records (gather)
+// rec[pos] = (u, v, A, B) | (C, sigma, r, g) | (b, id bits, 0, q_limit(sigma)), pos < P.
+__global__ void __launch_bounds__(256) k_gather_pairs(const uint32_t *__restrict__ vals,
+                                                      const uint64_t *__restrict__ keys,
+                                                      const float4 *__restrict__ rec0,
+                                                      const float4 *__restrict__ rec1,
+                                                      const float4 *__restrict__ rec2, int64_t n, int tiles,
+                                                      const uint32_t *count, int64_t cap,
+                                                      float4 *__restrict__ prec) {
+    uint32_t P = *count;
+    if (P > cap) P = 0;  // overflow: nothing valid to gather
+    for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < P;
+         pos += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t gi = vals[pos];
+        const int64_t view = (int64_t)(keys[pos] >> 32) / tiles;
+        const int64_t m = view * n + gi;
+        const float4 r1 = rec1[m];
+        prec[3 * pos] = rec0[m];
+        prec[3 * pos + 1] = r1;
+        prec[3 * pos + 2] = make_float4(rec2[m].x, __uint_as_float(gi), 0.f, q_limit(r1.y));
+    }
 }
 
-__global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restrict__ ranges,
-                                                          const uint32_t *__restrict__ vals,
-                                                          const float4 *__restrict__ rec0,
-                                                          const float4 *__restrict__ rec1,
-                                                          const float4 *__restrict__ rec2, int64_t n, int W, int H,
-                                                          int TX, int tiles, float bg0, float bg1, float bg2,
-                                                          float *__restrict__ out_rgb, float *__restrict__ out_T,
-                                                          float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib,
-                                                          uint32_t *__restrict__ ncomp) {
-    __shared__ float4 s0[BLOCK_PIX];
-    __shared__ float4 s1[BLOCK_PIX];
-    __shared__ float4 s2[BLOCK_PIX];
-    __shared__ uint8_t wl[BLOCK_PIX / 32][BLOCK_PIX];
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+// one elected thread: expect `bytes` on the barrier and start the global -> shared bulk copy
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct RasterSmem {
+    float4 rec[2][BATCH * 3];  // double-buffered batch of pair records (2 x 12 KB)
+    uint64_t bar[2];
+};
+
+// CTA = WARPS warps of one 16x16 tile: blockIdx.x = tile_x * (8 / WARPS) + sub-tile.
+template <int WARPS>
+__device__ __forceinline__ void warp_block(int &tile_x, int &wx0, int &wy0, int &lx, int &ly) {
+    constexpr int SUB = 8 / WARPS;
+    const int sub = blockIdx.x % SUB;
+    tile_x = blockIdx.x / SUB;
+    const int wg = sub * WARPS + (threadIdx.x >> 5);  // warp block index 0..7 within the tile
+    const int lane = threadIdx.x & 31;
+    wx0 = (wg & 1) * 8;
+    wy0 = (wg >> 1) * 4;
+    lx = wx0 + (lane & 7);
+    ly = wy0 + (lane >> 3);
+}
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restrict__ ranges,
+                                                           const float4 *__restrict__ prec, int W, int H, int TX,
+                                                           int tiles, float bg0, float bg1, float bg2,
+                                                           float *__restrict__ out_rgb, float *__restrict__ out_T,
+                                                           float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib,
+                                                           uint32_t *__restrict__ ncomp) {
+    constexpr int NT = WARPS * 32;
+    __shared__ __align__(128) RasterSmem S;
+    __shared__ uint8_t wl[WARPS][BATCH];
     const int view = blockIdx.z;
-    const int tile = blockIdx.y * TX + blockIdx.x;
+    int tile_x, bx0, by0, lx, ly;
+    warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
+    const int tile = blockIdx.y * TX + tile_x;
     const int tid = threadIdx.x;
-    int lx, ly;
-    pixel_of(tid, lx, ly);
-    const int px = blockIdx.x * TILE + lx;
+    const int px = tile_x * TILE + lx;
     const int py = blockIdx.y * TILE + ly;
-    const float wx0 = (float)(blockIdx.x * TILE + ((tid >> 5) & 1) * 8);
-    const float wy0 = (float)(blockIdx.y * TILE + (tid >> 6) * 4);
+    const float wx0 = (float)(tile_x * TILE + bx0);
+    const float wy0 = (float)(blockIdx.y * TILE + by0);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const int todo_all = (int)(range.y - range.x);
     const float fx = (float)px, fy = (float)py;
-    const int64_t vbase = (int64_t)view * n;
     float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f;
     uint32_t last = 0, composited = 0;
     bool done = !inside;
     const int warp = tid >> 5, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
-    for (int b0 = 0; b0 < todo_all; b0 += BLOCK_PIX) {
-        if (__syncthreads_count(done) == BLOCK_PIX) break;
-        int idx = b0 + tid;
-        if (idx < todo_all) {
-            int64_t m = vbase + vals[range.x + idx];
-            float4 r1 = rec1[m], r2 = rec2[m];
-            r2.w = q_limit(r1.y);
-            s0[tid] = rec0[m];
-            s1[tid] = r1;
-            s2[tid] = r2;
+    const float4 *src = prec + 3 * (size_t)range.x;
+    if (tid == 0) {
+        mbar_init(&S.bar[0]);
+        mbar_init(&S.bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (todo_all > 0) bulk_load(S.rec[0], src, (uint32_t)min(BATCH, todo_all) * 48u, &S.bar[0]);
+    }
+    __syncthreads();
+    uint32_t phase[2] = {0u, 0u};
+    int inflight = todo_all > 0 ? 0 : -1;  // buffer with an unconsumed copy (-1: none)
+    for (int b0 = 0, it = 0; b0 < todo_all; b0 += BATCH, it++) {
+        const int buf = it & 1;
+        if (__syncthreads_count(done) == NT) break;
+        const int cnt = min(BATCH, todo_all - b0);
+        if (tid == 0 && b0 + BATCH < todo_all) {  // prefetch the next batch into the other buffer
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b0 + BATCH),
+                      (uint32_t)min(BATCH, todo_all - b0 - BATCH) * 48u, &S.bar[buf ^ 1]);
         }
-        __syncthreads();
-        const int cnt = min(BLOCK_PIX, todo_all - b0);
-        // phase 1 (parallel over the batch): ordered list of the Gaussians whose padded
-        // 3-sigma box meets this warp's 8x4 block
+        mbar_wait(&S.bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        inflight = b0 + BATCH < todo_all ? (buf ^ 1) : -1;
+        const float4 *r = S.rec[buf];
+        // phase 1 (parallel over the batch): ordered list of the Gaussians that can reach this
+        // warp's 8x4 block
         int nsel = 0;
         for (int k = 0; k < cnt; k += 32) {
             int j = k + lane;
-            bool hit = j < cnt && !block_misses(s0[j], s1[j], s2[j].w, wx0, wy0);
+            bool hit = j < cnt && !block_misses(r[3 * j], r[3 * j + 1], r[3 * j + 2].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
             if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
             nsel += __popc(b);
@@ -147,9 +224,8 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
         for (int t = 0; t < nsel; t++) {
             if (__all_sync(0xffffffffu, done)) break;
             const int j = wl[warp][t];
-            float4 g0 = s0[j];
-            float4 g1 = s1[j];
-            float4 g2 = s2[j];
+            float4 g0 = r[3 * j];
+            float4 g1 = r[3 * j + 1];
             float dx, dy;
             float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
             if (done || power > 0.0f || power < POWER_CUT) continue;
@@ -163,12 +239,14 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_fwd(const uint2 *__restric
             float w = alpha * T;
             c0 += g1.z * w;
             c1 += g1.w * w;
-            c2 += g2.x * w;
+            c2 += r[3 * j + 2].x * w;
             T = test_T;
             composited++;
             last = (uint32_t)(b0 + j + 1);  // 1-based list position of the last composited
         }
     }
+    // never leave with a bulk copy still writing into this CTA's shared memory
+    if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], phase[inflight]);
     if (inside) {
         int64_t HW = (int64_t)H * W;
         int64_t pix = (int64_t)py * W + px;
@@ -216,31 +294,26 @@ __device__ __forceinline__ float warp_sum8_transposed(float a[8], int lane) {
     return r;
 }
 
-__global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restrict__ ranges,
-                                                          const uint32_t *__restrict__ vals,
-                                                          const float4 *__restrict__ rec0,
-                                                          const float4 *__restrict__ rec1,
-                                                          const float4 *__restrict__ rec2, int64_t n, int W, int H,
-                                                          int TX, int tiles, float bg0, float bg1, float bg2,
-                                                          const float *__restrict__ dL_drgb,
-                                                          const float *__restrict__ T_keep,
-                                                          const uint32_t *__restrict__ ncontrib,
-                                                          float4 *__restrict__ g2d) {
-    __shared__ float4 s0[BLOCK_PIX];
-    __shared__ float4 s1[BLOCK_PIX];
-    __shared__ float4 s2[BLOCK_PIX];
-    __shared__ uint32_t sid[BLOCK_PIX];
-    __shared__ uint8_t wl[BLOCK_PIX / 32][BLOCK_PIX];
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restrict__ ranges,
+                                                           const float4 *__restrict__ prec, int64_t n, int W, int H,
+                                                           int TX, int tiles, float bg0, float bg1, float bg2,
+                                                           const float *__restrict__ dL_drgb,
+                                                           const float *__restrict__ T_keep,
+                                                           const uint32_t *__restrict__ ncontrib,
+                                                           float4 *__restrict__ g2d) {
+    __shared__ __align__(128) RasterSmem S;
+    __shared__ uint8_t wl[WARPS][BATCH];
     __shared__ uint32_t s_maxlast;
     const int view = blockIdx.z;
-    const int tile = blockIdx.y * TX + blockIdx.x;
+    int tile_x, bx0, by0, lx, ly;
+    warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
+    const int tile = blockIdx.y * TX + tile_x;
     const int tid = threadIdx.x, lane = tid & 31;
-    int lx, ly;
-    pixel_of(tid, lx, ly);
-    const int px = blockIdx.x * TILE + lx;
+    const int px = tile_x * TILE + lx;
     const int py = blockIdx.y * TILE + ly;
-    const float wx0 = (float)(blockIdx.x * TILE + ((tid >> 5) & 1) * 8);
-    const float wy0 = (float)(blockIdx.y * TILE + (tid >> 6) * 4);
+    const float wx0 = (float)(tile_x * TILE + bx0);
+    const float wy0 = (float)(blockIdx.y * TILE + by0);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const float fx = (float)px, fy = (float)py;
@@ -257,7 +330,12 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
         g_1 = g[HW];
         g_2 = g[2 * HW];
     }
-    if (tid == 0) s_maxlast = 0;
+    if (tid == 0) {
+        s_maxlast = 0;
+        mbar_init(&S.bar[0]);
+        mbar_init(&S.bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     // the warp's own furthest composited position bounds its work; the CTA's bounds the batches
     uint32_t wlast = last;
@@ -266,44 +344,47 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
     if (lane == 0) atomicMax(&s_maxlast, wlast);
     __syncthreads();
     const int todo_all = (int)s_maxlast;
+    const float4 *src = prec + 3 * (size_t)range.x;
+    // batches cover list positions [b_end - cnt, b_end), walked from the back
+    if (tid == 0 && todo_all > 0) {
+        int cnt0 = min(BATCH, todo_all);
+        bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
+    }
+    uint32_t phase[2] = {0u, 0u};
     float acc0 = bg0, acc1 = bg1, acc2 = bg2;
-    // process positions todo_all .. 1 (1-based within the tile range), batches from the back
-    for (int b_end = todo_all; b_end > 0; b_end -= BLOCK_PIX) {
-        int b_start = max(0, b_end - BLOCK_PIX);
-        int cnt = b_end - b_start;
-        __syncthreads();
-        if (tid < cnt) {
-            int pos = b_end - 1 - tid;  // s[tid] holds 0-based position b_end-1-tid (back to front)
-            uint32_t gi = vals[range.x + pos];
-            int64_t m = vbase + gi;
-            sid[tid] = gi;
-            float4 r1 = rec1[m], r2 = rec2[m];
-            r2.w = q_limit(r1.y);
-            s0[tid] = rec0[m];
-            s1[tid] = r1;
-            s2[tid] = r2;
+    const int warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
+        const int buf = it & 1;
+        const int cnt = min(BATCH, b_end);
+        const int b_start = b_end - cnt;
+        __syncthreads();  // everyone is done with the other buffer
+        if (tid == 0 && b_start > 0) {
+            int cn = min(BATCH, b_start);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
         }
-        __syncthreads();
+        mbar_wait(&S.bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const float4 *r = S.rec[buf];
         // phase 1: ordered (back to front) list of the batch entries this warp must replay --
-        // at or before its furthest composited position and with a box meeting its block
-        const int warp = tid >> 5;
-        const unsigned lt = (1u << lane) - 1u;
-        const int j0 = (uint32_t)b_end > wlast ? (int)((uint32_t)b_end - wlast) : 0;
+        // at or before its furthest composited position and able to reach its block
         int nsel = 0;
         for (int k = 0; k < cnt; k += 32) {
-            int j = k + lane;
-            bool hit = j < cnt && j >= j0 && !block_misses(s0[j], s1[j], s2[j].w, wx0, wy0);
+            const int jj = k + lane;
+            const int idx = cnt - 1 - jj;  // batch slot; list position b_start + idx + 1
+            bool hit = jj < cnt && (uint32_t)(b_start + idx + 1) <= wlast &&
+                       !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
+            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
             nsel += __popc(b);
         }
         __syncwarp();
         for (int t = 0; t < nsel; t++) {
             const int j = wl[warp][t];
-            const uint32_t position = (uint32_t)(b_end - j);  // 1-based position in the tile list
-            float4 g0 = s0[j];
-            float4 g2 = s2[j];
-            float4 g1 = s1[j];
+            const uint32_t position = (uint32_t)(b_start + j + 1);  // 1-based position in the tile list
+            float4 g0 = r[3 * j];
+            float4 g1 = r[3 * j + 1];
             float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
             float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
             bool contrib = false;
@@ -321,7 +402,7 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                         dLdr = g_0 * w;
                         dLdg = g_1 * w;
                         dLdb = g_2 * w;
-                        float cr = g1.z, cg = g1.w, cb = g2.x;
+                        float cr = g1.z, cg = g1.w, cb = r[3 * j + 2].x;
                         float dLda = T * (g_0 * (cr - acc0) + g_1 * (cg - acc1) + g_2 * (cb - acc2));
                         acc0 = alpha * cr + (1.f - alpha) * acc0;
                         acc1 = alpha * cg + (1.f - alpha) * acc1;
@@ -344,33 +425,78 @@ __global__ void __launch_bounds__(BLOCK_PIX) k_raster_bwd(const uint2 *__restric
                 float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
                 float mine = warp_sum8_transposed(vals8, lane);
                 float bsum = warp_sum(dLdb);
-                float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + sid[j]));
+                const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
+                float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
                 if ((lane & 3) == 0)
                     atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
                 if (lane == 1) atomicAdd(dst + 8, bsum);
             }
         }
     }
+    // every issued copy was waited for inside the loop (the last batch issues none)
+}
+
+// Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
+// tile) at pyramid levels with few tiles so that every SM gets work.
+static int raster_warps(const Layout &L) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int64_t t = (int64_t)L.V * L.tiles;
+    if (t >= 4 * sms) return 8;
+    if (t >= sms) return 2;
+    return 1;
+}
+
+cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s) {
+    if (L.cap == 0) return cudaGetLastError();
+    const int blocks = (int)std::min<int64_t>((L.cap + 255) / 256, 148 * 16);
+    k_gather_pairs<<<blocks, 256, 0, s>>>(at<uint32_t>(ws, L.vals0), at<uint64_t>(ws, L.keys0), at<float4>(ws, L.rec0),
+                                          at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.tiles,
+                                          &at<WsHeader>(ws, L.hdr)->P, L.cap, at<float4>(ws, L.prec));
+    return cudaGetLastError();
+}
+
+template <int WARPS>
+static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T, cudaStream_t s) {
+    dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
+    k_raster_fwd<WARPS><<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX,
+                                                    L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T,
+                                                    at<float>(ws, L.Tfinal), at<uint32_t>(ws, L.ncontrib),
+                                                    at<uint32_t>(ws, L.ncomp));
+}
+
+template <int WARPS>
+static void bwd_launch(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
+    dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
+    k_raster_bwd<WARPS><<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H,
+                                                    L.TX, L.tiles, bg[0], bg[1], bg[2], dL_drgb,
+                                                    at<float>(ws, L.Tfinal), at<uint32_t>(ws, L.ncontrib),
+                                                    at<float4>(ws, L.grad2d));
 }
 
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s) {
-    dim3 grid(L.TX, L.TY, L.V);
     ProfScope prof("k_raster_fwd", s);
-    k_raster_fwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
-                                            at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
-                                            L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
-                                            at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp));
+    switch (raster_warps(L)) {
+        case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, s); break;
+        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, s); break;
+        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, s); break;
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
-    dim3 grid(L.TX, L.TY, L.V);
     ProfScope prof("k_raster_bwd", s);
-    k_raster_bwd<<<grid, BLOCK_PIX, 0, s>>>(at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.vals0), at<float4>(ws, L.rec0),
-                                            at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), L.n, L.W, L.H, L.TX,
-                                            L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
-                                            at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
+    switch (raster_warps(L)) {
+        case 8: bwd_launch<8>(L, ws, bg, dL_drgb, s); break;
+        case 2: bwd_launch<2>(L, ws, bg, dL_drgb, s); break;
+        default: bwd_launch<1>(L, ws, bg, dL_drgb, s); break;
+    }
     return cudaGetLastError();
 }
 
