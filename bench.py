@@ -172,12 +172,14 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def launches_per_iteration(key_bits: int, fused: bool) -> int:
+def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0) -> int:
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
-    duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, raster fwd (5 + passes);
-    loss (3); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
+    binning 0: bucket scatter, tile sort (2) / binning 1: duplicate, sort histogram, one pass per
+    8-bit digit, fixup, ranges (4 + passes); pair gather + raster fwd (2); loss (2); fused:
+    raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
-    return 2 + (5 + passes) + 3 + (3 if fused else 4)
+    binning_kernels = 2 if binning == 0 else 4 + passes
+    return 2 + binning_kernels + 2 + 2 + (3 if fused else 4)
 
 
 def run_ours(args):

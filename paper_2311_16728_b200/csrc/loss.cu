@@ -7,8 +7,9 @@
 // then a vertical 11-tap pass over the five moment maps (x, y, x^2, y^2, xy).  The gradient
 // is the windowed-correlation form: dSSIM/dx_p = (w * A)_p + 2 x_p (w * B)_p + y_p (w * C)_p
 // with A = dS/dmu_x, B = dS/dE[x^2], C = dS/dE[xy] per pixel, so a second kernel applies
-// the same separable window to the three partial maps.  Loss sums are reduced per CTA and
-// then per view in a fixed order (deterministic).
+// the same separable window to the three partial maps.  Loss sums are reduced per CTA; the
+// first CTA of each view in the gradient kernel (or a one-CTA-per-view kernel when no gradient
+// is requested) sums that view's partials in a fixed order (deterministic) and writes the loss.
 #include <cmath>
 
 #include "gs_internal.cuh"
@@ -18,6 +19,8 @@ namespace gsk {
 constexpr int LT = 16;          // output tile
 constexpr int HALO = 5;         // 11-tap window radius
 constexpr int LS = LT + 2 * HALO;  // 26
+constexpr int LSP = 48;         // padded row stride: the two half-warps of a row pass read
+                                // disjoint bank halves (48 = 16 mod 32)
 
 struct Win {
     float g[11];
@@ -42,7 +45,7 @@ constexpr float SS_C2 = 0.03f * 0.03f;
 __global__ void __launch_bounds__(LT *LT) k_ssim_fwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
                                                      int W, Win win, float *__restrict__ dA, float *__restrict__ dB,
                                                      float *__restrict__ dC, float2 *__restrict__ part) {
-    __shared__ float sx[LS][LS], sy[LS][LS];
+    __shared__ float sx[LS][LSP], sy[LS][LSP];
     __shared__ float h[5][LS][LT];
     __shared__ float red[2][LT * LT / 32];
     const int plane = blockIdx.z;  // v*3 + c
@@ -124,11 +127,48 @@ __global__ void __launch_bounds__(LT *LT) k_ssim_fwd(const float *__restrict__ X
     }
 }
 
+// Fixed-order sum of the 3 * nbt partials of view v with one CTA of 256 threads (deterministic).
+__device__ __forceinline__ void finalize_view(const float2 *__restrict__ part, int v, int nbt, float lambda,
+                                              float invN, float *loss) {
+    __shared__ double sa[8], sb[8];
+    double a = 0, b = 0;
+    for (int k = threadIdx.x; k < 3 * nbt; k += blockDim.x) {
+        const float2 p = part[(int64_t)v * 3 * nbt + k];
+        a += p.x;
+        b += p.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sa[threadIdx.x >> 5] = a;
+        sb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ta = 0, tb = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            ta += sa[w];
+            tb += sb[w];
+        }
+        loss[v] = (float)((1.0 - lambda) * ta * invN + lambda * (1.0 - tb * invN));
+    }
+}
+
+// loss only (no gradient requested): one CTA per view
+__global__ void __launch_bounds__(256) k_loss_final(const float2 *__restrict__ part, int nbt, float lambda, float invN,
+                                                    float *loss) {
+    finalize_view(part, blockIdx.x, nbt, lambda, invN, loss);
+}
+
 __global__ void __launch_bounds__(LT *LT) k_ssim_bwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
                                                      int W, Win win, float lambda, float invN,
                                                      const float *__restrict__ dA, const float *__restrict__ dB,
-                                                     const float *__restrict__ dC, float *__restrict__ dL) {
-    __shared__ float s[3][LS][LS];
+                                                     const float *__restrict__ dC, float *__restrict__ dL,
+                                                     const float2 *__restrict__ part, float *__restrict__ loss) {
+    __shared__ float s[3][LS][LSP];
     __shared__ float h[3][LS][LT];
     const int plane = blockIdx.z;
     const int64_t HW = (int64_t)H * W;
@@ -159,6 +199,9 @@ __global__ void __launch_bounds__(LT *LT) k_ssim_bwd(const float *__restrict__ X
     __syncthreads();
     const int r = tid / LT, c = tid % LT;
     const int gy = blockIdx.y * LT + r, gx = blockIdx.x * LT + c;
+    // the first CTA of each view also reduces that view's loss partials (written by k_ssim_fwd)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && plane % 3 == 0)
+        finalize_view(part, plane / 3, gridDim.x * gridDim.y, lambda, invN, loss);
     if (gy >= H || gx >= W) return;
     float sa = 0, sb = 0, sc = 0;
 #pragma unroll
@@ -176,29 +219,6 @@ __global__ void __launch_bounds__(LT *LT) k_ssim_bwd(const float *__restrict__ X
     dL[o] = (1.f - lambda) * sgn * invN - lambda * dssim * invN;
 }
 
-// one CTA per view: fixed-order sum of the per-CTA partials of its three planes
-__global__ void k_loss_final(const float2 *__restrict__ part, int nbt, float lambda, float invN, float *loss) {
-    __shared__ double sa[256], sb[256];
-    int v = blockIdx.x;
-    double a = 0, b = 0;
-    for (int k = threadIdx.x; k < 3 * nbt; k += blockDim.x) {
-        float2 p = part[(int64_t)v * 3 * nbt + k];
-        a += p.x;
-        b += p.y;
-    }
-    sa[threadIdx.x] = a;
-    sb[threadIdx.x] = b;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            sa[threadIdx.x] += sa[threadIdx.x + s];
-            sb[threadIdx.x] += sb[threadIdx.x + s];
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) loss[v] = (float)((1.0 - lambda) * sa[0] * invN + lambda * (1.0 - sb[0] * invN));
-}
-
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t loss_ws_bytes(int V, int H, int W) {
@@ -214,11 +234,13 @@ cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int 
     float *dA = at<float>(ws, 0), *dB = at<float>(ws, plane), *dC = at<float>(ws, 2 * plane);
     float2 *part = at<float2>(ws, 3 * plane);
     dim3 grid((W + LT - 1) / LT, (H + LT - 1) / LT, V * 3);
-    int nbt = grid.x * grid.y;
+    const int nbt = grid.x * grid.y;
     float invN = (float)(1.0 / (3.0 * H * W));
     k_ssim_fwd<<<grid, LT * LT, 0, s>>>(render, gt, H, W, win, dA, dB, dC, part);
-    if (dL) k_ssim_bwd<<<grid, LT * LT, 0, s>>>(render, gt, H, W, win, lambda, invN, dA, dB, dC, dL);
-    k_loss_final<<<V, 256, 0, s>>>(part, nbt, lambda, invN, loss);
+    if (dL)
+        k_ssim_bwd<<<grid, LT * LT, 0, s>>>(render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);
+    else
+        k_loss_final<<<V, 256, 0, s>>>(part, nbt, lambda, invN, loss);
     return cudaGetLastError();
 }
 

@@ -351,11 +351,16 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         const gs_camera &cam = cams.c[v];
         Proj p = project_recipe(cam, px, py, pz, cv, L.TX, L.TY);
         float4 ga = g2d[3 * m], gb = g2d[3 * m + 1];
-        float gu = ga.x, gv = ga.y, gA = ga.z, gB = ga.w, gC = gb.x;
+        // the raster backward accumulated moments over pixels: S(a), S(b), S(a dx), S(a dy),
+        // S(b dy) with a = dL/dpower dx, b = dL/dpower dy (d = pixel - mean2d); with the conic
+        // (A, B, C) of this view: dL/du = A S(a) + B S(b), dL/dv = B S(a) + C S(b),
+        // dL/dA = -S(a dx)/2, dL/dB = -S(a dy), dL/dC = -S(b dy)/2
+        float A = p.A, B = p.B, C = p.C;
+        float gu = A * ga.x + B * ga.y, gv = B * ga.x + C * ga.y;
+        float gA = -0.5f * ga.z, gB = -ga.w, gC = -0.5f * gb.x;
         gop += gb.y;
         norm_acc += sqrtf(gu * gu + gv * gv);
         // conic Q = Sigma2'^-1 : dL/dSigma2 = -Q G Q, G = [[gA, gB/2], [gB/2, gC]]
-        float A = p.A, B = p.B, C = p.C;
         float hB = 0.5f * gB;
         float QG00 = A * gA + B * hB, QG01 = A * hB + B * gC;
         float QG10 = B * gA + C * hB, QG11 = B * hB + C * gC;

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         if (todo_all > 0) bulk_load(S.rec[0], src, (uint32_t)min(BATCH, todo_all) * 48u, &S.bar[0]);
     }
     __syncthreads();
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phases = 0u;                  // bit b = parity to wait for on buffer b
     int inflight = todo_all > 0 ? 0 : -1;  // buffer with an unconsumed copy (-1: none)
     for (int b0 = 0, it = 0; b0 < todo_all; b0 += BATCH, it++) {
         const int buf = it & 1;
@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
             bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b0 + BATCH),
                       (uint32_t)min(BATCH, todo_all - b0 - BATCH) * 48u, &S.bar[buf ^ 1]);
         }
-        mbar_wait(&S.bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
+        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
         inflight = b0 + BATCH < todo_all ? (buf ^ 1) : -1;
         const float4 *r = S.rec[buf];
         // phase 1 (parallel over the batch): ordered list of the Gaussians that can reach this
@@ -221,32 +221,54 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         }
         __syncwarp();
         // phase 2 (sequential per pixel): composite the warp's list front to back
-        for (int t = 0; t < nsel; t++) {
+        // two list entries per step: their alphas are independent, only the compositing
+        // recurrence (T, C) is sequential, so the SFU/FMA latency of the second overlaps the first
+        for (int t = 0; t < nsel; t += 2) {
             if (__all_sync(0xffffffffu, done)) break;
-            const int j = wl[warp][t];
-            float4 g0 = r[3 * j];
-            float4 g1 = r[3 * j + 1];
-            float dx, dy;
-            float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
-            if (done || power > 0.0f || power < POWER_CUT) continue;
-            float alpha = fminf(ALPHA_MAX, g1.y * fast_exp(power));
-            if (alpha < ALPHA_MIN) continue;
-            float test_T = T * (1.0f - alpha);
-            if (test_T < T_STOP) {
-                done = true;
-                continue;
+            const int ja = wl[warp][t];
+            const bool has_b = t + 1 < nsel;
+            const int jb = has_b ? wl[warp][t + 1] : ja;
+            const float4 a0 = r[3 * ja], a1 = r[3 * ja + 1];
+            const float4 b0v = r[3 * jb], b1 = r[3 * jb + 1];
+            float dxa, dya, dxb, dyb;
+            const float pa = pixel_power(fx, fy, a0, a1.x, dxa, dya);
+            const float pb = pixel_power(fx, fy, b0v, b1.x, dxb, dyb);
+            const float alpha_a = fminf(ALPHA_MAX, a1.y * fast_exp(pa));
+            const float alpha_b = fminf(ALPHA_MAX, b1.y * fast_exp(pb));
+            const bool va = !(pa > 0.0f || pa < POWER_CUT) && alpha_a >= ALPHA_MIN;
+            const bool vb = has_b && !(pb > 0.0f || pb < POWER_CUT) && alpha_b >= ALPHA_MIN;
+            if (!done && va) {
+                const float test_T = T * (1.0f - alpha_a);
+                if (test_T < T_STOP) {
+                    done = true;
+                } else {
+                    const float w = alpha_a * T;
+                    c0 += a1.z * w;
+                    c1 += a1.w * w;
+                    c2 += r[3 * ja + 2].x * w;
+                    T = test_T;
+                    composited++;
+                    last = (uint32_t)(b0 + ja + 1);  // 1-based list position of the last composited
+                }
             }
-            float w = alpha * T;
-            c0 += g1.z * w;
-            c1 += g1.w * w;
-            c2 += r[3 * j + 2].x * w;
-            T = test_T;
-            composited++;
-            last = (uint32_t)(b0 + j + 1);  // 1-based list position of the last composited
+            if (!done && vb) {
+                const float test_T = T * (1.0f - alpha_b);
+                if (test_T < T_STOP) {
+                    done = true;
+                } else {
+                    const float w = alpha_b * T;
+                    c0 += b1.z * w;
+                    c1 += b1.w * w;
+                    c2 += r[3 * jb + 2].x * w;
+                    T = test_T;
+                    composited++;
+                    last = (uint32_t)(b0 + jb + 1);
+                }
+            }
         }
     }
     // never leave with a bulk copy still writing into this CTA's shared memory
-    if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], phase[inflight]);
+    if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], (phases >> inflight) & 1u);
     if (inside) {
         int64_t HW = (int64_t)H * W;
         int64_t pix = (int64_t)py * W + px;
@@ -350,7 +372,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restri
         int cnt0 = min(BATCH, todo_all);
         bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
     }
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phases = 0u;  // bit b = parity to wait for on buffer b
     float acc0 = bg0, acc1 = bg1, acc2 = bg2;
     const int warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -364,8 +386,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restri
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
         }
-        mbar_wait(&S.bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
+        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
         const float4 *r = S.rec[buf];
         // phase 1: ordered (back to front) list of the batch entries this warp must replay --
         // at or before its furthest composited position and able to reach its block
@@ -402,26 +424,29 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restri
                         dLdr = g_0 * w;
                         dLdg = g_1 * w;
                         dLdb = g_2 * w;
-                        float cr = g1.z, cg = g1.w, cb = r[3 * j + 2].x;
-                        float dLda = T * (g_0 * (cr - acc0) + g_1 * (cg - acc1) + g_2 * (cb - acc2));
-                        acc0 = alpha * cr + (1.f - alpha) * acc0;
-                        acc1 = alpha * cg + (1.f - alpha) * acc1;
-                        acc2 = alpha * cb + (1.f - alpha) * acc2;
+                        const float d0 = g1.z - acc0, d1 = g1.w - acc1, d2 = r[3 * j + 2].x - acc2;
+                        float dLda = T * (g_0 * d0 + g_1 * d1 + g_2 * d2);
+                        acc0 += alpha * d0;  // acc <- alpha c + (1 - alpha) acc
+                        acc1 += alpha * d1;
+                        acc2 += alpha * d2;
                         if (!(a_raw > ALPHA_MAX)) {
                             dLdsig = e * dLda;
-                            float dLdp = alpha * dLda;
-                            float A = g0.z, B = g0.w, C = g1.x;
-                            dLdu = dLdp * (A * dx + B * dy);
-                            dLdv = dLdp * (C * dy + B * dx);
-                            dLdA = -0.5f * dx * dx * dLdp;
-                            dLdB = -dx * dy * dLdp;
-                            dLdC = -0.5f * dy * dy * dLdp;
+                            // moments a = dL/dpower dx, b = dL/dpower dy, a dx, a dy, b dy; the
+                            // projection backward turns their sums into dL/du = A S(a) + B S(b),
+                            // dL/dv = B S(a) + C S(b), dL/dA = -S(a dx)/2, dL/dB = -S(a dy),
+                            // dL/dC = -S(b dy)/2 (the conic is constant per Gaussian and view)
+                            const float dLdp = alpha * dLda;
+                            dLdu = dLdp * dx;
+                            dLdv = dLdp * dy;
+                            dLdA = dLdu * dx;
+                            dLdB = dLdu * dy;
+                            dLdC = dLdv * dy;
                         }
                     }
                 }
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                // per-(view, Gaussian) record: [u, v, A, B | C, sigma, r, g | b, -, -, -]
+                // per-(view, Gaussian) record: [S(a), S(b), S(a dx), S(a dy) | S(b dy), sigma, r, g | b, -]
                 float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
                 float mine = warp_sum8_transposed(vals8, lane);
                 float bsum = warp_sum(dLdb);
@@ -447,7 +472,7 @@ static int raster_warps(const Layout &L) {
         if (sms <= 0) sms = 148;
     }
     const int64_t t = (int64_t)L.V * L.tiles;
-    if (t >= 4 * sms) return 8;
+    if (t >= 2 * sms) return 8;
     if (t >= sms) return 2;
     return 1;
 }

@@ -44,6 +44,8 @@ def test_pack_unpack_roundtrip():
 
 def test_launch_accounting_matches_design():
     import bench
-    # 43 key bits -> 6 digit passes
-    assert bench.launches_per_iteration(43, True) == 2 + 5 + 6 + 3 + 3
-    assert bench.launches_per_iteration(43, False) == bench.launches_per_iteration(43, True) + 1
+    # bucket binning: preprocess, scan, scatter, tile sort, gather, raster, 2 loss, 3 fused bwd
+    assert bench.launches_per_iteration(43, True) == 11
+    assert bench.launches_per_iteration(43, False) == 12
+    # radix binning, 43 key bits -> 6 digit passes
+    assert bench.launches_per_iteration(43, True, binning=1) == 2 + (4 + 6) + 2 + 2 + 3
