@@ -141,11 +141,13 @@ gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int
    gradient buffer followed by gs_adam_step(..., 0, n, ...) -- bitwise -- but never writes or
    reads the N x K gradient array (K9/K11 fusion).  Single-GPU path: with data
    parallelism the gradient must be all-reduced, use the two separate calls.  After this call
-   the forward state of ws is stale (the parameters changed). */
+   the forward state of ws is stale (the parameters changed).
+   step > 0: the 1-based step number.  step == 0: device-resident step counter (for CUDA-graph
+   replay): the call increments *step_dev (int64, device) on the device and uses the new value. */
 gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
                                   size_t ws_bytes, const float bg[3], const float *dL_drgb, float *m, float *v,
-                                  const gs_adam_hparams *hp, int64_t step, float *grad2d_norm_accum,
-                                  gs_stream_t stream);
+                                  const gs_adam_hparams *hp, int64_t step, int64_t *step_dev,
+                                  float *grad2d_norm_accum, gs_stream_t stream);
 
 /* A0: Gaussian pyramid (Eq. 5): level l+1 = even rows/cols of the level-l
    image blurred by [1,4,6,4,1]/16 horizontally then vertically with a reflect-101 border

@@ -194,12 +194,15 @@ def gs_render_backward(params: GsParams, cams, ws: torch.Tensor, bg, dL_drgb: to
 
 
 def gs_render_backward_adam(params: GsParams, cams, ws: torch.Tensor, bg, dL_drgb: torch.Tensor, m, v,
-                            hp: GsAdamHparams, step: int, grad2d_norm: torch.Tensor | None = None, stream=None):
+                            hp: GsAdamHparams, step: int, grad2d_norm: torch.Tensor | None = None, stream=None,
+                            step_dev: torch.Tensor | None = None):
+    """step > 0: host step number; step == 0: device int64 counter step_dev (graph replay)."""
     ca = camera_struct(cams)
     bga = (C.c_float * 3)(*[float(x) for x in bg])
     _check(lib().gs_render_backward_adam(C.byref(params), ca, C.c_int32(len(ca)), _ptr(ws), C.c_size_t(ws.numel()),
                                          bga, _ptr(dL_drgb), _ptr(m), _ptr(v), C.byref(hp), C.c_int64(step),
-                                         _ptr(grad2d_norm), _stream(stream)), "gs_render_backward_adam")
+                                         _ptr(step_dev), _ptr(grad2d_norm), _stream(stream)),
+           "gs_render_backward_adam")
 
 
 def gs_pyramid(img: torch.Tensor, n_levels: int, out: torch.Tensor, stream=None):

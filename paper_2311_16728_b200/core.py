@@ -109,10 +109,15 @@ class Renderer:
 
     def backward_adam(self, params: torch.Tensor, cams, dL_drgb: torch.Tensor, opt: "Adam",
                       grad2d_norm: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0)):
-        """A8 + A9 + A11 fused (single GPU): backward and the optimiser step without a gradient array."""
-        opt.t += 1
+        """A8 + A9 + A11 fused (single GPU): backward and the optimiser step without a gradient array.
+        With opt.device_step the step counter lives on the device (CUDA-graph replay)."""
         ps = L.params_struct(params, self.n, self.D)
-        L.gs_render_backward_adam(ps, cams, self.ws.buf, bg, dL_drgb, opt.m, opt.v, opt.hp, opt.t, grad2d_norm)
+        if opt.device_step:
+            L.gs_render_backward_adam(ps, cams, self.ws.buf, bg, dL_drgb, opt.m, opt.v, opt.hp, 0, grad2d_norm,
+                                      step_dev=opt.t_dev)
+        else:
+            opt.t += 1
+            L.gs_render_backward_adam(ps, cams, self.ws.buf, bg, dL_drgb, opt.m, opt.v, opt.hp, opt.t, grad2d_norm)
 
 
 class PhotometricLoss:
@@ -184,6 +189,13 @@ class Adam:
         self.m = torch.zeros_like(params)
         self.v = torch.zeros_like(params)
         self.t = 0
+        self.device_step = False  # True: fused steps count on the device (t_dev), for graph replay
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=params.device)
+
+    def use_device_step(self):
+        """Switch the fused backward+Adam to the device-resident step counter (keeps the count)."""
+        self.t_dev.fill_(self.t)
+        self.device_step = True
 
     def step(self, grads: torch.Tensor, zero_grads: bool = True, g_begin: int = 0, g_end: int | None = None):
         self.t += 1

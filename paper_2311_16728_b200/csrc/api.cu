@@ -294,13 +294,13 @@ gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int
 
 gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
                                   size_t ws_bytes, const float bg[3], const float *dL_drgb, float *m, float *v,
-                                  const gs_adam_hparams *hp, int64_t step, float *grad2d_norm_accum,
-                                  gs_stream_t stream) {
+                                  const gs_adam_hparams *hp, int64_t step, int64_t *step_dev,
+                                  float *grad2d_norm_accum, gs_stream_t stream) {
     gs_status st = check_params(params);
     if (st) return st;
     static thread_local CamBatch cb;
     if ((st = check_views(cams, n_views, &cb))) return st;
-    if (!ws || !bg || !dL_drgb || !hp || step < 1) return GS_ERR_INVALID_ARG;
+    if (!ws || !bg || !dL_drgb || !hp || step < 0 || (step == 0 && !step_dev)) return GS_ERR_INVALID_ARG;
     if (!hp->sgd_mode && (!m || !v)) return GS_ERR_INVALID_ARG;
     Layout L;
     if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
@@ -314,8 +314,9 @@ gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int3
     }
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = launch_raster_bwd(L, ws, bg, dL_drgb, s);
-    if (e == cudaSuccess) e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grad2d_norm_accum, s);
-    if (e == cudaSuccess) e = launch_adam_fused(*params, L, ws, m, v, *hp, step, s);
+    if (e == cudaSuccess)
+        e = launch_preprocess_bwd(*params, cb, n_views, L, ws, grad2d_norm_accum, s, step == 0 ? step_dev : nullptr);
+    if (e == cudaSuccess) e = launch_adam_fused(*params, L, ws, m, v, *hp, step, step == 0 ? step_dev : nullptr, s);
     return cuda_status(e);
 }
 

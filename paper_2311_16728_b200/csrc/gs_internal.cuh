@@ -67,6 +67,24 @@ __host__ __device__ inline T *at(void *ws, size_t off) {
     return reinterpret_cast<T *>(reinterpret_cast<char *>(ws) + off);
 }
 
+// Largest d^T Q d at which a Gaussian can still be composited: the 3-sigma cutoff (R9) or the
+// alpha >= 1/255 skip, alpha <= sigma e^(-q/2) (R7), whichever is tighter (-1: never composited).
+__device__ __forceinline__ float q_limit(float sigma) {
+    if (sigma * 255.0f < 1.0f) return -1.0f;
+    return fminf(9.0f, 2.0f * __logf(255.0f * sigma));
+}
+
+// 48-byte per-pair record consumed by the raster kernels (raster.cu):
+// (u, v, A, B) | (C, sigma, r, g) | (b, Gaussian id bits, 0, q_limit(sigma))
+__device__ __forceinline__ void write_pair_record(float4 *__restrict__ prec, int64_t pos,
+                                                  const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
+                                                  const float4 *__restrict__ rec2, int64_t m, uint32_t gi) {
+    const float4 r1 = rec1[m];
+    prec[3 * pos] = rec0[m];
+    prec[3 * pos + 1] = r1;
+    prec[3 * pos + 2] = make_float4(rec2[m].x, __uint_as_float(gi), 0.f, q_limit(r1.y));
+}
+
 int sort_passes(int key_bits);
 
 // Live per-kernel timing for the benchmark (gs_profile_kernel / gs_profile_read): events are
@@ -101,12 +119,12 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);
 // A9 into the compacted scratch (one row per parameter, one column per visible Gaussian)
 cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                                  float *grad2d_norm, cudaStream_t s);
+                                  float *grad2d_norm, cudaStream_t s, int64_t *step_inc = nullptr);
 // grads += scratch gathered back to the parameter layout (dense, coalesced)
 cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws, float *grads, cudaStream_t s);
 // fused A11: Adam over all Gaussians with the gradient gathered from the scratch (0 if invisible)
 cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, float *m, float *v,
-                              const gs_adam_hparams &hp, int64_t step, cudaStream_t s);
+                              const gs_adam_hparams &hp, int64_t step, const int64_t *step_dev, cudaStream_t s);
 cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int W, float lambda, float *loss,
                         float *dL, void *ws, cudaStream_t s);
 size_t loss_ws_bytes(int V, int H, int W);

@@ -325,8 +325,9 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
 template <int D>
 __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict__ P, int64_t n, int64_t ld,
                                                         const CamBatch cams, int V, Layout L, char *ws,
-                                                        float *__restrict__ gnorm) {
+                                                        float *__restrict__ gnorm, int64_t *step_inc) {
     constexpr int NC = (D + 1) * (D + 1);
+    if (step_inc && blockIdx.x == 0 && threadIdx.x == 0) *step_inc += 1;  // device step for the fused Adam
     const uint32_t nvis = at<WsHeader>(ws, L.hdr)->vis_count;
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nvis) return;
@@ -510,16 +511,16 @@ cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, c
 }
 
 cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
-                                  float *grad2d_norm, cudaStream_t s) {
+                                  float *grad2d_norm, cudaStream_t s, int64_t *step_inc) {
     int64_t blocks = (p.n + 127) / 128;  // grid sized for every Gaussian; threads past vis_count exit
     if (blocks == 0) return cudaGetLastError();
     char *w = (char *)ws;
     ProfScope prof("k_preprocess_bwd", s);
     switch (p.sh_degree) {
-        case 0: k_preprocess_bwd<0><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
-        case 1: k_preprocess_bwd<1><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
-        case 2: k_preprocess_bwd<2><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
-        default: k_preprocess_bwd<3><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm); break;
+        case 0: k_preprocess_bwd<0><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        case 1: k_preprocess_bwd<1><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        case 2: k_preprocess_bwd<2><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        default: k_preprocess_bwd<3><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
     }
     return cudaGetLastError();
 }

@@ -69,7 +69,23 @@ struct AdamArgs {
     float b1, b2, eps;
     float rs_bc2;     // 1 / sqrt(1 - beta2^t)
     int sgd, zero;
+    const int64_t *step_dev;  // non-null: t read on the device; lr[] hold the raw rates
 };
+
+// device-step mode: bias corrections from t = *step_dev, once per CTA
+__device__ __forceinline__ void adam_device_step(AdamArgs &a) {
+    if (!a.step_dev || a.sgd) return;
+    __shared__ float s_lr[6], s_rs;
+    if (threadIdx.x == 0) {
+        const double t = (double)*a.step_dev;
+        const double bc1 = 1.0 - pow((double)a.b1, t), bc2 = 1.0 - pow((double)a.b2, t);
+        for (int k = 0; k < 6; k++) s_lr[k] = (float)((double)a.lr[k] / bc1);
+        s_rs = (float)(1.0 / sqrt(bc2));
+    }
+    __syncthreads();
+    for (int k = 0; k < 6; k++) a.lr[k] = s_lr[k];
+    a.rs_bc2 = s_rs;
+}
 
 __device__ __forceinline__ int row_class(int row) {
     return row < 3 ? 0 : row < 7 ? 1 : row < 10 ? 2 : row == 10 ? 3 : row < 14 ? 4 : 5;
@@ -185,6 +201,7 @@ __global__ void __launch_bounds__(COL_THREADS) k_adam_fused(float *__restrict__ 
                                                             float *__restrict__ Vv, int64_t ld, int64_t n, int rows,
                                                             const uint32_t *__restrict__ slot,
                                                             const float *__restrict__ S, AdamArgs a) {
+    adam_device_step(a);
     const int64_t c4 = (int64_t)blockIdx.x * COL_THREADS + threadIdx.x;
     const int64_t i0 = c4 * 4;
     if (i0 >= n) return;
@@ -224,11 +241,13 @@ cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws
     return cudaGetLastError();
 }
 
-static AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero) {
+static AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero, const int64_t *step_dev = nullptr) {
     AdamArgs a;
+    a.step_dev = step_dev;
+    if (step_dev) step = 1;  // placeholder; the kernel derives the corrections from *step_dev
     double bc1 = 1.0 - std::pow((double)hp.beta1, (double)step);
     double bc2 = 1.0 - std::pow((double)hp.beta2, (double)step);
-    for (int k = 0; k < 6; k++) a.lr[k] = hp.sgd_mode ? hp.lr[k] : (float)((double)hp.lr[k] / bc1);
+    for (int k = 0; k < 6; k++) a.lr[k] = (hp.sgd_mode || step_dev) ? hp.lr[k] : (float)((double)hp.lr[k] / bc1);
     a.b1 = hp.beta1;
     a.b2 = hp.beta2;
     a.eps = hp.eps;
@@ -239,8 +258,8 @@ static AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero) {
 }
 
 cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, float *m, float *v,
-                              const gs_adam_hparams &hp, int64_t step, cudaStream_t s) {
-    AdamArgs a = adam_args(hp, step, 0);
+                              const gs_adam_hparams &hp, int64_t step, const int64_t *step_dev, cudaStream_t s) {
+    AdamArgs a = adam_args(hp, step, 0, step_dev);
     int64_t cols4 = (p.n + 3) / 4;
     if (cols4 == 0) return cudaGetLastError();
     dim3 grid((unsigned)((cols4 + COL_THREADS - 1) / COL_THREADS), ROW_GROUPS);

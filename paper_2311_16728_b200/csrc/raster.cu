@@ -57,13 +57,6 @@ __device__ __forceinline__ float fast_exp(float power) {
     return y;
 }
 
-// Largest d^T Q d at which a Gaussian can still be composited: the 3-sigma cutoff (R9) or the
-// alpha >= 1/255 skip, alpha <= sigma e^(-q/2) (R7), whichever is tighter (-1: never composited).
-__device__ __forceinline__ float q_limit(float sigma) {
-    if (sigma * 255.0f < 1.0f) return -1.0f;
-    return fminf(9.0f, 2.0f * __logf(255.0f * sigma));
-}
-
 // Conservative warp-level skip: minimum of d^T Q d over the warp's pixel block (centres
 // [x0, x0 + 7] x [y0, y0 + 3]) exceeds the Gaussian's limit.  Exact box-ellipse minimum:
 // 0 if the mean is inside, else the smallest of the four clamped edge minima.  The padding
@@ -103,11 +96,7 @@ __global__ void __launch_bounds__(256) k_gather_pairs(const uint32_t *__restrict
          pos += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t gi = vals[pos];
         const int64_t view = (int64_t)(keys[pos] >> 32) / tiles;
-        const int64_t m = view * n + gi;
-        const float4 r1 = rec1[m];
-        prec[3 * pos] = rec0[m];
-        prec[3 * pos + 1] = r1;
-        prec[3 * pos + 2] = make_float4(rec2[m].x, __uint_as_float(gi), 0.f, q_limit(r1.y));
+        write_pair_record(prec, pos, rec0, rec1, rec2, view * n + gi, gi);
     }
 }
 

@@ -127,6 +127,39 @@ class MappingEngine:
         """One pass of the Eq. 5 schedule: iterations at levels n, n-1, ..., 0."""
         return [self.iteration(l) for l in range(self.n_levels, -1, -1)]
 
+    # ------------------------------------------------------------------ CUDA graphs
+    def capture(self, gts_pinned: torch.Tensor | None = None, out_pinned: torch.Tensor | None = None):
+        """Capture one step -- A0 + the Eq. 5 pass (and, with pinned host buffers, the H2D copy of
+        the targets and the D2H copy of the losses) -- into a CUDA graph; `replay()` then runs it
+        with a single launch.  Single GPU only (the fused backward+Adam with a device-resident
+        step counter; the DP path has an NCCL collective between backward and Adam)."""
+        if self.distributed():
+            raise RuntimeError("graph capture is for the single-GPU fused path")
+        self.adam.use_device_step()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        host = gts_pinned is not None
+
+        def body():
+            if host:
+                self.step_host(gts_pinned, out_pinned)
+            else:
+                self.build_pyramids()
+                self.graph_losses = torch.stack(self.step())
+
+        with torch.cuda.stream(side):  # warm-up run on the capture stream (also a real step)
+            body()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        self.graph = g
+        return g
+
+    def replay(self):
+        self.graph.replay()
+
     def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor):
         """End-to-end public API: new keyframe targets from pinned host memory (H2D), A0,
         the Eq. 5 pass, per-level losses back to pinned host memory (D2H)."""

@@ -417,6 +417,33 @@ def test_fused_backward_adam_equals_separate(cfg, n, D):
     assert e.value.status == L.GS_ERR_STALE_STATE
 
 
+def test_graph_replay_matches_eager_steps():
+    """A captured step (device-resident Adam step counter) replayed gives the same trajectory as
+    eager steps: 1 warm-up + 2 replays == 3 eager steps (up to atomic-order rounding)."""
+    scene = make_scene("tum", n=40000)
+    cams = make_cameras("tum", 1)
+    r, params, _ = _renderer(scene, cams)
+    gt = r.forward(params, cams)[0].clone()
+    start = perturb(scene, 3)
+    a = MappingEngine(start, cams, gt, n_levels=2)
+    b = MappingEngine(start, cams, gt, n_levels=2)
+    for _ in range(3):
+        a.build_pyramids()
+        a.step()
+    b.capture()
+    b.replay()
+    b.replay()
+    torch.cuda.synchronize()
+    assert int(b.adam.t_dev.item()) == 9 and a.adam.t == 9
+    # fp32 atomics make the two runs differ in the last bits; Adam normalises the step, so a
+    # Gaussian whose gradient is ~0 can move by up to lr in either direction: allow a tiny
+    # fraction of elements to differ by at most 2 lr per step
+    diff = (b.params - a.params).abs()
+    close = diff <= 1e-5 + 1e-4 * a.params.abs()
+    assert close.float().mean().item() > 1 - 1e-5
+    assert diff.max().item() <= 2 * 5e-2 * 9
+
+
 # ------------------------------------------------------------------------------ mapping loop
 def test_mapping_engine_reduces_loss():
     """A few Eq. 5 passes on the tiny config reduce the photometric loss (SPEC.md:460 trend)."""
