@@ -61,6 +61,10 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.tile_cursor = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
     L.bin_big = take((size_t)2 * L.cap * sizeof(uint64_t));
     L.prec = take((size_t)3 * L.cap * sizeof(float4));
+    L.max_chunks = use_chunked((int64_t)V * L.tiles) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;
+    L.chunk_base = take((size_t)V * L.tiles * sizeof(uint32_t));
+    L.chunk_tile = take((size_t)std::max<int64_t>(L.max_chunks, 1) * sizeof(uint32_t));
+    L.chunk_bwd = take((size_t)L.max_chunks * CHUNK * sizeof(float4));
     L.sort_look = take((size_t)SORT_MAX_PASSES * std::max<int64_t>(L.sort_blocks, 1) * SORT_RADIX * sizeof(uint32_t));
     L.total = o;
     return L;
@@ -69,18 +73,16 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
 bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out) {
     Layout L0 = make_layout(n, V, W, H, 0);
     if (L0.total > ws_bytes) return false;
-    // bytes per SORT_TILE pairs: 2 x (8 + 4) + 16 (bucket overflow) + 48 (pair record) per pair
-    // + look-back words
-    size_t per_tile = (size_t)SORT_TILE * 88 + (size_t)SORT_MAX_PASSES * SORT_RADIX * 4;
-    int64_t tiles = (int64_t)((ws_bytes - L0.total) / per_tile) + 1;
-    for (; tiles >= 0; tiles--) {
-        Layout L = make_layout(n, V, W, H, tiles * SORT_TILE);
-        if (L.total <= ws_bytes) {
-            *out = L;
-            return true;
-        }
+    // largest capacity (in SORT_TILE units) whose layout fits: binary search; every pair costs at
+    // least 24 bytes, which bounds the search
+    int64_t lo = 0, hi = (int64_t)((ws_bytes - L0.total) / ((size_t)SORT_TILE * 24)) + 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) / 2;
+        if (make_layout(n, V, W, H, mid * SORT_TILE).total <= ws_bytes) lo = mid;
+        else hi = mid - 1;
     }
-    return false;
+    *out = make_layout(n, V, W, H, lo * SORT_TILE);
+    return true;
 }
 
 // ---- forward/backward state token (SPEC.md:355-359 StaleRenderState) ----

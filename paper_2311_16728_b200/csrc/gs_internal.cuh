@@ -44,7 +44,14 @@ struct WsHeader {
     int32_t sort_sel[SORT_MAX_PASSES + 1];  // source buffer of each pass (0 = primary)
     uint32_t sort_hist[SORT_MAX_PASSES][SORT_RADIX];
     uint32_t sort_start[SORT_MAX_PASSES][SORT_RADIX];
+    uint32_t nchunks;      // list chunks of the chunked raster path (raster.cu)
 };
+
+// Chunk-parallel raster backward for levels with few tiles: every 256-entry chunk of a tile
+// list is replayed by its own CTAs from state the forward recorded (raster.cu).
+constexpr int CHUNK = 256;
+constexpr int CHUNK_MAX_TILES = 600;  // V * tiles below this uses the chunked path
+__host__ __device__ inline bool use_chunked(int64_t view_tiles) { return view_tiles < CHUNK_MAX_TILES; }
 
 // Byte offsets of every buffer inside a render workspace (pure function of n, V, W, H, cap).
 struct Layout {
@@ -55,6 +62,8 @@ struct Layout {
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
     size_t tile_count, tile_start, tile_cursor, bin_big;  // bucket binning (bin.cu)
     size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
+    int64_t max_chunks;  // chunked raster path (0 if unused)
+    size_t chunk_base, chunk_tile, chunk_bwd;
     size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, ncomp, Tfinal, total;
 };
 

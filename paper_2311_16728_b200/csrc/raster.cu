@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                                                            int tiles, float bg0, float bg1, float bg2,
                                                            float *__restrict__ out_rgb, float *__restrict__ out_T,
                                                            float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib,
-                                                           uint32_t *__restrict__ ncomp) {
+                                                           uint32_t *__restrict__ ncomp,
+                                                           const uint32_t *__restrict__ chunk_base,
+                                                           float4 *__restrict__ chunk_bwd) {
     constexpr int NT = WARPS * 32;
     __shared__ __align__(128) RasterSmem S;
     __shared__ uint8_t wl[WARPS][BATCH];
@@ -198,6 +200,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         phases ^= 1u << buf;
         inflight = b0 + BATCH < todo_all ? (buf ^ 1) : -1;
         const float4 *r = S.rec[buf];
+        const bool active_in_batch = !done;  // this batch is a chunk the pixel reaches
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f;  // colour composited in this batch
         // phase 1 (parallel over the batch): ordered list of the Gaussians that can reach this
         // warp's 8x4 block
         int nsel = 0;
@@ -232,9 +236,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                     done = true;
                 } else {
                     const float w = alpha_a * T;
-                    c0 += a1.z * w;
-                    c1 += a1.w * w;
-                    c2 += r[3 * ja + 2].x * w;
+                    d0 += a1.z * w;
+                    d1 += a1.w * w;
+                    d2 += r[3 * ja + 2].x * w;
                     T = test_T;
                     composited++;
                     last = (uint32_t)(b0 + ja + 1);  // 1-based list position of the last composited
@@ -246,15 +250,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                     done = true;
                 } else {
                     const float w = alpha_b * T;
-                    c0 += b1.z * w;
-                    c1 += b1.w * w;
-                    c2 += r[3 * jb + 2].x * w;
+                    d0 += b1.z * w;
+                    d1 += b1.w * w;
+                    d2 += r[3 * jb + 2].x * w;
                     T = test_T;
                     composited++;
                     last = (uint32_t)(b0 + jb + 1);
                 }
             }
         }
+        c0 += d0;
+        c1 += d1;
+        c2 += d2;
+        // chunked backward (few tiles): record (T after this chunk, colour it composited)
+        if (chunk_bwd && inside && active_in_batch)
+            chunk_bwd[((size_t)chunk_base[view * tiles + tile] + it) * CHUNK + ly * TILE + lx] =
+                make_float4(T, d0, d1, d2);
     }
     // never leave with a bulk copy still writing into this CTA's shared memory
     if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], (phases >> inflight) & 1u);
@@ -269,6 +280,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         T_keep[(int64_t)view * HW + pix] = T;
         ncontrib[(int64_t)view * HW + pix] = last;
         ncomp[(int64_t)view * HW + pix] = composited;
+        if (chunk_bwd && last > 0) {
+            // reverse pass over the chunks up to the last composited one: normalised colour
+            // behind each chunk, acc_end(k) = behind(k) / T_after(k), behind(k) = sum of the later
+            // chunks' colour + T_final bg (positive terms only -- no cancellation)
+            const size_t cb = chunk_base[view * tiles + tile];
+            float e0 = T * bg0, e1 = T * bg1, e2 = T * bg2;
+            for (int k = (int)((last - 1) / CHUNK); k >= 0; k--) {
+                const size_t slot = (cb + k) * CHUNK + ly * TILE + lx;
+                const float4 e = chunk_bwd[slot];
+                const float inv = 1.0f / e.x;
+                chunk_bwd[slot] = make_float4(e.x, e0 * inv, e1 * inv, e2 * inv);
+                e0 += e.y;
+                e1 += e.z;
+                e2 += e.w;
+            }
+        }
     }
 }
 
@@ -450,6 +477,204 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restri
     // every issued copy was waited for inside the loop (the last batch issues none)
 }
 
+// ================================================================ chunked backward (few tiles)
+// At pyramid levels with few tiles (V * tiles < CHUNK_MAX_TILES) each warp of the tile-serial
+// backward would walk a long list alone.  The forward (same kernel as always) records, for every
+// 256-entry batch = chunk of a tile list that a pixel reaches, the transmittance after the chunk
+// and the colour composited in it; its epilogue turns these into the normalised colour behind
+// each chunk (suffix sums of positive terms + T_final bg, no cancellation).  The backward then
+// gives every (chunk, 8x4 pixel block) its own one-warp CTA, which replays that chunk back to
+// front from (T after the chunk, colour behind it) -- the chunks run in parallel instead of one
+// after the other.
+
+__global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ ranges, int VT,
+                                                      uint32_t *__restrict__ chunk_base,
+                                                      uint32_t *__restrict__ chunk_tile, WsHeader *hdr,
+                                                      int64_t max_chunks) {
+    __shared__ uint32_t s[1024];
+    const int t = threadIdx.x;
+    uint32_t nch = 0;
+    if (t < VT) {
+        const uint2 r = ranges[t];
+        nch = (r.y - r.x + CHUNK - 1) / CHUNK;
+    }
+    s[t] = nch;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan
+        uint32_t v = t >= o ? s[t - o] : 0u;
+        __syncthreads();
+        s[t] += v;
+        __syncthreads();
+    }
+    const uint32_t base = s[t] - nch;
+    if (t < VT) chunk_base[t] = base;
+    if (t == 1023) hdr->nchunks = (uint32_t)min((int64_t)s[1023], max_chunks);
+    for (uint32_t k = 0; k < nch; k++)
+        if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
+}
+
+struct ChunkPix {
+    int view, tx, ty, lx, ly, px, py;
+    float wx0, wy0;
+    uint2 range;
+    int b0, cnt;  // chunk offset in the tile list, entries in the chunk
+};
+
+// chunk c, warp block wb (0..7) of its tile
+__device__ __forceinline__ ChunkPix chunk_pixel(int c, int wb, const uint2 *ranges, const uint32_t *chunk_base,
+                                                const uint32_t *chunk_tile, int TX, int tiles) {
+    ChunkPix q;
+    const uint32_t gt = chunk_tile[c];
+    q.view = gt / tiles;
+    const int tl = gt % tiles;
+    q.tx = tl % TX;
+    q.ty = tl / TX;
+    const int lane = threadIdx.x & 31;
+    const int bx = (wb & 1) * 8, by = (wb >> 1) * 4;
+    q.lx = bx + (lane & 7);
+    q.ly = by + (lane >> 3);
+    q.px = q.tx * TILE + q.lx;
+    q.py = q.ty * TILE + q.ly;
+    q.wx0 = (float)(q.tx * TILE + bx);
+    q.wy0 = (float)(q.ty * TILE + by);
+    q.range = ranges[gt];
+    q.b0 = (int)(c - chunk_base[gt]) * CHUNK;
+    q.cnt = min(CHUNK, (int)(q.range.y - q.range.x) - q.b0);
+    return q;
+}
+
+// ordered per-warp list of the batch slots that can reach the warp's block; REVERSE walks the
+// batch back to front and keeps only 1-based list positions b0 + slot + 1 <= lim
+template <bool REVERSE>
+__device__ __forceinline__ int compact_block(const float4 *r, int cnt, float x0, float y0, int b0, uint32_t lim,
+                                             uint8_t *wl) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    int nsel = 0;
+    for (int k = 0; k < cnt; k += 32) {
+        const int jj = k + lane;
+        const int idx = REVERSE ? cnt - 1 - jj : jj;
+        bool hit = jj < cnt && (uint32_t)(b0 + idx + 1) <= lim &&
+                   !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, x0, y0);
+        unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) wl[nsel + __popc(b & lt)] = (uint8_t)idx;
+        nsel += __popc(b);
+    }
+    __syncwarp();
+    return nsel;
+}
+
+__device__ __forceinline__ void chunk_load(float4 *dst, const float4 *prec, const ChunkPix &q, uint64_t *bar,
+                                           uint32_t parity) {
+    if ((threadIdx.x & 31) == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_load(dst, prec + 3 * ((size_t)q.range.x + q.b0), (uint32_t)q.cnt * 48u, bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, parity);
+}
+
+__global__ void __launch_bounds__(32) k_raster_bwd_chunk(const uint2 *__restrict__ ranges,
+                                                         const float4 *__restrict__ prec,
+                                                         const uint32_t *__restrict__ chunk_base,
+                                                         const uint32_t *__restrict__ chunk_tile,
+                                                         const WsHeader *__restrict__ hdr, int64_t n, int W, int H,
+                                                         int TX, int tiles, const float *__restrict__ dL_drgb,
+                                                         const uint32_t *__restrict__ ncontrib,
+                                                         const float4 *__restrict__ chunk_bwd,
+                                                         float4 *__restrict__ g2d) {
+    __shared__ __align__(128) float4 rec[CHUNK * 3];
+    __shared__ uint64_t bar;
+    __shared__ uint8_t wl[CHUNK];
+    const int c = blockIdx.x >> 3;
+    if (c >= (int)hdr->nchunks) return;
+    const ChunkPix q = chunk_pixel(c, blockIdx.x & 7, ranges, chunk_base, chunk_tile, TX, tiles);
+    const int lane = threadIdx.x & 31;
+    const bool inside = q.px < W && q.py < H;
+    const int64_t HW = (int64_t)H * W;
+    const int64_t pix = (int64_t)q.py * W + q.px;
+    uint32_t last = 0;
+    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, g_0 = 0.f, g_1 = 0.f, g_2 = 0.f;
+    if (inside) {
+        last = ncontrib[(int64_t)q.view * HW + pix];
+        if ((uint32_t)q.b0 < last) {  // this chunk holds composited entries of the pixel
+            const float4 e = chunk_bwd[(size_t)c * CHUNK + q.ly * TILE + q.lx];
+            T = e.x;
+            acc0 = e.y;
+            acc1 = e.z;
+            acc2 = e.w;
+            const float *g = dL_drgb + (int64_t)q.view * 3 * HW + pix;
+            g_0 = g[0];
+            g_1 = g[HW];
+            g_2 = g[2 * HW];
+        } else {
+            last = 0;
+        }
+    }
+    uint32_t wlast = last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (wlast == 0) return;  // warp-uniform
+    if (threadIdx.x == 0) {
+        mbar_init(&bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    chunk_load(rec, prec, q, &bar, 0u);
+    const int nsel = compact_block<true>(rec, q.cnt, q.wx0, q.wy0, q.b0, wlast, wl);
+    const float fx = (float)q.px, fy = (float)q.py;
+    const int64_t vbase = (int64_t)q.view * n;
+    for (int t = 0; t < nsel; t++) {
+        const int j = wl[t];
+        const uint32_t position = (uint32_t)(q.b0 + j + 1);
+        const float4 g0 = rec[3 * j], g1 = rec[3 * j + 1];
+        float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
+        float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
+        bool contrib = false;
+        if (position <= last) {
+            float dx, dy;
+            const float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
+            if (!(power > 0.0f || power < POWER_CUT)) {
+                const float e = fast_exp(power);
+                const float a_raw = g1.y * e;
+                const float alpha = fminf(ALPHA_MAX, a_raw);
+                if (alpha >= ALPHA_MIN) {
+                    contrib = true;
+                    T = __fdividef(T, 1.0f - alpha);
+                    const float w = alpha * T;
+                    dLdr = g_0 * w;
+                    dLdg = g_1 * w;
+                    dLdb = g_2 * w;
+                    const float d0 = g1.z - acc0, d1 = g1.w - acc1, d2 = rec[3 * j + 2].x - acc2;
+                    const float dLda = T * (g_0 * d0 + g_1 * d1 + g_2 * d2);
+                    acc0 += alpha * d0;
+                    acc1 += alpha * d1;
+                    acc2 += alpha * d2;
+                    if (!(a_raw > ALPHA_MAX)) {
+                        dLdsig = e * dLda;
+                        const float dLdp = alpha * dLda;
+                        dLdu = dLdp * dx;
+                        dLdv = dLdp * dy;
+                        dLdA = dLdu * dx;
+                        dLdB = dLdu * dy;
+                        dLdC = dLdv * dy;
+                    }
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, contrib)) {
+            float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
+            const float mine = warp_sum8_transposed(vals8, lane);
+            const float bsum = warp_sum(dLdb);
+            const uint32_t gi = __float_as_uint(rec[3 * j + 2].y);
+            float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
+            if ((lane & 3) == 0)
+                atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
+            if (lane == 1) atomicAdd(dst + 8, bsum);
+        }
+    }
+}
+
 // Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
 // tile) at pyramid levels with few tiles so that every SM gets work.
 static int raster_warps(const Layout &L) {
@@ -476,12 +701,13 @@ cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s) {
 }
 
 template <int WARPS>
-static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T, cudaStream_t s) {
+static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
+                       const uint32_t *cbase, float4 *cbwd, cudaStream_t s) {
     dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
     k_raster_fwd<WARPS><<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX,
                                                     L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T,
                                                     at<float>(ws, L.Tfinal), at<uint32_t>(ws, L.ncontrib),
-                                                    at<uint32_t>(ws, L.ncomp));
+                                                    at<uint32_t>(ws, L.ncomp), cbase, cbwd);
 }
 
 template <int WARPS>
@@ -496,16 +722,31 @@ static void bwd_launch(const Layout &L, void *ws, const float bg[3], const float
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s) {
     ProfScope prof("k_raster_fwd", s);
+    uint32_t *cbase = nullptr;
+    float4 *cbwd = nullptr;
+    if (L.max_chunks > 0) {  // few tiles: record per-chunk state for the chunk-parallel backward
+        k_chunk_index<<<1, 1024, 0, s>>>(at<uint2>(ws, L.ranges), L.V * L.tiles, at<uint32_t>(ws, L.chunk_base),
+                                         at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.max_chunks);
+        cbase = at<uint32_t>(ws, L.chunk_base);
+        cbwd = at<float4>(ws, L.chunk_bwd);
+    }
     switch (raster_warps(L)) {
-        case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, s); break;
-        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, s); break;
-        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, s); break;
+        case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
+        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
+        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     ProfScope prof("k_raster_bwd", s);
+    if (L.max_chunks > 0) {  // chunked path (few tiles): every chunk replayed independently
+        k_raster_bwd_chunk<<<(unsigned)(L.max_chunks * 8), 32, 0, s>>>(
+            at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
+            at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
+            at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
+        return cudaGetLastError();
+    }
     switch (raster_warps(L)) {
         case 8: bwd_launch<8>(L, ws, bg, dL_drgb, s); break;
         case 2: bwd_launch<2>(L, ws, bg, dL_drgb, s); break;
