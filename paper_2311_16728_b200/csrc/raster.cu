@@ -62,10 +62,11 @@ __device__ __forceinline__ float fast_exp(float power) {
 // 0 if the mean is inside, else the smallest of the four clamped edge minima.  The padding
 // (1e-3 relative + 1e-3 absolute) absorbs the rounding of the per-pixel fp32 power, so a
 // culled Gaussian can never pass the per-pixel tests.
-__device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, float qlim, float x0, float y0) {
+__device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, float qlim, float x0, float y0,
+                                             float h = 3.f) {
     if (qlim < 0.f) return true;
     const float A = g0.z, B = g0.w, C = g1.x;
-    const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + 3.f - g0.y;
+    const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + h - g0.y;
     if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return false;
     float best = 3.4e38f;
     // edges x = X: f = A X^2 + 2 B X y + C y^2, y* = -B X / C clamped to [ay, by]
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                                                            float4 *__restrict__ chunk_bwd) {
     constexpr int NT = WARPS * 32;
     __shared__ __align__(128) RasterSmem S;
-    __shared__ uint8_t wl[WARPS][BATCH];
+    __shared__ __align__(16) uint8_t wl[WARPS][BATCH];
     const int view = blockIdx.z;
     int tile_x, bx0, by0, lx, ly;
     warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
@@ -213,50 +214,43 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
             nsel += __popc(b);
         }
         __syncwarp();
-        // phase 2 (sequential per pixel): composite the warp's list front to back
-        // two list entries per step: their alphas are independent, only the compositing
-        // recurrence (T, C) is sequential, so the SFU/FMA latency of the second overlaps the first
-        for (int t = 0; t < nsel; t += 2) {
+        // phase 2 (sequential per pixel): composite the warp's list front to back, FG entries at
+        // a time: their alphas (record loads, power, SFU exp) are independent and computed first,
+        // then the compositing recurrence (T, C) runs over them branch-free -- the latency of the
+        // independent part overlaps across the group instead of stalling every entry
+        constexpr int FG = 8;
+        for (int t = 0; t < nsel; t += FG) {
             if (__all_sync(0xffffffffu, done)) break;
-            const int ja = wl[warp][t];
-            const bool has_b = t + 1 < nsel;
-            const int jb = has_b ? wl[warp][t + 1] : ja;
-            const float4 a0 = r[3 * ja], a1 = r[3 * ja + 1];
-            const float4 b0v = r[3 * jb], b1 = r[3 * jb + 1];
-            float dxa, dya, dxb, dyb;
-            const float pa = pixel_power(fx, fy, a0, a1.x, dxa, dya);
-            const float pb = pixel_power(fx, fy, b0v, b1.x, dxb, dyb);
-            const float alpha_a = fminf(ALPHA_MAX, a1.y * fast_exp(pa));
-            const float alpha_b = fminf(ALPHA_MAX, b1.y * fast_exp(pb));
-            const bool va = !(pa > 0.0f || pa < POWER_CUT) && alpha_a >= ALPHA_MIN;
-            const bool vb = has_b && !(pb > 0.0f || pb < POWER_CUT) && alpha_b >= ALPHA_MIN;
-            if (!done && va) {
-                const float test_T = T * (1.0f - alpha_a);
-                if (test_T < T_STOP) {
-                    done = true;
-                } else {
-                    const float w = alpha_a * T;
-                    d0 += a1.z * w;
-                    d1 += a1.w * w;
-                    d2 += r[3 * ja + 2].x * w;
-                    T = test_T;
-                    composited++;
-                    last = (uint32_t)(b0 + ja + 1);  // 1-based list position of the last composited
-                }
+            const uint2 jw = *reinterpret_cast<const uint2 *>(&wl[warp][t]);
+            float al[FG], cr[FG], cg[FG], cb[FG];
+            bool ok[FG];
+#pragma unroll
+            for (int k = 0; k < FG; k++) {
+                // slots past the list end hold stale indices: point them at entry t (finite data)
+                const int j = t + k < nsel ? ((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff : (jw.x & 0xff);
+                const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
+                float dx, dy;
+                const float p = pixel_power(fx, fy, g0, g1.x, dx, dy);
+                al[k] = fminf(ALPHA_MAX, g1.y * fast_exp(p));
+                ok[k] = t + k < nsel && !(p > 0.0f || p < POWER_CUT) && al[k] >= ALPHA_MIN;
+                cr[k] = g1.z;
+                cg[k] = g1.w;
+                cb[k] = r[3 * j + 2].x;
             }
-            if (!done && vb) {
-                const float test_T = T * (1.0f - alpha_b);
-                if (test_T < T_STOP) {
-                    done = true;
-                } else {
-                    const float w = alpha_b * T;
-                    d0 += b1.z * w;
-                    d1 += b1.w * w;
-                    d2 += r[3 * jb + 2].x * w;
-                    T = test_T;
-                    composited++;
-                    last = (uint32_t)(b0 + jb + 1);
-                }
+#pragma unroll
+            for (int k = 0; k < FG; k++) {
+                const float test_T = T * (1.0f - al[k]);
+                const bool live = ok[k] && !done;
+                const bool stop = live && test_T < T_STOP;
+                const bool take = live && !(test_T < T_STOP);
+                done = done || stop;
+                const float w = take ? al[k] * T : 0.f;
+                d0 += cr[k] * w;
+                d1 += cg[k] * w;
+                d2 += cb[k] * w;
+                T = take ? test_T : T;
+                composited += take ? 1u : 0u;
+                if (take) last = (uint32_t)(b0 + (((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff) + 1);
             }
         }
         c0 += d0;
@@ -675,6 +669,157 @@ __global__ void __launch_bounds__(32) k_raster_bwd_chunk(const uint2 *__restrict
     }
 }
 
+// ================================================================ two-pixel packed backward
+// Backward for levels with many tiles: a warp owns an 8x8 block and every lane two pixels
+// (x, y) and (x, y + 4), evaluated with Blackwell's packed fp32x2 instructions (FFMA2 / FMUL2 /
+// FADD2, IEEE round-to-nearest per element, so the power and alpha of each pixel are the same
+// bits as the scalar forward).  Per-pixel validity is folded into masked alphas instead of
+// branches; the list walk, record loads, the warp reduction and the atomics are shared by 64
+// pixels instead of 32.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ ranges,
+                                                     const float4 *__restrict__ prec, int64_t n, int W, int H,
+                                                     int TX, int tiles, float bg0, float bg1, float bg2,
+                                                     const float *__restrict__ dL_drgb,
+                                                     const float *__restrict__ T_keep,
+                                                     const uint32_t *__restrict__ ncontrib,
+                                                     float4 *__restrict__ g2d) {
+    __shared__ __align__(128) RasterSmem S;
+    __shared__ uint8_t wl[4][BATCH];
+    __shared__ uint32_t s_maxlast;
+    const int view = blockIdx.z;
+    const int tile = blockIdx.y * TX + blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
+    const int px = blockIdx.x * TILE + bx + (lane & 7);
+    const int pyA = blockIdx.y * TILE + by + (lane >> 3), pyB = pyA + 4;
+    const float wx0 = (float)(blockIdx.x * TILE + bx), wy0 = (float)(blockIdx.y * TILE + by);
+    const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
+    const uint2 range = ranges[(int64_t)view * tiles + tile];
+    const float fx = (float)px;
+    const float2 fy2 = make_float2((float)pyA, (float)pyB);
+    const int64_t vbase = (int64_t)view * n;
+    const int64_t HW = (int64_t)H * W;
+    const int64_t pixA = (int64_t)pyA * W + px, pixB = (int64_t)pyB * W + px;
+    float2 T2 = f2(1.f), g0v = f2(0.f), g1v = f2(0.f), g2v = f2(0.f);
+    uint32_t lastA = 0, lastB = 0;
+    const float *gbase = dL_drgb + (int64_t)view * 3 * HW;
+    if (inA) {
+        T2.x = T_keep[(int64_t)view * HW + pixA];
+        lastA = ncontrib[(int64_t)view * HW + pixA];
+        g0v.x = gbase[pixA];
+        g1v.x = gbase[HW + pixA];
+        g2v.x = gbase[2 * HW + pixA];
+    }
+    if (inB) {
+        T2.y = T_keep[(int64_t)view * HW + pixB];
+        lastB = ncontrib[(int64_t)view * HW + pixB];
+        g0v.y = gbase[pixB];
+        g1v.y = gbase[HW + pixB];
+        g2v.y = gbase[2 * HW + pixB];
+    }
+    if (tid == 0) {
+        s_maxlast = 0;
+        mbar_init(&S.bar[0]);
+        mbar_init(&S.bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t wlast = max(lastA, lastB);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (lane == 0) atomicMax(&s_maxlast, wlast);
+    __syncthreads();
+    const int todo_all = (int)s_maxlast;
+    const float4 *src = prec + 3 * (size_t)range.x;
+    if (tid == 0 && todo_all > 0) {
+        int cnt0 = min(BATCH, todo_all);
+        bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
+    }
+    uint32_t phases = 0u;
+    float2 acc0 = f2(bg0), acc1 = f2(bg1), acc2 = f2(bg2);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
+        const int buf = it & 1;
+        const int cnt = min(BATCH, b_end);
+        const int b_start = b_end - cnt;
+        __syncthreads();
+        if (tid == 0 && b_start > 0) {
+            int cn = min(BATCH, b_start);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
+        }
+        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const float4 *r = S.rec[buf];
+        int nsel = 0;
+        for (int k = 0; k < cnt; k += 32) {
+            const int jj = k + lane;
+            const int idx = cnt - 1 - jj;
+            bool hit = jj < cnt && (uint32_t)(b_start + idx + 1) <= wlast &&
+                       !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, wx0, wy0, 7.f);
+            unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
+            nsel += __popc(b);
+        }
+        __syncwarp();
+        for (int t = 0; t < nsel; t++) {
+            const int j = wl[warp][t];
+            const uint32_t position = (uint32_t)(b_start + j + 1);
+            const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
+            // power per pixel in the recipe's op order (bit-identical to pixel_power)
+            const float dx = SUB(fx, g0.x);
+            const float2 dy2 = __fadd2_rn(fy2, f2(-g0.y));
+            const float Adxdx = MUL(MUL(g0.z, dx), dx);
+            const float2 qf2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(Adxdx));
+            const float2 p2 = __ffma2_rn(f2(-MUL(g0.w, dx)), dy2, __fmul2_rn(f2(-0.5f), qf2));
+            const float2 e2 = make_float2(fast_exp(p2.x), fast_exp(p2.y));
+            const float2 araw = __fmul2_rn(f2(g1.y), e2);
+            const float aA = fminf(ALPHA_MAX, araw.x), aB = fminf(ALPHA_MAX, araw.y);
+            const bool vA = position <= lastA && !(p2.x > 0.0f || p2.x < POWER_CUT) && aA >= ALPHA_MIN;
+            const bool vB = position <= lastB && !(p2.y > 0.0f || p2.y < POWER_CUT) && aB >= ALPHA_MIN;
+            if (!__any_sync(0xffffffffu, vA || vB)) continue;
+            const float2 al = make_float2(vA ? aA : 0.f, vB ? aB : 0.f);            // masked alpha
+            const float2 ua = make_float2(vA && !(araw.x > ALPHA_MAX) ? aA : 0.f,  // unclamped part
+                                          vB && !(araw.y > ALPHA_MAX) ? aB : 0.f);
+            const float2 ue = make_float2(ua.x != 0.f ? e2.x : 0.f, ua.y != 0.f ? e2.y : 0.f);
+            T2 = __fmul2_rn(T2, make_float2(rcp_approx(1.0f - al.x), rcp_approx(1.0f - al.y)));
+            const float2 w2 = __fmul2_rn(al, T2);
+            const float2 d0 = __fadd2_rn(f2(g1.z), make_float2(-acc0.x, -acc0.y));
+            const float2 d1 = __fadd2_rn(f2(g1.w), make_float2(-acc1.x, -acc1.y));
+            const float cb = r[3 * j + 2].x;
+            const float2 d2 = __fadd2_rn(f2(cb), make_float2(-acc2.x, -acc2.y));
+            const float2 dLda = __fmul2_rn(T2, __ffma2_rn(g2v, d2, __ffma2_rn(g1v, d1, __fmul2_rn(g0v, d0))));
+            acc0 = __ffma2_rn(al, d0, acc0);
+            acc1 = __ffma2_rn(al, d1, acc1);
+            acc2 = __ffma2_rn(al, d2, acc2);
+            const float2 dr = __fmul2_rn(g0v, w2), dg = __fmul2_rn(g1v, w2), db = __fmul2_rn(g2v, w2);
+            const float2 dsig = __fmul2_rn(ue, dLda);
+            const float2 dp = __fmul2_rn(ua, dLda);
+            const float2 a2 = __fmul2_rn(dp, f2(dx));
+            const float2 b2 = __fmul2_rn(dp, dy2);
+            const float2 qa = __fmul2_rn(a2, f2(dx));
+            const float2 qb = __fmul2_rn(a2, dy2);
+            const float2 qc = __fmul2_rn(b2, dy2);
+            float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
+                              qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
+            const float mine = warp_sum8_transposed(vals8, lane);
+            const float bsum = warp_sum(db.x + db.y);
+            const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
+            float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
+            if ((lane & 3) == 0)
+                atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
+            if (lane == 1) atomicAdd(dst + 8, bsum);
+        }
+    }
+}
+
 // Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
 // tile) at pyramid levels with few tiles so that every SM gets work.
 static int raster_warps(const Layout &L) {
@@ -745,6 +890,13 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
             at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
             at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
+        return cudaGetLastError();
+    }
+    if (raster_warps(L) == 8) {  // many tiles: two pixels per lane, packed fp32x2
+        dim3 grid(L.TX, L.TY, L.V);
+        k_raster_bwd2<<<grid, 128, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
+                                           L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
+                                           at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
         return cudaGetLastError();
     }
     switch (raster_warps(L)) {
