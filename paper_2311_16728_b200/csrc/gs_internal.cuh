@@ -49,7 +49,8 @@ struct WsHeader {
 
 // Chunk-parallel raster backward for levels with few tiles: every 256-entry chunk of a tile
 // list is replayed by its own CTAs from state the forward recorded (raster.cu).
-constexpr int CHUNK = 256;
+constexpr int CHUNK = 64;              // list entries per chunk of the chunked raster path
+constexpr int TILE_PIX = 256;          // pixels per 16x16 tile (per-chunk record stride)
 constexpr int CHUNK_MAX_TILES = 600;  // V * tiles below this uses the chunked path
 __host__ __device__ inline bool use_chunked(int64_t view_tiles) { return view_tiles < CHUNK_MAX_TILES; }
 

@@ -148,7 +148,7 @@ __device__ __forceinline__ void warp_block(int &tile_x, int &wx0, int &wy0, int 
     ly = wy0 + (lane >> 3);
 }
 
-template <int WARPS>
+template <int WARPS, bool CHUNKED>
 __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restrict__ ranges,
                                                            const float4 *__restrict__ prec, int W, int H, int TX,
                                                            int tiles, float bg0, float bg1, float bg2,
@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                                                            float4 *__restrict__ chunk_bwd) {
     constexpr int NT = WARPS * 32;
     __shared__ __align__(128) RasterSmem S;
-    __shared__ __align__(16) uint8_t wl[WARPS][BATCH];
+    constexpr int SEG = CHUNKED ? CHUNK : BATCH;  // list segment = unit of chunk recording
+    constexpr int NSEG = BATCH / SEG;
+    __shared__ __align__(16) uint8_t wl[WARPS][BATCH];  // segment s's selection at [s * SEG, ...)
+    __shared__ int segn[WARPS][NSEG];
     const int view = blockIdx.z;
     int tile_x, bx0, by0, lx, ly;
     warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
@@ -201,65 +204,74 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         phases ^= 1u << buf;
         inflight = b0 + BATCH < todo_all ? (buf ^ 1) : -1;
         const float4 *r = S.rec[buf];
-        const bool active_in_batch = !done;  // this batch is a chunk the pixel reaches
-        float d0 = 0.f, d1 = 0.f, d2 = 0.f;  // colour composited in this batch
-        // phase 1 (parallel over the batch): ordered list of the Gaussians that can reach this
-        // warp's 8x4 block
+        // phase 1 (parallel over the batch): per SEG-entry segment, the ordered list of the
+        // Gaussians that can reach this warp's 8x4 block
         int nsel = 0;
         for (int k = 0; k < cnt; k += 32) {
+            const int seg = k / SEG;
+            if (k % SEG == 0) nsel = 0;
             int j = k + lane;
             bool hit = j < cnt && !block_misses(r[3 * j], r[3 * j + 1], r[3 * j + 2].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)j;
+            if (hit) wl[warp][seg * SEG + nsel + __popc(b & lt)] = (uint8_t)j;
             nsel += __popc(b);
+            if (lane == 0) segn[warp][seg] = nsel;
         }
         __syncwarp();
-        // phase 2 (sequential per pixel): composite the warp's list front to back, FG entries at
-        // a time: their alphas (record loads, power, SFU exp) are independent and computed first,
-        // then the compositing recurrence (T, C) runs over them branch-free -- the latency of the
-        // independent part overlaps across the group instead of stalling every entry
-        constexpr int FG = 8;
-        for (int t = 0; t < nsel; t += FG) {
+        const int nseg = (cnt + SEG - 1) / SEG;
+        for (int sg = 0; sg < nseg; sg++) {
+            const bool active_in_seg = !done;    // this segment is a chunk the pixel reaches
             if (__all_sync(0xffffffffu, done)) break;
-            const uint2 jw = *reinterpret_cast<const uint2 *>(&wl[warp][t]);
-            float al[FG], cr[FG], cg[FG], cb[FG];
-            bool ok[FG];
+            float d0 = 0.f, d1 = 0.f, d2 = 0.f;  // colour composited in this segment
+            const int ns = segn[warp][sg];
+            const uint8_t *wls = &wl[warp][sg * SEG];
+            // phase 2 (sequential per pixel): composite the warp's list front to back, FG entries
+            // at a time: their alphas (record loads, power, SFU exp) are independent and computed
+            // first, then the compositing recurrence (T, C) runs over them branch-free -- the
+            // latency of the independent part overlaps across the group
+            constexpr int FG = 8;
+            for (int t = 0; t < ns; t += FG) {
+                if (__all_sync(0xffffffffu, done)) break;
+                const uint2 jw = *reinterpret_cast<const uint2 *>(&wls[t]);
+                float al[FG], cr[FG], cg[FG], cb[FG];
+                bool ok[FG];
 #pragma unroll
-            for (int k = 0; k < FG; k++) {
-                // slots past the list end hold stale indices: point them at entry t (finite data)
-                const int j = t + k < nsel ? ((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff : (jw.x & 0xff);
-                const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
-                float dx, dy;
-                const float p = pixel_power(fx, fy, g0, g1.x, dx, dy);
-                al[k] = fminf(ALPHA_MAX, g1.y * fast_exp(p));
-                ok[k] = t + k < nsel && !(p > 0.0f || p < POWER_CUT) && al[k] >= ALPHA_MIN;
-                cr[k] = g1.z;
-                cg[k] = g1.w;
-                cb[k] = r[3 * j + 2].x;
-            }
+                for (int k = 0; k < FG; k++) {
+                    // slots past the list end hold stale indices: use entry t's (finite data)
+                    const int j = t + k < ns ? ((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff : (jw.x & 0xff);
+                    const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
+                    float dx, dy;
+                    const float p = pixel_power(fx, fy, g0, g1.x, dx, dy);
+                    al[k] = fminf(ALPHA_MAX, g1.y * fast_exp(p));
+                    ok[k] = t + k < ns && !(p > 0.0f || p < POWER_CUT) && al[k] >= ALPHA_MIN;
+                    cr[k] = g1.z;
+                    cg[k] = g1.w;
+                    cb[k] = r[3 * j + 2].x;
+                }
 #pragma unroll
-            for (int k = 0; k < FG; k++) {
-                const float test_T = T * (1.0f - al[k]);
-                const bool live = ok[k] && !done;
-                const bool stop = live && test_T < T_STOP;
-                const bool take = live && !(test_T < T_STOP);
-                done = done || stop;
-                const float w = take ? al[k] * T : 0.f;
-                d0 += cr[k] * w;
-                d1 += cg[k] * w;
-                d2 += cb[k] * w;
-                T = take ? test_T : T;
-                composited += take ? 1u : 0u;
-                if (take) last = (uint32_t)(b0 + (((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff) + 1);
+                for (int k = 0; k < FG; k++) {
+                    const float test_T = T * (1.0f - al[k]);
+                    const bool live = ok[k] && !done;
+                    const bool stop = live && test_T < T_STOP;
+                    const bool take = live && !(test_T < T_STOP);
+                    done = done || stop;
+                    const float w = take ? al[k] * T : 0.f;
+                    d0 += cr[k] * w;
+                    d1 += cg[k] * w;
+                    d2 += cb[k] * w;
+                    T = take ? test_T : T;
+                    composited += take ? 1u : 0u;
+                    if (take) last = (uint32_t)(b0 + (((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff) + 1);
+                }
             }
+            c0 += d0;
+            c1 += d1;
+            c2 += d2;
+            // chunked backward (few tiles): record (T after this chunk, colour it composited)
+            if (CHUNKED && inside && active_in_seg)
+                chunk_bwd[((size_t)chunk_base[view * tiles + tile] + it * NSEG + sg) * TILE_PIX + ly * TILE + lx] =
+                    make_float4(T, d0, d1, d2);
         }
-        c0 += d0;
-        c1 += d1;
-        c2 += d2;
-        // chunked backward (few tiles): record (T after this chunk, colour it composited)
-        if (chunk_bwd && inside && active_in_batch)
-            chunk_bwd[((size_t)chunk_base[view * tiles + tile] + it) * CHUNK + ly * TILE + lx] =
-                make_float4(T, d0, d1, d2);
     }
     // never leave with a bulk copy still writing into this CTA's shared memory
     if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], (phases >> inflight) & 1u);
@@ -274,20 +286,28 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
         T_keep[(int64_t)view * HW + pix] = T;
         ncontrib[(int64_t)view * HW + pix] = last;
         ncomp[(int64_t)view * HW + pix] = composited;
-        if (chunk_bwd && last > 0) {
+        if (CHUNKED && last > 0) {
             // reverse pass over the chunks up to the last composited one: normalised colour
             // behind each chunk, acc_end(k) = behind(k) / T_after(k), behind(k) = sum of the later
             // chunks' colour + T_final bg (positive terms only -- no cancellation)
             const size_t cb = chunk_base[view * tiles + tile];
             float e0 = T * bg0, e1 = T * bg1, e2 = T * bg2;
-            for (int k = (int)((last - 1) / CHUNK); k >= 0; k--) {
-                const size_t slot = (cb + k) * CHUNK + ly * TILE + lx;
-                const float4 e = chunk_bwd[slot];
-                const float inv = 1.0f / e.x;
-                chunk_bwd[slot] = make_float4(e.x, e0 * inv, e1 * inv, e2 * inv);
-                e0 += e.y;
-                e1 += e.z;
-                e2 += e.w;
+            // eight chunks per round: their loads are issued together, before any store
+            float4 *col = chunk_bwd + cb * TILE_PIX + ly * TILE + lx;
+            for (int k = (int)((last - 1) / CHUNK); k >= 0; k -= 8) {
+                float4 e[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (k - u >= 0) e[u] = col[(size_t)(k - u) * TILE_PIX];
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (k - u >= 0) {
+                        const float inv = 1.0f / e[u].x;
+                        col[(size_t)(k - u) * TILE_PIX] = make_float4(e[u].x, e0 * inv, e1 * inv, e2 * inv);
+                        e0 += e[u].y;
+                        e1 += e[u].z;
+                        e2 += e[u].w;
+                    }
             }
         }
     }
@@ -473,13 +493,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restri
 
 // ================================================================ chunked backward (few tiles)
 // At pyramid levels with few tiles (V * tiles < CHUNK_MAX_TILES) each warp of the tile-serial
-// backward would walk a long list alone.  The forward (same kernel as always) records, for every
-// 256-entry batch = chunk of a tile list that a pixel reaches, the transmittance after the chunk
-// and the colour composited in it; its epilogue turns these into the normalised colour behind
-// each chunk (suffix sums of positive terms + T_final bg, no cancellation).  The backward then
-// gives every (chunk, 8x4 pixel block) its own one-warp CTA, which replays that chunk back to
-// front from (T after the chunk, colour behind it) -- the chunks run in parallel instead of one
-// after the other.
+// backward would walk a long list alone.  The forward (same kernel, CHUNKED instance) records,
+// for every CHUNK-entry chunk of a tile list that a pixel reaches, the transmittance after the
+// chunk and the colour composited in it; its epilogue turns these into the normalised colour
+// behind each chunk (suffix sums of positive terms + T_final bg, no cancellation).  The backward
+// then gives every chunk its own CTA (the whole tile, two pixels per lane), which replays that
+// chunk back to front from (T after the chunk, colour behind it) -- the chunks run in parallel
+// instead of one after the other, and the longest dependent chain is CHUNK entries.
 
 __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ ranges, int VT,
                                                       uint32_t *__restrict__ chunk_base,
@@ -507,168 +527,6 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
         if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
 }
 
-struct ChunkPix {
-    int view, tx, ty, lx, ly, px, py;
-    float wx0, wy0;
-    uint2 range;
-    int b0, cnt;  // chunk offset in the tile list, entries in the chunk
-};
-
-// chunk c, warp block wb (0..7) of its tile
-__device__ __forceinline__ ChunkPix chunk_pixel(int c, int wb, const uint2 *ranges, const uint32_t *chunk_base,
-                                                const uint32_t *chunk_tile, int TX, int tiles) {
-    ChunkPix q;
-    const uint32_t gt = chunk_tile[c];
-    q.view = gt / tiles;
-    const int tl = gt % tiles;
-    q.tx = tl % TX;
-    q.ty = tl / TX;
-    const int lane = threadIdx.x & 31;
-    const int bx = (wb & 1) * 8, by = (wb >> 1) * 4;
-    q.lx = bx + (lane & 7);
-    q.ly = by + (lane >> 3);
-    q.px = q.tx * TILE + q.lx;
-    q.py = q.ty * TILE + q.ly;
-    q.wx0 = (float)(q.tx * TILE + bx);
-    q.wy0 = (float)(q.ty * TILE + by);
-    q.range = ranges[gt];
-    q.b0 = (int)(c - chunk_base[gt]) * CHUNK;
-    q.cnt = min(CHUNK, (int)(q.range.y - q.range.x) - q.b0);
-    return q;
-}
-
-// ordered per-warp list of the batch slots that can reach the warp's block; REVERSE walks the
-// batch back to front and keeps only 1-based list positions b0 + slot + 1 <= lim
-template <bool REVERSE>
-__device__ __forceinline__ int compact_block(const float4 *r, int cnt, float x0, float y0, int b0, uint32_t lim,
-                                             uint8_t *wl) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    int nsel = 0;
-    for (int k = 0; k < cnt; k += 32) {
-        const int jj = k + lane;
-        const int idx = REVERSE ? cnt - 1 - jj : jj;
-        bool hit = jj < cnt && (uint32_t)(b0 + idx + 1) <= lim &&
-                   !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, x0, y0);
-        unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (hit) wl[nsel + __popc(b & lt)] = (uint8_t)idx;
-        nsel += __popc(b);
-    }
-    __syncwarp();
-    return nsel;
-}
-
-__device__ __forceinline__ void chunk_load(float4 *dst, const float4 *prec, const ChunkPix &q, uint64_t *bar,
-                                           uint32_t parity) {
-    if ((threadIdx.x & 31) == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_load(dst, prec + 3 * ((size_t)q.range.x + q.b0), (uint32_t)q.cnt * 48u, bar);
-    }
-    __syncwarp();
-    mbar_wait(bar, parity);
-}
-
-__global__ void __launch_bounds__(32) k_raster_bwd_chunk(const uint2 *__restrict__ ranges,
-                                                         const float4 *__restrict__ prec,
-                                                         const uint32_t *__restrict__ chunk_base,
-                                                         const uint32_t *__restrict__ chunk_tile,
-                                                         const WsHeader *__restrict__ hdr, int64_t n, int W, int H,
-                                                         int TX, int tiles, const float *__restrict__ dL_drgb,
-                                                         const uint32_t *__restrict__ ncontrib,
-                                                         const float4 *__restrict__ chunk_bwd,
-                                                         float4 *__restrict__ g2d) {
-    __shared__ __align__(128) float4 rec[CHUNK * 3];
-    __shared__ uint64_t bar;
-    __shared__ uint8_t wl[CHUNK];
-    const int c = blockIdx.x >> 3;
-    if (c >= (int)hdr->nchunks) return;
-    const ChunkPix q = chunk_pixel(c, blockIdx.x & 7, ranges, chunk_base, chunk_tile, TX, tiles);
-    const int lane = threadIdx.x & 31;
-    const bool inside = q.px < W && q.py < H;
-    const int64_t HW = (int64_t)H * W;
-    const int64_t pix = (int64_t)q.py * W + q.px;
-    uint32_t last = 0;
-    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, g_0 = 0.f, g_1 = 0.f, g_2 = 0.f;
-    if (inside) {
-        last = ncontrib[(int64_t)q.view * HW + pix];
-        if ((uint32_t)q.b0 < last) {  // this chunk holds composited entries of the pixel
-            const float4 e = chunk_bwd[(size_t)c * CHUNK + q.ly * TILE + q.lx];
-            T = e.x;
-            acc0 = e.y;
-            acc1 = e.z;
-            acc2 = e.w;
-            const float *g = dL_drgb + (int64_t)q.view * 3 * HW + pix;
-            g_0 = g[0];
-            g_1 = g[HW];
-            g_2 = g[2 * HW];
-        } else {
-            last = 0;
-        }
-    }
-    uint32_t wlast = last;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
-    if (wlast == 0) return;  // warp-uniform
-    if (threadIdx.x == 0) {
-        mbar_init(&bar);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    chunk_load(rec, prec, q, &bar, 0u);
-    const int nsel = compact_block<true>(rec, q.cnt, q.wx0, q.wy0, q.b0, wlast, wl);
-    const float fx = (float)q.px, fy = (float)q.py;
-    const int64_t vbase = (int64_t)q.view * n;
-    for (int t = 0; t < nsel; t++) {
-        const int j = wl[t];
-        const uint32_t position = (uint32_t)(q.b0 + j + 1);
-        const float4 g0 = rec[3 * j], g1 = rec[3 * j + 1];
-        float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
-        float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
-        bool contrib = false;
-        if (position <= last) {
-            float dx, dy;
-            const float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
-            if (!(power > 0.0f || power < POWER_CUT)) {
-                const float e = fast_exp(power);
-                const float a_raw = g1.y * e;
-                const float alpha = fminf(ALPHA_MAX, a_raw);
-                if (alpha >= ALPHA_MIN) {
-                    contrib = true;
-                    T = __fdividef(T, 1.0f - alpha);
-                    const float w = alpha * T;
-                    dLdr = g_0 * w;
-                    dLdg = g_1 * w;
-                    dLdb = g_2 * w;
-                    const float d0 = g1.z - acc0, d1 = g1.w - acc1, d2 = rec[3 * j + 2].x - acc2;
-                    const float dLda = T * (g_0 * d0 + g_1 * d1 + g_2 * d2);
-                    acc0 += alpha * d0;
-                    acc1 += alpha * d1;
-                    acc2 += alpha * d2;
-                    if (!(a_raw > ALPHA_MAX)) {
-                        dLdsig = e * dLda;
-                        const float dLdp = alpha * dLda;
-                        dLdu = dLdp * dx;
-                        dLdv = dLdp * dy;
-                        dLdA = dLdu * dx;
-                        dLdB = dLdu * dy;
-                        dLdC = dLdv * dy;
-                    }
-                }
-            }
-        }
-        if (__any_sync(0xffffffffu, contrib)) {
-            float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
-            const float mine = warp_sum8_transposed(vals8, lane);
-            const float bsum = warp_sum(dLdb);
-            const uint32_t gi = __float_as_uint(rec[3 * j + 2].y);
-            float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
-            if ((lane & 3) == 0)
-                atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
-            if (lane == 1) atomicAdd(dst + 8, bsum);
-        }
-    }
-}
-
 // ================================================================ two-pixel packed backward
 // Backward for levels with many tiles: a warp owns an 8x8 block and every lane two pixels
 // (x, y) and (x, y + 4), evaluated with Blackwell's packed fp32x2 instructions (FFMA2 / FMUL2 /
@@ -681,6 +539,62 @@ __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// Per-lane state of the two pixels (x, y) and (x, y + 4) in the back-to-front replay.
+struct Pix2 {
+    float2 T, acc0, acc1, acc2, g0, g1, g2;  // T after the entry, colour behind, dL/dpixel
+    uint32_t lastA, lastB;                   // 1-based list position of the last composited
+};
+
+// One list entry j (1-based list position `position`) of the replay for the warp's 64 pixels:
+// recover T before it, dL/dalpha = T sum_c g_c (c - acc), then the gradient moments
+// S(a), S(b), S(a dx), S(a dy), S(b dy) with a = dL/dpower dx, b = dL/dpower dy, dL/dsigma and
+// dL/dcolour summed over the warp and added to the Gaussian's per-view record.
+__device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint32_t position, float fx,
+                                           float2 fy2, int lane, int64_t vbase, float4 *g2d) {
+    const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
+    // power per pixel in the recipe's op order (bit-identical to pixel_power)
+    const float dx = SUB(fx, g0.x);
+    const float2 dy2 = __fadd2_rn(fy2, f2(-g0.y));
+    const float Adxdx = MUL(MUL(g0.z, dx), dx);
+    const float2 qf2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(Adxdx));
+    const float2 p2 = __ffma2_rn(f2(-MUL(g0.w, dx)), dy2, __fmul2_rn(f2(-0.5f), qf2));
+    const float2 e2 = make_float2(fast_exp(p2.x), fast_exp(p2.y));
+    const float2 araw = __fmul2_rn(f2(g1.y), e2);
+    const float aA = fminf(ALPHA_MAX, araw.x), aB = fminf(ALPHA_MAX, araw.y);
+    const bool vA = position <= P.lastA && !(p2.x > 0.0f || p2.x < POWER_CUT) && aA >= ALPHA_MIN;
+    const bool vB = position <= P.lastB && !(p2.y > 0.0f || p2.y < POWER_CUT) && aB >= ALPHA_MIN;
+    if (!__any_sync(0xffffffffu, vA || vB)) return;
+    const float2 al = make_float2(vA ? aA : 0.f, vB ? aB : 0.f);            // masked alpha
+    const float2 ua = make_float2(vA && !(araw.x > ALPHA_MAX) ? aA : 0.f,  // unclamped part
+                                  vB && !(araw.y > ALPHA_MAX) ? aB : 0.f);
+    const float2 ue = make_float2(ua.x != 0.f ? e2.x : 0.f, ua.y != 0.f ? e2.y : 0.f);
+    P.T = __fmul2_rn(P.T, make_float2(rcp_approx(1.0f - al.x), rcp_approx(1.0f - al.y)));
+    const float2 w2 = __fmul2_rn(al, P.T);
+    const float2 d0 = __fadd2_rn(f2(g1.z), make_float2(-P.acc0.x, -P.acc0.y));
+    const float2 d1 = __fadd2_rn(f2(g1.w), make_float2(-P.acc1.x, -P.acc1.y));
+    const float2 d2 = __fadd2_rn(f2(r[3 * j + 2].x), make_float2(-P.acc2.x, -P.acc2.y));
+    const float2 dLda = __fmul2_rn(P.T, __ffma2_rn(P.g2, d2, __ffma2_rn(P.g1, d1, __fmul2_rn(P.g0, d0))));
+    P.acc0 = __ffma2_rn(al, d0, P.acc0);
+    P.acc1 = __ffma2_rn(al, d1, P.acc1);
+    P.acc2 = __ffma2_rn(al, d2, P.acc2);
+    const float2 dr = __fmul2_rn(P.g0, w2), dg = __fmul2_rn(P.g1, w2), db = __fmul2_rn(P.g2, w2);
+    const float2 dsig = __fmul2_rn(ue, dLda);
+    const float2 dp = __fmul2_rn(ua, dLda);
+    const float2 a2 = __fmul2_rn(dp, f2(dx));
+    const float2 b2 = __fmul2_rn(dp, dy2);
+    const float2 qa = __fmul2_rn(a2, f2(dx));
+    const float2 qb = __fmul2_rn(a2, dy2);
+    const float2 qc = __fmul2_rn(b2, dy2);
+    float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
+                      qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
+    const float mine = warp_sum8_transposed(vals8, lane);
+    const float bsum = warp_sum(db.x + db.y);
+    const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
+    float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
+    if ((lane & 3) == 0) atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
+    if (lane == 1) atomicAdd(dst + 8, bsum);
 }
 
 __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ ranges,
@@ -707,22 +621,24 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
     const int64_t vbase = (int64_t)view * n;
     const int64_t HW = (int64_t)H * W;
     const int64_t pixA = (int64_t)pyA * W + px, pixB = (int64_t)pyB * W + px;
-    float2 T2 = f2(1.f), g0v = f2(0.f), g1v = f2(0.f), g2v = f2(0.f);
-    uint32_t lastA = 0, lastB = 0;
+    Pix2 P;
+    P.T = f2(1.f);
+    P.g0 = P.g1 = P.g2 = f2(0.f);
+    P.lastA = P.lastB = 0;
     const float *gbase = dL_drgb + (int64_t)view * 3 * HW;
     if (inA) {
-        T2.x = T_keep[(int64_t)view * HW + pixA];
-        lastA = ncontrib[(int64_t)view * HW + pixA];
-        g0v.x = gbase[pixA];
-        g1v.x = gbase[HW + pixA];
-        g2v.x = gbase[2 * HW + pixA];
+        P.T.x = T_keep[(int64_t)view * HW + pixA];
+        P.lastA = ncontrib[(int64_t)view * HW + pixA];
+        P.g0.x = gbase[pixA];
+        P.g1.x = gbase[HW + pixA];
+        P.g2.x = gbase[2 * HW + pixA];
     }
     if (inB) {
-        T2.y = T_keep[(int64_t)view * HW + pixB];
-        lastB = ncontrib[(int64_t)view * HW + pixB];
-        g0v.y = gbase[pixB];
-        g1v.y = gbase[HW + pixB];
-        g2v.y = gbase[2 * HW + pixB];
+        P.T.y = T_keep[(int64_t)view * HW + pixB];
+        P.lastB = ncontrib[(int64_t)view * HW + pixB];
+        P.g0.y = gbase[pixB];
+        P.g1.y = gbase[HW + pixB];
+        P.g2.y = gbase[2 * HW + pixB];
     }
     if (tid == 0) {
         s_maxlast = 0;
@@ -731,7 +647,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t wlast = max(lastA, lastB);
+    uint32_t wlast = max(P.lastA, P.lastB);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
     if (lane == 0) atomicMax(&s_maxlast, wlast);
@@ -743,7 +659,9 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
     }
     uint32_t phases = 0u;
-    float2 acc0 = f2(bg0), acc1 = f2(bg1), acc2 = f2(bg2);
+    P.acc0 = f2(bg0);
+    P.acc1 = f2(bg1);
+    P.acc2 = f2(bg2);
     const unsigned lt = (1u << lane) - 1u;
     for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
         const int buf = it & 1;
@@ -771,52 +689,105 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         __syncwarp();
         for (int t = 0; t < nsel; t++) {
             const int j = wl[warp][t];
-            const uint32_t position = (uint32_t)(b_start + j + 1);
-            const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
-            // power per pixel in the recipe's op order (bit-identical to pixel_power)
-            const float dx = SUB(fx, g0.x);
-            const float2 dy2 = __fadd2_rn(fy2, f2(-g0.y));
-            const float Adxdx = MUL(MUL(g0.z, dx), dx);
-            const float2 qf2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(Adxdx));
-            const float2 p2 = __ffma2_rn(f2(-MUL(g0.w, dx)), dy2, __fmul2_rn(f2(-0.5f), qf2));
-            const float2 e2 = make_float2(fast_exp(p2.x), fast_exp(p2.y));
-            const float2 araw = __fmul2_rn(f2(g1.y), e2);
-            const float aA = fminf(ALPHA_MAX, araw.x), aB = fminf(ALPHA_MAX, araw.y);
-            const bool vA = position <= lastA && !(p2.x > 0.0f || p2.x < POWER_CUT) && aA >= ALPHA_MIN;
-            const bool vB = position <= lastB && !(p2.y > 0.0f || p2.y < POWER_CUT) && aB >= ALPHA_MIN;
-            if (!__any_sync(0xffffffffu, vA || vB)) continue;
-            const float2 al = make_float2(vA ? aA : 0.f, vB ? aB : 0.f);            // masked alpha
-            const float2 ua = make_float2(vA && !(araw.x > ALPHA_MAX) ? aA : 0.f,  // unclamped part
-                                          vB && !(araw.y > ALPHA_MAX) ? aB : 0.f);
-            const float2 ue = make_float2(ua.x != 0.f ? e2.x : 0.f, ua.y != 0.f ? e2.y : 0.f);
-            T2 = __fmul2_rn(T2, make_float2(rcp_approx(1.0f - al.x), rcp_approx(1.0f - al.y)));
-            const float2 w2 = __fmul2_rn(al, T2);
-            const float2 d0 = __fadd2_rn(f2(g1.z), make_float2(-acc0.x, -acc0.y));
-            const float2 d1 = __fadd2_rn(f2(g1.w), make_float2(-acc1.x, -acc1.y));
-            const float cb = r[3 * j + 2].x;
-            const float2 d2 = __fadd2_rn(f2(cb), make_float2(-acc2.x, -acc2.y));
-            const float2 dLda = __fmul2_rn(T2, __ffma2_rn(g2v, d2, __ffma2_rn(g1v, d1, __fmul2_rn(g0v, d0))));
-            acc0 = __ffma2_rn(al, d0, acc0);
-            acc1 = __ffma2_rn(al, d1, acc1);
-            acc2 = __ffma2_rn(al, d2, acc2);
-            const float2 dr = __fmul2_rn(g0v, w2), dg = __fmul2_rn(g1v, w2), db = __fmul2_rn(g2v, w2);
-            const float2 dsig = __fmul2_rn(ue, dLda);
-            const float2 dp = __fmul2_rn(ua, dLda);
-            const float2 a2 = __fmul2_rn(dp, f2(dx));
-            const float2 b2 = __fmul2_rn(dp, dy2);
-            const float2 qa = __fmul2_rn(a2, f2(dx));
-            const float2 qb = __fmul2_rn(a2, dy2);
-            const float2 qc = __fmul2_rn(b2, dy2);
-            float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
-                              qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
-            const float mine = warp_sum8_transposed(vals8, lane);
-            const float bsum = warp_sum(db.x + db.y);
-            const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
-            float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
-            if ((lane & 3) == 0)
-                atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
-            if (lane == 1) atomicAdd(dst + 8, bsum);
+            bwd2_entry(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, vbase, g2d);
         }
+    }
+}
+
+// Chunked backward with the two-pixel layout: one CTA (4 warps, 8x8 blocks) per chunk; the
+// chunk's records are loaded once for the whole tile.
+__global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restrict__ ranges,
+                                                           const float4 *__restrict__ prec,
+                                                           const uint32_t *__restrict__ chunk_base,
+                                                           const uint32_t *__restrict__ chunk_tile,
+                                                           const WsHeader *__restrict__ hdr, int64_t n, int W,
+                                                           int H, int TX, int tiles,
+                                                           const float *__restrict__ dL_drgb,
+                                                           const uint32_t *__restrict__ ncontrib,
+                                                           const float4 *__restrict__ chunk_bwd,
+                                                           float4 *__restrict__ g2d) {
+    __shared__ __align__(128) float4 rec[CHUNK * 3];
+    __shared__ uint64_t bar;
+    __shared__ uint8_t wl[4][CHUNK];
+    const int c = blockIdx.x;
+    if (c >= (int)hdr->nchunks) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t gt = chunk_tile[c];
+    const int view = gt / tiles, tl = gt % tiles;
+    const int tx = tl % TX, ty = tl / TX;
+    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
+    const int lx = bx + (lane & 7), lyA = by + (lane >> 3);
+    const int px = tx * TILE + lx, pyA = ty * TILE + lyA, pyB = pyA + 4;
+    const uint2 range = ranges[gt];
+    const int b0 = (int)(c - chunk_base[gt]) * CHUNK;
+    const int cnt = min(CHUNK, (int)(range.y - range.x) - b0);
+    const int64_t HW = (int64_t)H * W;
+    Pix2 P;
+    P.T = f2(1.f);
+    P.acc0 = P.acc1 = P.acc2 = P.g0 = P.g1 = P.g2 = f2(0.f);
+    P.lastA = P.lastB = 0;
+    const float *gbase = dL_drgb + (int64_t)view * 3 * HW;
+    const float4 *cb = chunk_bwd + (size_t)c * TILE_PIX;
+    if (px < W && pyA < H) {
+        const int64_t pix = (int64_t)pyA * W + px;
+        const uint32_t last = ncontrib[(int64_t)view * HW + pix];
+        if ((uint32_t)b0 < last) {  // this chunk holds composited entries of the pixel
+            const float4 e = cb[lyA * TILE + lx];
+            P.lastA = last;
+            P.T.x = e.x;
+            P.acc0.x = e.y;
+            P.acc1.x = e.z;
+            P.acc2.x = e.w;
+            P.g0.x = gbase[pix];
+            P.g1.x = gbase[HW + pix];
+            P.g2.x = gbase[2 * HW + pix];
+        }
+    }
+    if (px < W && pyB < H) {
+        const int64_t pix = (int64_t)pyB * W + px;
+        const uint32_t last = ncontrib[(int64_t)view * HW + pix];
+        if ((uint32_t)b0 < last) {
+            const float4 e = cb[(lyA + 4) * TILE + lx];
+            P.lastB = last;
+            P.T.y = e.x;
+            P.acc0.y = e.y;
+            P.acc1.y = e.z;
+            P.acc2.y = e.w;
+            P.g0.y = gbase[pix];
+            P.g1.y = gbase[HW + pix];
+            P.g2.y = gbase[2 * HW + pix];
+        }
+    }
+    uint32_t wlast = max(P.lastA, P.lastB);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (tid == 0) {
+        mbar_init(&bar);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (__syncthreads_or(wlast != 0) == 0) return;  // no pixel of the tile reaches this chunk
+    if (tid == 0) bulk_load(rec, prec + 3 * ((size_t)range.x + b0), (uint32_t)cnt * 48u, &bar);
+    if (wlast == 0) return;  // warp-uniform; the copy is waited on by the warps that use it
+    mbar_wait(&bar, 0u);
+    const unsigned lt = (1u << lane) - 1u;
+    const float wx0 = (float)(tx * TILE + bx), wy0 = (float)(ty * TILE + by);
+    int nsel = 0;
+    for (int k = 0; k < cnt; k += 32) {
+        const int jj = k + lane;
+        const int idx = cnt - 1 - jj;
+        bool hit = jj < cnt && (uint32_t)(b0 + idx + 1) <= wlast &&
+                   !block_misses(rec[3 * idx], rec[3 * idx + 1], rec[3 * idx + 2].w, wx0, wy0, 7.f);
+        unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
+        nsel += __popc(b);
+    }
+    __syncwarp();
+    const float fx = (float)px;
+    const float2 fy2 = make_float2((float)pyA, (float)pyB);
+    const int64_t vbase = (int64_t)view * n;
+    for (int t = 0; t < nsel; t++) {
+        const int j = wl[warp][t];
+        bwd2_entry(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, vbase, g2d);
     }
 }
 
@@ -849,10 +820,10 @@ template <int WARPS>
 static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                        const uint32_t *cbase, float4 *cbwd, cudaStream_t s) {
     dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
-    k_raster_fwd<WARPS><<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX,
-                                                    L.tiles, bg[0], bg[1], bg[2], out_rgb, out_T,
-                                                    at<float>(ws, L.Tfinal), at<uint32_t>(ws, L.ncontrib),
-                                                    at<uint32_t>(ws, L.ncomp), cbase, cbwd);
+    auto kern = cbwd ? k_raster_fwd<WARPS, true> : k_raster_fwd<WARPS, false>;
+    kern<<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX, L.tiles, bg[0],
+                                     bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
+                                     at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd);
 }
 
 template <int WARPS>
@@ -886,7 +857,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     ProfScope prof("k_raster_bwd", s);
     if (L.max_chunks > 0) {  // chunked path (few tiles): every chunk replayed independently
-        k_raster_bwd_chunk<<<(unsigned)(L.max_chunks * 8), 32, 0, s>>>(
+        k_raster_bwd2_chunk<<<(unsigned)L.max_chunks, 128, 0, s>>>(
             at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
             at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
