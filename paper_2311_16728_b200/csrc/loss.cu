@@ -16,11 +16,13 @@
 
 namespace gsk {
 
-constexpr int LT = 16;          // output tile
-constexpr int HALO = 5;         // 11-tap window radius
-constexpr int LS = LT + 2 * HALO;  // 26
-constexpr int LSP = 48;         // padded row stride: the two half-warps of a row pass read
-                                // disjoint bank halves (48 = 16 mod 32)
+constexpr int TW = 32, TH = 32;  // output tile (columns x rows)
+constexpr int HALO = 5;           // 11-tap window radius
+constexpr int SW = TW + 2 * HALO, SH = TH + 2 * HALO;  // 42 x 42 input patch
+constexpr int SWP = SW + 1;       // padded row stride
+constexpr int NT = 256;           // threads per CTA
+constexpr int HC = 4;             // horizontal pass: consecutive output columns per thread
+constexpr int VR = 4;             // vertical pass: consecutive output rows per thread
 
 struct Win {
     float g[11];
@@ -40,89 +42,138 @@ static Win make_window() {
 constexpr float SS_C1 = 0.01f * 0.01f;
 constexpr float SS_C2 = 0.03f * 0.03f;
 
-// grid: (ceil(W/16), ceil(H/16), V*3); partial maps dA, dB, dC [V][3][H][W];
-// block partial sums part[(v*3 + c) * nbt + bt][2] = (sum |x-y|, sum SSIM)
-__global__ void __launch_bounds__(LT *LT) k_ssim_fwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
-                                                     int W, Win win, float *__restrict__ dA, float *__restrict__ dB,
-                                                     float *__restrict__ dC, float2 *__restrict__ part) {
-    __shared__ float sx[LS][LSP], sy[LS][LSP];
-    __shared__ float h[5][LS][LT];
-    __shared__ float red[2][LT * LT / 32];
+// Load the (TH + 10) x (TW + 10) patches of M maps around the tile into smem (zero outside the
+// image).  All global loads are issued before the first shared store, so their latencies overlap.
+template <int M>
+__device__ __forceinline__ void load_patches(float (*dst)[SH][SWP], const float *const (&src)[M], int H, int W,
+                                             int x0, int y0) {
+    constexpr int IT = (SH * SW + NT - 1) / NT;
+    float v[M][IT];
+#pragma unroll
+    for (int i = 0; i < IT; i++) {
+        const int k = threadIdx.x + i * NT;
+        const int r = k / SW, c = k % SW;
+        const int gy = y0 + r, gx = x0 + c;
+        const bool ok = k < SH * SW && gy >= 0 && gy < H && gx >= 0 && gx < W;
+#pragma unroll
+        for (int m = 0; m < M; m++) v[m][i] = ok ? __ldg(src[m] + (int64_t)gy * W + gx) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < IT; i++) {
+        const int k = threadIdx.x + i * NT;
+        if (k < SH * SW)
+#pragma unroll
+            for (int m = 0; m < M; m++) dst[m][k / SW][k % SW] = v[m][i];
+    }
+}
+
+// grid: (ceil(W/TW), ceil(H/TH), V*3); partial maps dA, dB, dC [V][3][H][W];
+// block partial sums part[(v*3 + c) * nbt + bt] = (sum |x-y|, sum SSIM).
+// Register blocking: the horizontal pass gives each thread HC adjacent outputs of one row (the
+// 10 + HC inputs are loaded once), the vertical pass VR adjacent outputs of one column.
+__global__ void __launch_bounds__(NT) k_ssim_fwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
+                                                 int W, Win win, float *__restrict__ dA, float *__restrict__ dB,
+                                                 float *__restrict__ dC, float2 *__restrict__ part) {
+    __shared__ float sxy[2][SH][SWP];
+    __shared__ float hm[5][SH][TW + 1];
+    float (*sx)[SWP] = sxy[0];
+    float (*sy)[SWP] = sxy[1];
+    __shared__ float red[2][NT / 32];
     const int plane = blockIdx.z;  // v*3 + c
     const int64_t HW = (int64_t)H * W;
-    const float *x = X + plane * HW, *y = Y + plane * HW;
-    const int x0 = blockIdx.x * LT - HALO, y0 = blockIdx.y * LT - HALO;
     const int tid = threadIdx.x;
-    for (int k = tid; k < LS * LS; k += LT * LT) {
-        int r = k / LS, c = k % LS;
-        int gy = y0 + r, gx = x0 + c;
-        bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        sx[r][c] = ok ? x[(int64_t)gy * W + gx] : 0.f;
-        sy[r][c] = ok ? y[(int64_t)gy * W + gx] : 0.f;
-    }
+    const float *const srcs[2] = {X + plane * HW, Y + plane * HW};
+    load_patches<2>(sxy, srcs, H, W, blockIdx.x * TW - HALO, blockIdx.y * TH - HALO);
     __syncthreads();
-    // horizontal pass over all LS rows, LT output columns
-    for (int k = tid; k < LS * LT; k += LT * LT) {
-        int r = k / LT, c = k % LT;
-        float a = 0, b = 0, aa = 0, bb = 0, ab = 0;
+    // horizontal pass: SH rows x TW columns of the five moment maps (x, y, x^2, y^2, xy)
+    for (int it = tid; it < SH * (TW / HC); it += NT) {
+        const int r = it / (TW / HC), c0 = (it % (TW / HC)) * HC;
+        float a[HC] = {}, b[HC] = {}, aa[HC] = {}, bb[HC] = {}, ab[HC] = {};
 #pragma unroll
-        for (int j = 0; j < 11; j++) {
-            float xv = sx[r][c + j], yv = sy[r][c + j], w = win.g[j];
-            a += w * xv;
-            b += w * yv;
-            aa += w * xv * xv;
-            bb += w * yv * yv;
-            ab += w * xv * yv;
+        for (int j = 0; j < 10 + HC; j++) {
+            const float xv = sx[r][c0 + j], yv = sy[r][c0 + j];
+            const float xx = xv * xv, yy = yv * yv, xy = xv * yv;
+#pragma unroll
+            for (int o = 0; o < HC; o++) {
+                const int t = j - o;  // tap index of input j for output o
+                if (t >= 0 && t < 11) {
+                    const float w = win.g[t];
+                    a[o] += w * xv;
+                    b[o] += w * yv;
+                    aa[o] += w * xx;
+                    bb[o] += w * yy;
+                    ab[o] += w * xy;
+                }
+            }
         }
-        h[0][r][c] = a; h[1][r][c] = b; h[2][r][c] = aa; h[3][r][c] = bb; h[4][r][c] = ab;
+#pragma unroll
+        for (int o = 0; o < HC; o++) {
+            hm[0][r][c0 + o] = a[o];
+            hm[1][r][c0 + o] = b[o];
+            hm[2][r][c0 + o] = aa[o];
+            hm[3][r][c0 + o] = bb[o];
+            hm[4][r][c0 + o] = ab[o];
+        }
     }
     __syncthreads();
-    const int r = tid / LT, c = tid % LT;
-    const int gy = blockIdx.y * LT + r, gx = blockIdx.x * LT + c;
-    float mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+    // vertical pass: column c, rows r0 .. r0 + VR - 1
+    const int c = tid % TW, r0 = (tid / TW) * VR;
+    float mom[5][VR] = {};
 #pragma unroll
-    for (int i = 0; i < 11; i++) {
-        float w = win.g[i];
-        mx += w * h[0][r + i][c];
-        my += w * h[1][r + i][c];
-        exx += w * h[2][r + i][c];
-        eyy += w * h[3][r + i][c];
-        exy += w * h[4][r + i][c];
+    for (int j = 0; j < 10 + VR; j++) {
+        float v[5];
+#pragma unroll
+        for (int m = 0; m < 5; m++) v[m] = hm[m][r0 + j][c];
+#pragma unroll
+        for (int o = 0; o < VR; o++) {
+            const int t = j - o;
+            if (t >= 0 && t < 11) {
+#pragma unroll
+                for (int m = 0; m < 5; m++) mom[m][o] += win.g[t] * v[m];
+            }
+        }
     }
-    float l1 = 0.f, S = 0.f;
-    if (gy < H && gx < W) {
-        float sxx = exx - mx * mx, syy = eyy - my * my, sxy = exy - mx * my;
-        float a1 = 2.f * mx * my + SS_C1, a2 = 2.f * sxy + SS_C2;
-        float b1 = mx * mx + my * my + SS_C1, b2 = sxx + syy + SS_C2;
-        float ib = 1.f / (b1 * b2);
-        S = a1 * a2 * ib;
-        float dS_dmx = 2.f * my * a2 * ib - S * 2.f * mx / b1;
-        float dS_dsxx = -S / b2;
-        float dS_dsxy = 2.f * a1 * ib;
-        int64_t o = plane * HW + (int64_t)gy * W + gx;
-        dA[o] = dS_dmx + dS_dsxx * (-2.f * mx) + dS_dsxy * (-my);
-        dB[o] = dS_dsxx;
-        dC[o] = dS_dsxy;
-        l1 = fabsf(sx[r + HALO][c + HALO] - sy[r + HALO][c + HALO]);
+    float l1 = 0.f, S_sum = 0.f;
+    const int gx = blockIdx.x * TW + c;
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        const int gy = blockIdx.y * TH + r0 + o;
+        if (gy < H && gx < W) {
+            const float mx = mom[0][o], my = mom[1][o];
+            const float sxx = mom[2][o] - mx * mx, syy = mom[3][o] - my * my, sxy = mom[4][o] - mx * my;
+            const float a1 = 2.f * mx * my + SS_C1, a2 = 2.f * sxy + SS_C2;
+            const float b1 = mx * mx + my * my + SS_C1, b2 = sxx + syy + SS_C2;
+            const float ib = 1.f / (b1 * b2);
+            const float S = a1 * a2 * ib;
+            const float dS_dmx = 2.f * my * a2 * ib - S * 2.f * mx / b1;
+            const float dS_dsxx = -S / b2;
+            const float dS_dsxy = 2.f * a1 * ib;
+            const int64_t o_ = plane * HW + (int64_t)gy * W + gx;
+            dA[o_] = dS_dmx + dS_dsxx * (-2.f * mx) + dS_dsxy * (-my);
+            dB[o_] = dS_dsxx;
+            dC[o_] = dS_dsxy;
+            S_sum += S;
+            l1 += fabsf(sx[r0 + o + HALO][c + HALO] - sy[r0 + o + HALO][c + HALO]);
+        }
     }
     // block reduction (fixed order)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-        S += __shfl_xor_sync(0xffffffffu, S, o);
+        S_sum += __shfl_xor_sync(0xffffffffu, S_sum, o);
     }
     if ((tid & 31) == 0) {
         red[0][tid >> 5] = l1;
-        red[1][tid >> 5] = S;
+        red[1][tid >> 5] = S_sum;
     }
     __syncthreads();
     if (tid == 0) {
         float a = 0, b = 0;
-        for (int k = 0; k < LT * LT / 32; k++) {
+        for (int k = 0; k < NT / 32; k++) {
             a += red[0][k];
             b += red[1][k];
         }
-        int nbt = gridDim.x * gridDim.y;
+        const int nbt = gridDim.x * gridDim.y;
         part[(int64_t)plane * nbt + blockIdx.y * gridDim.x + blockIdx.x] = make_float2(a, b);
     }
 }
@@ -163,67 +214,91 @@ __global__ void __launch_bounds__(256) k_loss_final(const float2 *__restrict__ p
     finalize_view(part, blockIdx.x, nbt, lambda, invN, loss);
 }
 
-__global__ void __launch_bounds__(LT *LT) k_ssim_bwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
-                                                     int W, Win win, float lambda, float invN,
-                                                     const float *__restrict__ dA, const float *__restrict__ dB,
-                                                     const float *__restrict__ dC, float *__restrict__ dL,
-                                                     const float2 *__restrict__ part, float *__restrict__ loss) {
-    __shared__ float s[3][LS][LSP];
-    __shared__ float h[3][LS][LT];
+__global__ void __launch_bounds__(NT) k_ssim_bwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
+                                                 int W, Win win, float lambda, float invN,
+                                                 const float *__restrict__ dA, const float *__restrict__ dB,
+                                                 const float *__restrict__ dC, float *__restrict__ dL,
+                                                 const float2 *__restrict__ part, float *__restrict__ loss) {
+    __shared__ float s[3][SH][SWP];
+    __shared__ float hm[3][SH][TW + 1];
     const int plane = blockIdx.z;
     const int64_t HW = (int64_t)H * W;
-    const int x0 = blockIdx.x * LT - HALO, y0 = blockIdx.y * LT - HALO;
     const int tid = threadIdx.x;
-    for (int k = tid; k < LS * LS; k += LT * LT) {
-        int r = k / LS, c = k % LS;
-        int gy = y0 + r, gx = x0 + c;
-        bool ok = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        int64_t o = plane * HW + (int64_t)gy * W + gx;
-        s[0][r][c] = ok ? dA[o] : 0.f;
-        s[1][r][c] = ok ? dB[o] : 0.f;
-        s[2][r][c] = ok ? dC[o] : 0.f;
-    }
-    __syncthreads();
-    for (int k = tid; k < LS * LT; k += LT * LT) {
-        int r = k / LT, c = k % LT;
-        float a = 0, b = 0, cc = 0;
+    const int x0 = blockIdx.x * TW - HALO, y0 = blockIdx.y * TH - HALO;
+    // this thread's output pixels: column c, rows r0 .. r0 + VR - 1 (x, y prefetched now)
+    const int c = tid % TW, r0 = (tid / TW) * VR;
+    const int gx = blockIdx.x * TW + c;
+    float xv[VR], yv[VR];
 #pragma unroll
-        for (int j = 0; j < 11; j++) {
-            float w = win.g[j];
-            a += w * s[0][r][c + j];
-            b += w * s[1][r][c + j];
-            cc += w * s[2][r][c + j];
+    for (int o = 0; o < VR; o++) {
+        const int gy = blockIdx.y * TH + r0 + o;
+        const bool ok = gx < W && gy < H;
+        xv[o] = ok ? __ldg(X + plane * HW + (int64_t)gy * W + gx) : 0.f;
+        yv[o] = ok ? __ldg(Y + plane * HW + (int64_t)gy * W + gx) : 0.f;
+    }
+    const float *const srcs[3] = {dA + plane * HW, dB + plane * HW, dC + plane * HW};
+    load_patches<3>(s, srcs, H, W, x0, y0);
+    __syncthreads();
+    for (int it = tid; it < SH * (TW / HC); it += NT) {
+        const int r = it / (TW / HC), c0 = (it % (TW / HC)) * HC;
+        float acc[3][HC] = {};
+#pragma unroll
+        for (int j = 0; j < 10 + HC; j++) {
+            float v[3];
+#pragma unroll
+            for (int m = 0; m < 3; m++) v[m] = s[m][r][c0 + j];
+#pragma unroll
+            for (int o = 0; o < HC; o++) {
+                const int t = j - o;
+                if (t >= 0 && t < 11) {
+#pragma unroll
+                    for (int m = 0; m < 3; m++) acc[m][o] += win.g[t] * v[m];
+                }
+            }
         }
-        h[0][r][c] = a; h[1][r][c] = b; h[2][r][c] = cc;
+#pragma unroll
+        for (int o = 0; o < HC; o++) {
+#pragma unroll
+            for (int m = 0; m < 3; m++) hm[m][r][c0 + o] = acc[m][o];
+        }
     }
     __syncthreads();
-    const int r = tid / LT, c = tid % LT;
-    const int gy = blockIdx.y * LT + r, gx = blockIdx.x * LT + c;
     // the first CTA of each view also reduces that view's loss partials (written by k_ssim_fwd)
     if (blockIdx.x == 0 && blockIdx.y == 0 && plane % 3 == 0)
         finalize_view(part, plane / 3, gridDim.x * gridDim.y, lambda, invN, loss);
-    if (gy >= H || gx >= W) return;
-    float sa = 0, sb = 0, sc = 0;
+    float acc[3][VR] = {};
 #pragma unroll
-    for (int i = 0; i < 11; i++) {
-        float w = win.g[i];
-        sa += w * h[0][r + i][c];
-        sb += w * h[1][r + i][c];
-        sc += w * h[2][r + i][c];
+    for (int j = 0; j < 10 + VR; j++) {
+        float v[3];
+#pragma unroll
+        for (int m = 0; m < 3; m++) v[m] = hm[m][r0 + j][c];
+#pragma unroll
+        for (int o = 0; o < VR; o++) {
+            const int t = j - o;
+            if (t >= 0 && t < 11) {
+#pragma unroll
+                for (int m = 0; m < 3; m++) acc[m][o] += win.g[t] * v[m];
+            }
+        }
     }
-    int64_t o = plane * HW + (int64_t)gy * W + gx;
-    float xv = X[o], yv = Y[o];
-    float dssim = sa + 2.f * xv * sb + yv * sc;
-    float d = xv - yv;
-    float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    dL[o] = (1.f - lambda) * sgn * invN - lambda * dssim * invN;
+    if (gx >= W) return;
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        const int gy = blockIdx.y * TH + r0 + o;
+        if (gy >= H) break;
+        const int64_t o_ = plane * HW + (int64_t)gy * W + gx;
+        const float dssim = acc[0][o] + 2.f * xv[o] * acc[1][o] + yv[o] * acc[2][o];
+        const float d = xv[o] - yv[o];
+        const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        dL[o_] = (1.f - lambda) * sgn * invN - lambda * dssim * invN;
+    }
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t loss_ws_bytes(int V, int H, int W) {
     size_t plane = (size_t)V * 3 * H * W * sizeof(float);
-    size_t nbt = (size_t)((W + LT - 1) / LT) * ((H + LT - 1) / LT);
+    size_t nbt = (size_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH);
     return 3 * align256(plane) + align256((size_t)V * 3 * nbt * sizeof(float2));
 }
 
@@ -233,12 +308,12 @@ cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int 
     size_t plane = align256((size_t)V * 3 * H * W * sizeof(float));
     float *dA = at<float>(ws, 0), *dB = at<float>(ws, plane), *dC = at<float>(ws, 2 * plane);
     float2 *part = at<float2>(ws, 3 * plane);
-    dim3 grid((W + LT - 1) / LT, (H + LT - 1) / LT, V * 3);
+    dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, V * 3);
     const int nbt = grid.x * grid.y;
     float invN = (float)(1.0 / (3.0 * H * W));
-    k_ssim_fwd<<<grid, LT * LT, 0, s>>>(render, gt, H, W, win, dA, dB, dC, part);
+    k_ssim_fwd<<<grid, NT, 0, s>>>(render, gt, H, W, win, dA, dB, dC, part);
     if (dL)
-        k_ssim_bwd<<<grid, LT * LT, 0, s>>>(render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);
+        k_ssim_bwd<<<grid, NT, 0, s>>>(render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);
     else
         k_loss_final<<<V, 256, 0, s>>>(part, nbt, lambda, invN, loss);
     return cudaGetLastError();
