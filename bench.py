@@ -172,14 +172,18 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0) -> int:
+CHUNK_MAX_TILES = 600  # views x tiles below this use the chunked raster path (gs_internal.cuh)
+
+
+def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked: bool = False) -> int:
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
-    binning 0: bucket scatter, tile sort (2) / binning 1: duplicate, sort histogram, one pass per
-    8-bit digit, fixup, ranges (4 + passes); pair gather + raster fwd (2); loss (2); fused:
-    raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
+    binning 0: bucket scatter, warp tile sort, CTA tile sort (3) / binning 1: duplicate, sort
+    histogram, one pass per 8-bit digit, fixup, ranges (4 + passes); pair gather + raster fwd (2),
+    + chunk index on levels with few tiles (chunked raster path); loss (2); fused: raster bwd +
+    preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
-    binning_kernels = 2 if binning == 0 else 4 + passes
-    return 2 + binning_kernels + 2 + 2 + (3 if fused else 4)
+    binning_kernels = 3 if binning == 0 else 4 + passes
+    return 2 + binning_kernels + 2 + (1 if chunked else 0) + 2 + (3 if fused else 4)
 
 
 def run_ours(args):
@@ -388,11 +392,12 @@ def run_ours(args):
     total_views = len(cams) * world
     value = iters_per_step * total_views * args.steps / (ms_max * 1e-3)
     e2e_value = iters_per_step * total_views * args.steps / (e2e_ms * 1e-3)
-    levels_bits = []
+    launches_step = 2  # pyramid levels (k_pyr_down)
     for r in eng.renderers:
         t = r.ws.tiles_x * r.ws.tiles_y * len(cams)
-        levels_bits.append(32 + max(1, math.ceil(math.log2(max(t, 2)))))
-    launches = args.steps * (2 + sum(launches_per_iteration(b, world == 1) for b in levels_bits))
+        bits = 32 + max(1, math.ceil(math.log2(max(t, 2))))
+        launches_step += launches_per_iteration(bits, world == 1, chunked=t < CHUNK_MAX_TILES)
+    launches = args.steps * launches_step
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

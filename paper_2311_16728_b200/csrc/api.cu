@@ -60,6 +60,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.tile_start = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.tile_cursor = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
     L.bin_big = take((size_t)2 * L.cap * sizeof(uint64_t));
+    L.big_tiles = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.prec = take((size_t)3 * L.cap * sizeof(float4));
     L.max_chunks = use_chunked((int64_t)V * L.tiles) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;
     L.chunk_base = take((size_t)V * L.tiles * sizeof(uint32_t));
@@ -200,7 +201,7 @@ gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t 
     if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
     cudaStream_t s = (cudaStream_t)stream;
     WsHeader *hdr = at<WsHeader>(ws, L.hdr);
-    cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter, visible count
+    cudaMemsetAsync(hdr, 0, offsetof(WsHeader, hist_ctr), s);  // flags, P, scan counter, visible count, n_big
     cudaMemsetAsync(at<char>(ws, L.scan_flags), 0, (size_t)std::max<int64_t>(L.scan_blocks, 1) * 8, s);
     const bool buckets = binning_mode() == 0;
     if (buckets)

@@ -7,18 +7,21 @@
 //   2. an exclusive scan of the V*tiles counts gives each tile's range (and the total P);
 //   3. k_bin_scatter writes each pair's (depth_bits << 32 | gaussian id) into its tile's bucket
 //      (slot from a per-tile atomic cursor -- arbitrary order inside the bucket);
-//   4. k_tile_sort sorts every bucket by (depth_bits, id) in shared memory (bitonic network,
-//      padded to a power of two) -- (depth, id) is unique, so the order is exactly the stable
-//      order of the global sort -- and writes the sorted values, the full keys and the range.
-// Buckets longer than the shared-memory capacity (4096 pairs) are sorted with the same network
-// in global memory (correct, slower; only for extreme tile lists).  Compared with the global LSD sort
-// this reads/writes each pair ~3 times instead of 2 x (number of 8-bit digits) and replaces
-// ~10 dependent launches per iteration by 3.
+//   4. every bucket is sorted by (depth_bits, id) with a bitonic network padded to a power of
+//      two -- (depth, id) is unique, so the order is exactly the stable order of the global
+//      sort -- and the sorted values, the full keys and the range are written.  Buckets of up
+//      to 256 pairs are sorted by a group of two warps (k_tile_sort_small), longer ones are
+//      queued for k_tile_sort_big (a CTA of 16 warps, up to 4096 pairs; beyond that the same
+//      network in global memory -- correct, slower, only for extreme tile lists).  Keys live
+//      in registers; short exchange distances use shuffles, long ones shared memory.
+// Compared with the global LSD sort this reads/writes each pair ~3 times instead of
+// 2 x (number of 8-bit digits) and replaces ~10 dependent launches per iteration by 4.
+#include <algorithm>
+
 #include "gs_internal.cuh"
 
 namespace gsk {
 
-constexpr int TS_THREADS = 512;
 constexpr int TS_SMEM_KEYS = 4096;  // 32 KB of u64 keys per CTA
 
 // One thread per visible Gaussian (compacted list).  When the V*tiles table fits in shared
@@ -99,46 +102,157 @@ __device__ __forceinline__ void bitonic(uint64_t *a, int len) {
     }
 }
 
-__global__ void __launch_bounds__(TS_THREADS) k_tile_sort(const uint32_t *__restrict__ tile_start,
-                                                          const uint32_t *__restrict__ tile_count, int64_t cap,
-                                                          uint64_t *__restrict__ tmp, uint64_t *__restrict__ keys,
-                                                          uint32_t *__restrict__ vals, uint2 *__restrict__ ranges,
-                                                          uint64_t *__restrict__ big, const WsHeader *hdr) {
-    __shared__ uint64_t sk[TS_SMEM_KEYS];
-    const uint32_t gt = blockIdx.x;
+// ---- group bitonic sort: a group of W warps holds lp = 32 E W keys in registers; key g (its
+// bitonic index) = w * 32 E + e * 32 + lane (striped, so loads and stores coalesce).  Distances
+// j < 32 are exchanged with shuffles, 32 <= j < 32 E inside the thread, j >= 32 E through shared
+// memory with a group barrier per stage.  Pair direction: ascending iff (g & k) == 0.
+template <int E>
+__device__ __forceinline__ void merge_regs(uint64_t (&x)[E], int lane, int gw, int k, int jmax) {
+#pragma unroll
+    for (int j = 16 * E; j >= 1; j >>= 1) {
+        if (j > jmax) continue;
+        if (j >= 32) {
+            const int ej = j >> 5;
+#pragma unroll
+            for (int e = 0; e < E; e++)
+                if ((e & ej) == 0) {
+                    const bool up = ((gw + e * 32 + lane) & k) == 0;
+                    const uint64_t a = x[e], b = x[e | ej];
+                    if ((a > b) == up) {
+                        x[e] = b;
+                        x[e | ej] = a;
+                    }
+                }
+        } else {
+            const bool lower = (lane & j) == 0;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const bool up = ((gw + e * 32 + lane) & k) == 0;
+                const uint64_t a = x[e];
+                const uint64_t b = __shfl_xor_sync(0xffffffffu, a, j);
+                const bool take_min = lower == up;
+                x[e] = take_min ? (a < b ? a : b) : (a < b ? b : a);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Sort the bucket tmp[start, start + len) (len <= 32 E W) with a group of W warps (group-local
+// thread index gt_idx, named barrier bar_id; sk = 32 E W keys of shared memory) and write the
+// sorted values and full keys (hi | depth bits).
+template <int E, int W>
+__device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len,
+                                           uint64_t hi, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                                           uint64_t *sk, int gt_idx, int bar_id) {
+    constexpr int LP = 32 * E * W, NTH = 32 * W;
+    const int lane = gt_idx & 31;
+    const int gw = (gt_idx >> 5) * 32 * E;
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t g = gw + e * 32 + lane;
+        x[e] = g < len ? tmp[start + g] : ~0ull;
+    }
+    for (int k = 2; k <= 32 * E; k <<= 1) merge_regs<E>(x, lane, gw, k, k >> 1);
+    for (int k = 64 * E; k <= LP; k <<= 1) {
+#pragma unroll
+        for (int e = 0; e < E; e++) sk[gw + e * 32 + lane] = x[e];
+        group_bar(bar_id, NTH);
+        for (int j = k >> 1; j >= 32 * E; j >>= 1) {
+            for (int q = gt_idx; q < LP / 2; q += NTH) {
+                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+                const int p = i + j;
+                const uint64_t a = sk[i], c = sk[p];
+                if ((a > c) == ((i & k) == 0)) {
+                    sk[i] = c;
+                    sk[p] = a;
+                }
+            }
+            group_bar(bar_id, NTH);
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) x[e] = sk[gw + e * 32 + lane];
+        merge_regs<E>(x, lane, gw, k, 16 * E);
+        group_bar(bar_id, NTH);  // sk is rewritten by the next round
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t g = gw + e * 32 + lane;
+        if (g < len) {
+            vals[start + g] = (uint32_t)x[e];
+            keys[start + g] = hi | (x[e] >> 32);
+        }
+    }
+}
+
+constexpr int SG_WARPS = 2;   // warps per small-bucket group (<= 256 pairs)
+constexpr int SG_GROUPS = 4;  // groups (tiles) per CTA of the small-bucket sort
+constexpr int BG_WARPS = 16;  // warps of the long-bucket CTA (<= 4096 pairs)
+
+// Pass 1: one 2-warp group per (view, tile).  Writes the range; sorts buckets of <= 256 pairs;
+// queues longer buckets for pass 2.
+__global__ void __launch_bounds__(SG_GROUPS * SG_WARPS * 32) k_tile_sort_small(
+    const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, int VT, int64_t cap,
+    const uint64_t *__restrict__ tmp, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+    uint2 *__restrict__ ranges, uint32_t *__restrict__ big_tiles, WsHeader *hdr) {
+    __shared__ uint64_t sk[SG_GROUPS][256];
+    const int grp = threadIdx.x / (SG_WARPS * 32), gi = threadIdx.x % (SG_WARPS * 32);
+    const int gt = blockIdx.x * SG_GROUPS + grp;
+    if (gt >= VT) return;  // group-uniform; the groups never synchronise with each other
     const bool ok = (int64_t)hdr->P <= cap;
     const uint32_t start = ok ? tile_start[gt] : 0u;
     const uint32_t len = ok ? tile_count[(size_t)gt * CNT_STRIDE] : 0u;
     // empty tiles keep the (0, 0) range of the other binning path and of the oracle
-    if (threadIdx.x == 0) ranges[gt] = len ? make_uint2(start, start + len) : make_uint2(0u, 0u);
+    if (gi == 0) ranges[gt] = len ? make_uint2(start, start + len) : make_uint2(0u, 0u);
     if (len == 0) return;
     const uint64_t hi = (uint64_t)gt << 32;
-    if (len <= TS_SMEM_KEYS) {
-        int lp = 1;
-        while (lp < (int)len) lp <<= 1;
-        for (int i = threadIdx.x; i < lp; i += TS_THREADS) sk[i] = i < (int)len ? tmp[start + i] : ~0ull;
-        __syncthreads();
-        bitonic(sk, lp);
-        for (int i = threadIdx.x; i < (int)len; i += TS_THREADS) {
-            uint64_t k = sk[i];
-            vals[start + i] = (uint32_t)k;
-            keys[start + i] = hi | (k >> 32);
+    const int bar = 1 + grp;
+    if (len <= 64) group_sort<1, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
+    else if (len <= 128) group_sort<2, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
+    else if (len <= 256) group_sort<4, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
+    else if (gi == 0) big_tiles[atomicAdd(&hdr->n_big, 1u)] = (uint32_t)gt;
+}
+
+// Pass 2: one CTA per queued bucket (grid-stride).  Buckets beyond 4096 pairs use the plain
+// network in global memory.
+__global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t *__restrict__ tile_start,
+                                                                 const uint32_t *__restrict__ tile_count,
+                                                                 const uint64_t *__restrict__ tmp,
+                                                                 uint64_t *__restrict__ keys,
+                                                                 uint32_t *__restrict__ vals,
+                                                                 const uint32_t *__restrict__ big_tiles,
+                                                                 uint64_t *__restrict__ big, const WsHeader *hdr) {
+    __shared__ uint64_t sk[TS_SMEM_KEYS];
+    const uint32_t nb = hdr->n_big;
+    for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const uint32_t gt = big_tiles[b];
+        const uint32_t start = tile_start[gt];
+        const uint32_t len = tile_count[(size_t)gt * CNT_STRIDE];
+        const uint64_t hi = (uint64_t)gt << 32;
+        if (len <= 512) group_sort<1, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
+        else if (len <= 1024) group_sort<2, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
+        else if (len <= 2048) group_sort<4, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
+        else if (len <= 4096) group_sort<8, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
+        else {
+            // very long bucket: on a padded copy in this bucket's own region
+            // [2*start, 2*start + 2*len) of the overflow buffer (lp <= 2*len; disjoint per bucket)
+            int lp = 1;
+            while (lp < (int)len) lp <<= 1;
+            uint64_t *g = big + 2 * (size_t)start;
+            for (int i = threadIdx.x; i < lp; i += blockDim.x) g[i] = i < (int)len ? tmp[start + i] : ~0ull;
+            __threadfence_block();
+            __syncthreads();
+            bitonic(g, lp);
+            for (int i = threadIdx.x; i < (int)len; i += blockDim.x) {
+                vals[start + i] = (uint32_t)g[i];
+                keys[start + i] = hi | (g[i] >> 32);
+            }
         }
-    } else {
-        // long bucket: the same network in global memory, on a padded copy in this bucket's own
-        // region [2*start, 2*start + 2*len) of the overflow buffer (lp <= 2*len; disjoint per CTA)
-        int lp = 1;
-        while (lp < (int)len) lp <<= 1;
-        uint64_t *g = big + 2 * (size_t)start;
-        for (int i = threadIdx.x; i < lp; i += TS_THREADS) g[i] = i < (int)len ? tmp[start + i] : ~0ull;
-        __threadfence_block();
         __syncthreads();
-        bitonic(g, lp);
-        for (int i = threadIdx.x; i < (int)len; i += TS_THREADS) {
-            uint64_t k = g[i];
-            vals[start + i] = (uint32_t)k;
-            keys[start + i] = hi | (k >> 32);
-        }
     }
 }
 
@@ -158,10 +272,20 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
     ProfScope prof("k_tile_sort", s);
-    k_tile_sort<<<(unsigned)VT, TS_THREADS, 0, s>>>(at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count),
-                                                    L.cap, at<uint64_t>(ws, L.keys1), at<uint64_t>(ws, L.keys0),
-                                                    at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges),
-                                                    at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr));
+    k_tile_sort_small<<<(unsigned)((VT + SG_GROUPS - 1) / SG_GROUPS), SG_GROUPS * SG_WARPS * 32, 0, s>>>(
+        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), (int)VT, L.cap, at<uint64_t>(ws, L.keys1),
+        at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.big_tiles),
+        at<WsHeader>(ws, L.hdr));
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    k_tile_sort_big<<<(unsigned)std::min<int64_t>(VT, 2 * sms), BG_WARPS * 32, 0, s>>>(
+        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
+        at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
+        at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr));
     return cudaGetLastError();
 }
 

@@ -39,6 +39,7 @@ struct WsHeader {
     uint32_t P;            // total pairs of the last preprocess (may exceed capacity)
     uint32_t scan_ctr;     // dynamic CTA index of the scan
     uint32_t vis_count;    // Gaussians visible in at least one view (compacted list length)
+    uint32_t n_big;        // tiles whose list is too long for the one-warp sort (bin.cu)
     uint32_t hist_ctr;     // last-CTA detection of the sort histogram
     uint32_t sort_ctr[SORT_MAX_PASSES];
     int32_t sort_sel[SORT_MAX_PASSES + 1];  // source buffer of each pass (0 = primary)
@@ -61,7 +62,7 @@ struct Layout {
     int64_t scan_blocks, sort_blocks;
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
-    size_t tile_count, tile_start, tile_cursor, bin_big;  // bucket binning (bin.cu)
+    size_t tile_count, tile_start, tile_cursor, bin_big, big_tiles;  // bucket binning (bin.cu)
     size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
     int64_t max_chunks;  // chunked raster path (0 if unused)
     size_t chunk_base, chunk_tile, chunk_bwd;

@@ -383,7 +383,8 @@ def test_backward_accumulates_and_zero_upstream():
     r.backward(params, cams, G, grads)
     one = grads.clone()
     r.backward(params, cams, G, grads)
-    torch.testing.assert_close(grads, 2 * one, rtol=1e-5, atol=1e-7)
+    # the raster backward sums with fp32 atomics in no fixed order: allow reordering noise
+    torch.testing.assert_close(grads, 2 * one, rtol=1e-5, atol=1e-5 * one.abs().max().item())
 
 
 @pytest.mark.parametrize("cfg,n,D", [("tiny", None, 0), ("tum", 60000, 3)])
