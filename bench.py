@@ -177,13 +177,13 @@ CHUNK_MAX_TILES = 600  # views x tiles below this use the chunked raster path (g
 
 def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked: bool = False) -> int:
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
-    binning 0: bucket scatter, warp tile sort, CTA tile sort (3) / binning 1: duplicate, sort
-    histogram, one pass per 8-bit digit, fixup, ranges (4 + passes); pair gather + raster fwd (2),
-    + chunk index on levels with few tiles (chunked raster path); loss (2); fused: raster bwd +
-    preprocess bwd + Adam (3), else + gradient accumulate (4)."""
+    binning 0: bucket scatter, short- and long-bucket tile sorts with the pair-record gather (3) /
+    binning 1: duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, pair gather
+    (5 + passes); raster fwd (1), + chunk index on levels with few tiles (chunked raster path);
+    loss (2); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
-    binning_kernels = 3 if binning == 0 else 4 + passes
-    return 2 + binning_kernels + 2 + (1 if chunked else 0) + 2 + (3 if fused else 4)
+    binning_kernels = 3 if binning == 0 else 5 + passes
+    return 2 + binning_kernels + 1 + (1 if chunked else 0) + 2 + (3 if fused else 4)
 
 
 def run_ours(args):

@@ -249,8 +249,8 @@ gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int3
                             at<uint32_t>(ws, L.vals1), &hdr->P, L.cap, key_bits, hdr,
                             at<uint32_t>(ws, L.sort_look), L.sort_blocks, s);
         if (e == cudaSuccess) e = launch_ranges(L, ws, s);
+        if (e == cudaSuccess) e = launch_gather_pairs(L, ws, s);  // bucket sort gathers itself
     }
-    if (e == cudaSuccess) e = launch_gather_pairs(L, ws, s);
     if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s);
     if (e != cudaSuccess) return GS_ERR_CUDA;
     std::lock_guard<std::mutex> g(g_mu);

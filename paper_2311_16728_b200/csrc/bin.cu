@@ -13,7 +13,8 @@
 //      to 256 pairs are sorted by a group of two warps (k_tile_sort_small), longer ones are
 //      queued for k_tile_sort_big (a CTA of 16 warps, up to 4096 pairs; beyond that the same
 //      network in global memory -- correct, slower, only for extreme tile lists).  Keys live
-//      in registers; short exchange distances use shuffles, long ones shared memory.
+//      in registers; short exchange distances use shuffles, long ones shared memory.  The
+//      sorted pairs' 48-byte raster records are gathered in the same pass (raster.cu).
 // Compared with the global LSD sort this reads/writes each pair ~3 times instead of
 // 2 x (number of 8-bit digits) and replaces ~10 dependent launches per iteration by 4.
 #include <algorithm>
@@ -106,11 +107,12 @@ __device__ __forceinline__ void bitonic(uint64_t *a, int len) {
 // bitonic index) = w * 32 E + e * 32 + lane (striped, so loads and stores coalesce).  Distances
 // j < 32 are exchanged with shuffles, 32 <= j < 32 E inside the thread, j >= 32 E through shared
 // memory with a group barrier per stage.  Pair direction: ascending iff (g & k) == 0.
-template <int E>
-__device__ __forceinline__ void merge_regs(uint64_t (&x)[E], int lane, int gw, int k, int jmax) {
+// distances JMAX, JMAX / 2, ..., 1 of the merge step k (all static: no divergent-looking
+// branches around the shuffles)
+template <int E, int JMAX>
+__device__ __forceinline__ void merge_regs(uint64_t (&x)[E], int lane, int gw, int k) {
 #pragma unroll
-    for (int j = 16 * E; j >= 1; j >>= 1) {
-        if (j > jmax) continue;
+    for (int j = JMAX; j >= 1; j >>= 1) {
         if (j >= 32) {
             const int ej = j >> 5;
 #pragma unroll
@@ -118,10 +120,9 @@ __device__ __forceinline__ void merge_regs(uint64_t (&x)[E], int lane, int gw, i
                 if ((e & ej) == 0) {
                     const bool up = ((gw + e * 32 + lane) & k) == 0;
                     const uint64_t a = x[e], b = x[e | ej];
-                    if ((a > b) == up) {
-                        x[e] = b;
-                        x[e | ej] = a;
-                    }
+                    const bool sw = (a > b) == up;
+                    x[e] = sw ? b : a;
+                    x[e | ej] = sw ? a : b;
                 }
         } else {
             const bool lower = (lane & j) == 0;
@@ -137,6 +138,13 @@ __device__ __forceinline__ void merge_regs(uint64_t (&x)[E], int lane, int gw, i
     }
 }
 
+// merge steps k = K, 2K, ..., 32 E (each entirely in registers)
+template <int E, int K>
+__device__ __forceinline__ void sort_regs(uint64_t (&x)[E], int lane, int gw) {
+    merge_regs<E, K / 2>(x, lane, gw, K);
+    if constexpr (K < 32 * E) sort_regs<E, 2 * K>(x, lane, gw);
+}
+
 __device__ __forceinline__ void group_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -144,10 +152,16 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 // Sort the bucket tmp[start, start + len) (len <= 32 E W) with a group of W warps (group-local
 // thread index gt_idx, named barrier bar_id; sk = 32 E W keys of shared memory) and write the
 // sorted values and full keys (hi | depth bits).
+struct RecSrc {  // per-(view, Gaussian) record sources for the fused pair-record gather
+    const float4 *rec0, *rec1, *rec2;
+    float4 *prec;
+    int64_t vbase;  // view * n of the bucket's view
+};
+
 template <int E, int W>
 __device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len,
                                            uint64_t hi, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
-                                           uint64_t *sk, int gt_idx, int bar_id) {
+                                           uint64_t *sk, int gt_idx, int bar_id, const RecSrc &rs) {
     constexpr int LP = 32 * E * W, NTH = 32 * W;
     const int lane = gt_idx & 31;
     const int gw = (gt_idx >> 5) * 32 * E;
@@ -157,7 +171,7 @@ __device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uin
         const uint32_t g = gw + e * 32 + lane;
         x[e] = g < len ? tmp[start + g] : ~0ull;
     }
-    for (int k = 2; k <= 32 * E; k <<= 1) merge_regs<E>(x, lane, gw, k, k >> 1);
+    sort_regs<E, 2>(x, lane, gw);
     for (int k = 64 * E; k <= LP; k <<= 1) {
 #pragma unroll
         for (int e = 0; e < E; e++) sk[gw + e * 32 + lane] = x[e];
@@ -176,45 +190,45 @@ __device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uin
         }
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = sk[gw + e * 32 + lane];
-        merge_regs<E>(x, lane, gw, k, 16 * E);
+        merge_regs<E, 16 * E>(x, lane, gw, k);
         group_bar(bar_id, NTH);  // sk is rewritten by the next round
     }
 #pragma unroll
     for (int e = 0; e < E; e++) {
         const uint32_t g = gw + e * 32 + lane;
         if (g < len) {
-            vals[start + g] = (uint32_t)x[e];
+            const uint32_t gi = (uint32_t)x[e];
+            vals[start + g] = gi;
             keys[start + g] = hi | (x[e] >> 32);
+            write_pair_record(rs.prec, start + g, rs.rec0, rs.rec1, rs.rec2, rs.vbase + gi, gi);
         }
     }
 }
 
-constexpr int SG_WARPS = 2;   // warps per small-bucket group (<= 256 pairs)
-constexpr int SG_GROUPS = 4;  // groups (tiles) per CTA of the small-bucket sort
+constexpr int SG_WARPS = 2;   // warps of the small-bucket CTA (<= 256 pairs)
 constexpr int BG_WARPS = 16;  // warps of the long-bucket CTA (<= 4096 pairs)
 
-// Pass 1: one 2-warp group per (view, tile).  Writes the range; sorts buckets of <= 256 pairs;
-// queues longer buckets for pass 2.
-__global__ void __launch_bounds__(SG_GROUPS * SG_WARPS * 32) k_tile_sort_small(
-    const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, int VT, int64_t cap,
+// Pass 1: one 2-warp CTA per (view, tile) (tile = blockIdx.x, so every branch below is provably
+// uniform and the shuffles need no warp re-convergence).  Writes the range; sorts buckets of
+// <= 256 pairs; queues longer buckets for pass 2.
+__global__ void __launch_bounds__(SG_WARPS * 32) k_tile_sort_small(
+    const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, int64_t cap,
     const uint64_t *__restrict__ tmp, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
-    uint2 *__restrict__ ranges, uint32_t *__restrict__ big_tiles, WsHeader *hdr) {
-    __shared__ uint64_t sk[SG_GROUPS][256];
-    const int grp = threadIdx.x / (SG_WARPS * 32), gi = threadIdx.x % (SG_WARPS * 32);
-    const int gt = blockIdx.x * SG_GROUPS + grp;
-    if (gt >= VT) return;  // group-uniform; the groups never synchronise with each other
+    uint2 *__restrict__ ranges, uint32_t *__restrict__ big_tiles, WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
+    __shared__ uint64_t sk[256];
+    const int gt = blockIdx.x;
+    rs.vbase = (int64_t)(gt / tiles) * n;
     const bool ok = (int64_t)hdr->P <= cap;
     const uint32_t start = ok ? tile_start[gt] : 0u;
     const uint32_t len = ok ? tile_count[(size_t)gt * CNT_STRIDE] : 0u;
     // empty tiles keep the (0, 0) range of the other binning path and of the oracle
-    if (gi == 0) ranges[gt] = len ? make_uint2(start, start + len) : make_uint2(0u, 0u);
-    if (len == 0) return;
+    if (threadIdx.x == 0) ranges[gt] = len ? make_uint2(start, start + len) : make_uint2(0u, 0u);
     const uint64_t hi = (uint64_t)gt << 32;
-    const int bar = 1 + grp;
-    if (len <= 64) group_sort<1, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
-    else if (len <= 128) group_sort<2, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
-    else if (len <= 256) group_sort<4, SG_WARPS>(tmp, start, len, hi, keys, vals, sk[grp], gi, bar);
-    else if (gi == 0) big_tiles[atomicAdd(&hdr->n_big, 1u)] = (uint32_t)gt;
+    if (len == 0) return;
+    if (len <= 64) group_sort<1, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+    else if (len <= 128) group_sort<2, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+    else if (len <= 256) group_sort<4, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+    else if (threadIdx.x == 0) big_tiles[atomicAdd(&hdr->n_big, 1u)] = (uint32_t)gt;
 }
 
 // Pass 2: one CTA per queued bucket (grid-stride).  Buckets beyond 4096 pairs use the plain
@@ -225,7 +239,8 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t 
                                                                  uint64_t *__restrict__ keys,
                                                                  uint32_t *__restrict__ vals,
                                                                  const uint32_t *__restrict__ big_tiles,
-                                                                 uint64_t *__restrict__ big, const WsHeader *hdr) {
+                                                                 uint64_t *__restrict__ big, const WsHeader *hdr,
+                                                                 RecSrc rs, int64_t n, int tiles) {
     __shared__ uint64_t sk[TS_SMEM_KEYS];
     const uint32_t nb = hdr->n_big;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -233,10 +248,11 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t 
         const uint32_t start = tile_start[gt];
         const uint32_t len = tile_count[(size_t)gt * CNT_STRIDE];
         const uint64_t hi = (uint64_t)gt << 32;
-        if (len <= 512) group_sort<1, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
-        else if (len <= 1024) group_sort<2, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
-        else if (len <= 2048) group_sort<4, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
-        else if (len <= 4096) group_sort<8, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1);
+        rs.vbase = (int64_t)(gt / tiles) * n;
+        if (len <= 512) group_sort<1, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= 1024) group_sort<2, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= 2048) group_sort<4, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= 4096) group_sort<8, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
         else {
             // very long bucket: on a padded copy in this bucket's own region
             // [2*start, 2*start + 2*len) of the overflow buffer (lp <= 2*len; disjoint per bucket)
@@ -248,8 +264,10 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t 
             __syncthreads();
             bitonic(g, lp);
             for (int i = threadIdx.x; i < (int)len; i += blockDim.x) {
-                vals[start + i] = (uint32_t)g[i];
+                const uint32_t gi = (uint32_t)g[i];
+                vals[start + i] = gi;
                 keys[start + i] = hi | (g[i] >> 32);
+                write_pair_record(rs.prec, start + i, rs.rec0, rs.rec1, rs.rec2, rs.vbase + gi, gi);
             }
         }
         __syncthreads();
@@ -272,10 +290,11 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
     ProfScope prof("k_tile_sort", s);
-    k_tile_sort_small<<<(unsigned)((VT + SG_GROUPS - 1) / SG_GROUPS), SG_GROUPS * SG_WARPS * 32, 0, s>>>(
-        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), (int)VT, L.cap, at<uint64_t>(ws, L.keys1),
+    const RecSrc rs{at<float4>(ws, L.rec0), at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), at<float4>(ws, L.prec), 0};
+    k_tile_sort_small<<<(unsigned)VT, SG_WARPS * 32, 0, s>>>(
+        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), L.cap, at<uint64_t>(ws, L.keys1),
         at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.big_tiles),
-        at<WsHeader>(ws, L.hdr));
+        at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
@@ -285,7 +304,7 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
     k_tile_sort_big<<<(unsigned)std::min<int64_t>(VT, 2 * sms), BG_WARPS * 32, 0, s>>>(
         at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
         at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
-        at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr));
+        at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
     return cudaGetLastError();
 }
 
