@@ -138,8 +138,9 @@ gs_status gs_render_backward(const gs_params *params, const gs_camera *cams, int
    backward of gs_render_backward (same definition) followed by the Adam / SGD step of
    gs_adam_step over ALL Gaussians (Gaussians invisible in every view get g = 0, as in the
    dense step, R20), in place on params, m, v.  Equivalent to gs_render_backward into a zeroed
-   gradient buffer followed by gs_adam_step(..., 0, n, ...) -- bitwise -- but never writes or
-   reads the N x K gradient array (DESIGN.md, K9/K11 fusion).  Single-GPU path: with data
+   gradient buffer followed by gs_adam_step(..., 0, n, ...) -- up to the summation order of the
+   raster backward's fp32 atomics -- but never writes or reads the N x K gradient array
+   (DESIGN.md, fused backward + Adam).  Single-GPU path: with data
    parallelism the gradient must be all-reduced, use the two separate calls.  After this call
    the forward state of ws is stale (the parameters changed).
    step > 0: the 1-based step number.  step == 0: device-resident step counter (for CUDA-graph

@@ -346,151 +346,6 @@ __device__ __forceinline__ float warp_sum8_transposed(float a[8], int lane) {
     return r;
 }
 
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_raster_bwd(const uint2 *__restrict__ ranges,
-                                                           const float4 *__restrict__ prec, int64_t n, int W, int H,
-                                                           int TX, int tiles, float bg0, float bg1, float bg2,
-                                                           const float *__restrict__ dL_drgb,
-                                                           const float *__restrict__ T_keep,
-                                                           const uint32_t *__restrict__ ncontrib,
-                                                           float4 *__restrict__ g2d) {
-    __shared__ __align__(128) RasterSmem S;
-    __shared__ uint8_t wl[WARPS][BATCH];
-    __shared__ uint32_t s_maxlast;
-    const int view = blockIdx.z;
-    int tile_x, bx0, by0, lx, ly;
-    warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
-    const int tile = blockIdx.y * TX + tile_x;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int px = tile_x * TILE + lx;
-    const int py = blockIdx.y * TILE + ly;
-    const float wx0 = (float)(tile_x * TILE + bx0);
-    const float wy0 = (float)(blockIdx.y * TILE + by0);
-    const bool inside = px < W && py < H;
-    const uint2 range = ranges[(int64_t)view * tiles + tile];
-    const float fx = (float)px, fy = (float)py;
-    const int64_t vbase = (int64_t)view * n;
-    const int64_t HW = (int64_t)H * W;
-    const int64_t pix = (int64_t)py * W + px;
-    float T = 1.f, g_0 = 0.f, g_1 = 0.f, g_2 = 0.f;
-    uint32_t last = 0;
-    if (inside) {
-        T = T_keep[(int64_t)view * HW + pix];
-        last = ncontrib[(int64_t)view * HW + pix];
-        const float *g = dL_drgb + (int64_t)view * 3 * HW + pix;
-        g_0 = g[0];
-        g_1 = g[HW];
-        g_2 = g[2 * HW];
-    }
-    if (tid == 0) {
-        s_maxlast = 0;
-        mbar_init(&S.bar[0]);
-        mbar_init(&S.bar[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // the warp's own furthest composited position bounds its work; the CTA's bounds the batches
-    uint32_t wlast = last;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
-    if (lane == 0) atomicMax(&s_maxlast, wlast);
-    __syncthreads();
-    const int todo_all = (int)s_maxlast;
-    const float4 *src = prec + 3 * (size_t)range.x;
-    // batches cover list positions [b_end - cnt, b_end), walked from the back
-    if (tid == 0 && todo_all > 0) {
-        int cnt0 = min(BATCH, todo_all);
-        bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
-    }
-    uint32_t phases = 0u;  // bit b = parity to wait for on buffer b
-    float acc0 = bg0, acc1 = bg1, acc2 = bg2;
-    const int warp = tid >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
-        const int buf = it & 1;
-        const int cnt = min(BATCH, b_end);
-        const int b_start = b_end - cnt;
-        __syncthreads();  // everyone is done with the other buffer
-        if (tid == 0 && b_start > 0) {
-            int cn = min(BATCH, b_start);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
-        }
-        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
-        phases ^= 1u << buf;
-        const float4 *r = S.rec[buf];
-        // phase 1: ordered (back to front) list of the batch entries this warp must replay --
-        // at or before its furthest composited position and able to reach its block
-        int nsel = 0;
-        for (int k = 0; k < cnt; k += 32) {
-            const int jj = k + lane;
-            const int idx = cnt - 1 - jj;  // batch slot; list position b_start + idx + 1
-            bool hit = jj < cnt && (uint32_t)(b_start + idx + 1) <= wlast &&
-                       !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, wx0, wy0);
-            unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
-            nsel += __popc(b);
-        }
-        __syncwarp();
-        for (int t = 0; t < nsel; t++) {
-            const int j = wl[warp][t];
-            const uint32_t position = (uint32_t)(b_start + j + 1);  // 1-based position in the tile list
-            float4 g0 = r[3 * j];
-            float4 g1 = r[3 * j + 1];
-            float dLdu = 0.f, dLdv = 0.f, dLdA = 0.f, dLdB = 0.f, dLdC = 0.f, dLdsig = 0.f;
-            float dLdr = 0.f, dLdg = 0.f, dLdb = 0.f;
-            bool contrib = false;
-            if (position <= last) {
-                float dx, dy;
-                float power = pixel_power(fx, fy, g0, g1.x, dx, dy);
-                if (!(power > 0.0f || power < POWER_CUT)) {
-                    float e = fast_exp(power);
-                    float a_raw = g1.y * e;
-                    float alpha = fminf(ALPHA_MAX, a_raw);
-                    if (alpha >= ALPHA_MIN) {
-                        contrib = true;
-                        T = __fdividef(T, 1.0f - alpha);  // transmittance before this Gaussian
-                        float w = alpha * T;
-                        dLdr = g_0 * w;
-                        dLdg = g_1 * w;
-                        dLdb = g_2 * w;
-                        const float d0 = g1.z - acc0, d1 = g1.w - acc1, d2 = r[3 * j + 2].x - acc2;
-                        float dLda = T * (g_0 * d0 + g_1 * d1 + g_2 * d2);
-                        acc0 += alpha * d0;  // acc <- alpha c + (1 - alpha) acc
-                        acc1 += alpha * d1;
-                        acc2 += alpha * d2;
-                        if (!(a_raw > ALPHA_MAX)) {
-                            dLdsig = e * dLda;
-                            // moments a = dL/dpower dx, b = dL/dpower dy, a dx, a dy, b dy; the
-                            // projection backward turns their sums into dL/du = A S(a) + B S(b),
-                            // dL/dv = B S(a) + C S(b), dL/dA = -S(a dx)/2, dL/dB = -S(a dy),
-                            // dL/dC = -S(b dy)/2 (the conic is constant per Gaussian and view)
-                            const float dLdp = alpha * dLda;
-                            dLdu = dLdp * dx;
-                            dLdv = dLdp * dy;
-                            dLdA = dLdu * dx;
-                            dLdB = dLdu * dy;
-                            dLdC = dLdv * dy;
-                        }
-                    }
-                }
-            }
-            if (__any_sync(0xffffffffu, contrib)) {
-                // per-(view, Gaussian) record: [S(a), S(b), S(a dx), S(a dy) | S(b dy), sigma, r, g | b, -]
-                float vals8[8] = {dLdu, dLdv, dLdA, dLdB, dLdC, dLdsig, dLdr, dLdg};
-                float mine = warp_sum8_transposed(vals8, lane);
-                float bsum = warp_sum(dLdb);
-                const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
-                float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
-                if ((lane & 3) == 0)
-                    atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
-                if (lane == 1) atomicAdd(dst + 8, bsum);
-            }
-        }
-    }
-    // every issued copy was waited for inside the loop (the last batch issues none)
-}
-
 // ================================================================ chunked backward (few tiles)
 // At pyramid levels with few tiles (V * tiles < CHUNK_MAX_TILES) each warp of the tile-serial
 // backward would walk a long list alone.  The forward (same kernel, CHUNKED instance) records,
@@ -826,14 +681,6 @@ static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_
                                      at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd);
 }
 
-template <int WARPS>
-static void bwd_launch(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
-    dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
-    k_raster_bwd<WARPS><<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H,
-                                                    L.TX, L.tiles, bg[0], bg[1], bg[2], dL_drgb,
-                                                    at<float>(ws, L.Tfinal), at<uint32_t>(ws, L.ncontrib),
-                                                    at<float4>(ws, L.grad2d));
-}
 
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                               cudaStream_t s) {
@@ -863,18 +710,11 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
         return cudaGetLastError();
     }
-    if (raster_warps(L) == 8) {  // many tiles: two pixels per lane, packed fp32x2
-        dim3 grid(L.TX, L.TY, L.V);
-        k_raster_bwd2<<<grid, 128, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
-                                           L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
-                                           at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
-        return cudaGetLastError();
-    }
-    switch (raster_warps(L)) {
-        case 8: bwd_launch<8>(L, ws, bg, dL_drgb, s); break;
-        case 2: bwd_launch<2>(L, ws, bg, dL_drgb, s); break;
-        default: bwd_launch<1>(L, ws, bg, dL_drgb, s); break;
-    }
+    // many tiles: two pixels per lane, packed fp32x2
+    dim3 grid(L.TX, L.TY, L.V);
+    k_raster_bwd2<<<grid, 128, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
+                                       L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
+                                       at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
     return cudaGetLastError();
 }
 
