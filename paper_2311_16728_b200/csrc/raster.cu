@@ -69,14 +69,21 @@ __device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, f
     const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + h - g0.y;
     if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return false;
     float best = 3.4e38f;
-    // edges x = X: f = A X^2 + 2 B X y + C y^2, y* = -B X / C clamped to [ay, by]
+    // edges x = X: f = A X^2 + 2 B X y + C y^2, y* = -B X / C clamped to [ay, by].  The
+    // minimiser may be approximate (SFU reciprocals): f is evaluated exactly at a feasible
+    // point, and a point off the true minimiser by a relative 1e-7 raises f by O(1e-14),
+    // far inside the padding
+    float rC, rA;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rC) : "f"(C));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rA) : "f"(A));
+    const float nBC = -B * rC, nBA = -B * rA;
 #pragma unroll
     for (int e = 0; e < 2; e++) {
         float X = e ? bx : ax;
-        float y = fminf(fmaxf(-B * X / C, ay), by);
+        float y = fminf(fmaxf(nBC * X, ay), by);
         best = fminf(best, A * X * X + 2.f * B * X * y + C * y * y);
         float Y = e ? by : ay;
-        float x = fminf(fmaxf(-B * Y / A, ax), bx);
+        float x = fminf(fmaxf(nBA * Y, ax), bx);
         best = fminf(best, A * x * x + 2.f * B * x * Y + C * Y * Y);
     }
     return best > qlim * 1.001f + 1e-3f;
