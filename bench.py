@@ -32,10 +32,14 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "mapping iters/sec (fwd+bwd) and render FPS at 1/2/4/8 B200; % HBM roofline"
-# FP32 operations of the raster backward per composited (pixel, Gaussian) pair (K8):
-# power 9, exp 2, alpha 2, T recovery 2, colour grads 3, dL/dalpha 10, acc update 9,
-# dL/dsigma 1, dL/dpower 1, mean2d grads 10, conic grads 9 -> 58
-BWD_FLOP_PER_PAIR = 58
+# FP32 operations of the raster backward (A8; SURVEY §8(d)'s ALU model counts per
+# evaluated (pixel, Gaussian) pair).  Every list entry up to the pixel's last contributor is
+# evaluated: power 9, exp 2, alpha 2 -> 13.  A composited entry adds T recovery 2, colour grads
+# 3, dL/dalpha 10, acc update 9, dL/dsigma 1, dL/dpower 1, mean2d moments 10, conic moments 9
+# -> 45 (58 in total).
+BWD_FLOP_PER_EVAL = 13
+BWD_FLOP_PER_COMP = 45
+BWD_FLOP_PER_PAIR = BWD_FLOP_PER_EVAL + BWD_FLOP_PER_COMP
 
 
 def dist_env():
@@ -226,7 +230,7 @@ def run_ours(args):
     iters_per_step = cfg["levels"] + 1
 
     def step():
-        eng.build_pyramids()
+        eng.build_pyramids(overlap=True)
         return eng.step()
 
     for _ in range(max(args.warmup, 3)):
@@ -273,13 +277,18 @@ def run_ours(args):
                 stage[name] += e[k].elapsed_time(e[k + 1])
     stage = {k: v / reps for k, v in stage.items()}
 
-    # ---- algorithmic work of the raster kernels: composited (pixel, Gaussian) pairs per level
-    comp_pairs = []
+    # ---- algorithmic work of the raster kernels per level: composited (pixel, Gaussian) pairs
+    # and evaluated pairs (list entries up to each pixel's last contributor, which the
+    # back-to-front replay visits)
+    comp_pairs, eval_pairs = [], []
     for level in range(cfg["levels"], -1, -1):
         eng.render(level)
         torch.cuda.synchronize()
-        comp_pairs.append(int(eng.renderers[level].ws.views()["n_composited"].sum().item()))
+        v = eng.renderers[level].ws.views()
+        comp_pairs.append(int(v["n_composited"].sum().item()))
+        eval_pairs.append(int(v["n_contrib"].to(torch.int64).sum().item()))
     pairs_per_step = sum(comp_pairs)
+    flops_per_step = BWD_FLOP_PER_EVAL * sum(eval_pairs) + BWD_FLOP_PER_COMP * pairs_per_step
 
     # ---- live kernel timing (eager launches): the dominant kernels are bracketed with CUDA
     # events recorded by libgs.so on their launching stream (gs_profile_kernel)
@@ -365,7 +374,7 @@ def run_ours(args):
     e2e_ms = float(e2e_ms.item())
 
     # ---- rooflines.  Dominant kernel: the raster backward (A8), FP32-ALU bound: algorithmic
-    # FLOPs = composited pairs x BWD_FLOP_PER_PAIR against 148 SMs x 128 FP32
+    # FLOPs = evaluated pairs x 13 + composited pairs x 45 against 148 SMs x 128 FP32
     # lanes x 2 x the SM clock sampled during the run.  Second: the fused Adam (A11), HBM bound.
     K = 11 + 3 * (D + 1) ** 2
     ld = eng.params.shape[1]
@@ -374,7 +383,7 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
     bwd_ms, bwd_launches, _ = live["k_raster_bwd"]
-    bwd_flops = pairs_per_step * BWD_FLOP_PER_PAIR * args.steps
+    bwd_flops = flops_per_step * args.steps
     bwd_achieved = bwd_flops / (bwd_ms * 1e-3) / 1e12
     akern = "k_adam_fused" if world == 1 else "k_adam"
     adam_ms, adam_launches, _ = live[akern]
@@ -419,8 +428,10 @@ def run_ours(args):
                          "peak": fp32_peak, "unit": "TFLOP/s", "frac": bwd_achieved / fp32_peak,
                          "traffic": (traffic or {}).get("k_raster_bwd"),
                          "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sampled)",
-                         "algorithmic_flops_per_launch": pairs_per_step * BWD_FLOP_PER_PAIR / len(comp_pairs),
-                         "flop_per_composited_pair": BWD_FLOP_PER_PAIR, "composited_pairs_per_level": comp_pairs,
+                         "algorithmic_flops_per_launch": flops_per_step / len(comp_pairs),
+                         "flop_per_evaluated_pair": BWD_FLOP_PER_EVAL,
+                         "flop_per_composited_pair_extra": BWD_FLOP_PER_COMP,
+                         "evaluated_pairs_per_level": eval_pairs, "composited_pairs_per_level": comp_pairs,
                          "avg_launch_ms": bwd_ms / max(bwd_launches, 1),
                          "share_of_step": bwd_ms / live["k_raster_bwd"][2],
                          "timing": "CUDA events around each launch, eager pass of K steps"},

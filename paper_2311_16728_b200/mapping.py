@@ -73,9 +73,28 @@ class MappingEngine:
         self.gt0.copy_(g.to(self.device, non_blocking=True).view_as(self.gt0))
         self.build_pyramids()
 
-    def build_pyramids(self):
-        """A0: GP^l(I_gt), l = 1..n, once per keyframe."""
-        self.pyr = gaussian_pyramid(self.gt0, self.n_levels)
+    def build_pyramids(self, overlap: bool = False):
+        """A0: GP^l(I_gt), l = 1..n, once per keyframe.  overlap: build them on a
+        side stream; the first loss that needs them waits for it (iteration), so the pyramid
+        runs concurrently with the first level's projection, binning and rendering."""
+        if not overlap or not self.device.startswith("cuda"):
+            self.pyr = gaussian_pyramid(self.gt0, self.n_levels)
+            self._pyr_pending = False
+            return
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.gt0.device)
+            self._pyr_event = torch.cuda.Event()
+        self._side.wait_stream(torch.cuda.current_stream())  # after the targets' copy
+        with torch.cuda.stream(self._side):
+            self.pyr = gaussian_pyramid(self.gt0, self.n_levels)
+            self._pyr_event.record()
+        self._pyr_pending = True
+
+    def _pyramid(self, level: int):
+        if getattr(self, "_pyr_pending", False):
+            torch.cuda.current_stream().wait_event(self._pyr_event)
+            self._pyr_pending = False
+        return self.pyr[level]
 
     # ------------------------------------------------------------------ capacity
     def calibrate(self, min_capacity: int = 1 << 16):
@@ -112,7 +131,7 @@ class MappingEngine:
         r = self.renderers[level]
         cams = self.cams[level]
         rgb, _ = r.forward(self.params, cams, self.bg)                       # A1-A6
-        loss, dL = self.losses[level](rgb, self.pyr[level])                  # A7
+        loss, dL = self.losses[level](rgb, self._pyramid(level))             # A7
         if fused is None:
             fused = not self.distributed()
         if fused:
@@ -144,7 +163,7 @@ class MappingEngine:
             if host:
                 self.step_host(gts_pinned, out_pinned)
             else:
-                self.build_pyramids()
+                self.build_pyramids(overlap=True)
                 self.graph_losses = torch.stack(self.step())
 
         with torch.cuda.stream(side):  # warm-up run on the capture stream (also a real step)
@@ -164,7 +183,7 @@ class MappingEngine:
         """End-to-end public API: new keyframe targets from pinned host memory (H2D), A0,
         the Eq. 5 pass, per-level losses back to pinned host memory (D2H)."""
         self.gt0.copy_(gts_pinned, non_blocking=True)
-        self.build_pyramids()
+        self.build_pyramids(overlap=True)
         losses = self.step()
         out_pinned.copy_(torch.stack(losses), non_blocking=True)
         return out_pinned
