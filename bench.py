@@ -265,9 +265,17 @@ def run_ours(args):
             if eng.distributed():
                 e[3].record(); r.backward(eng.params, c, dL, eng.grads, eng.grad2d_norm, eng.bg)
                 e[4].record()
-                from paper_2311_16728_b200.mapping import reduce_gradients
-                reduce_gradients(eng.grads)
-                e[5].record(); eng.adam.step(eng.grads, zero_grads=True)
+                from paper_2311_16728_b200.mapping import all_gather_rows, reduce_gradients, reduce_scatter_rows
+                if eng.sharded is not None:  # reduce-scatter | row-sharded Adam + all-gather
+                    sh = eng.sharded
+                    reduce_scatter_rows(sh.padded_grads, sh.R)
+                    e[5].record()
+                    sh.t += 1
+                    sh._adam_rows()
+                    all_gather_rows(sh.padded_params, sh.R)
+                else:
+                    reduce_gradients(eng.grads)
+                    e[5].record(); eng.adam.step(eng.grads, zero_grads=True)
                 e[6].record()
             else:  # fused backward + Adam (single GPU)
                 e[3].record(); r.backward_adam(eng.params, c, dL, eng.adam, eng.grad2d_norm, eng.bg)
@@ -387,7 +395,12 @@ def run_ours(args):
     bwd_achieved = bwd_flops / (bwd_ms * 1e-3) / 1e12
     akern = "k_adam_fused" if world == 1 else "k_adam"
     adam_ms, adam_launches, _ = live[akern]
-    adam_bytes = (K * n * 24 + 4 * n) if world == 1 else K * ld * 32
+    if world == 1:
+        adam_bytes = K * n * 24 + 4 * n
+    elif eng.sharded is not None:  # this rank's rows only
+        adam_bytes = (eng.sharded.r1 - eng.sharded.r0) * ld * 32
+    else:
+        adam_bytes = K * ld * 32
     peak, peak_src = load_peaks()
     adam_achieved = adam_bytes * adam_launches / (adam_ms * 1e-3) / 1e9
     traffic = None

@@ -164,6 +164,16 @@ gs_status gs_pyramid(const float *img, int32_t n_images, int32_t C, int32_t H, i
 gs_status gs_adam_step(gs_params *params, float *grads, float *m, float *v, const gs_adam_hparams *hp,
                        int64_t step, int64_t g_begin, int64_t g_end, int32_t zero_grads, gs_stream_t stream);
 
+/* A11 on a parameter-row shard (reduce-scatter -> sharded Adam -> all-gather):
+   the step of gs_adam_step over all n Gaussians of parameter rows [row_begin, row_end) of the
+   [K][ld] layout (K = gs_param_rows; each row's class decides its learning rate).  params and
+   grads are the full layout; m_rows, v_rows hold only the shard's moments, row r at
+   (r - row_begin) * ld (a rank keeps 1/G of the optimiser state).  Same arithmetic as
+   gs_adam_step, element for element.  GS_ERR_INVALID_ARG for a range outside [0, K]. */
+gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, float *v_rows, const gs_adam_hparams *hp,
+                            int64_t step, int32_t row_begin, int32_t row_end, int32_t zero_grads,
+                            gs_stream_t stream);
+
 /* Synchronises stream, then reads the workspace status: *flags (host) bit 0 = pair capacity
    overflow; *pairs (host, may be NULL) = pair count of the last gs_preprocess.  Returns
    GS_ERR_CAPACITY if bit 0 is set. */

@@ -25,7 +25,7 @@ GS_TILE = 16
 # every symbol declared in include/gs.h
 EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess", "gs_render_forward",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
-           "gs_pyramid", "gs_adam_step",
+           "gs_pyramid", "gs_adam_step", "gs_adam_step_rows",
            "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
@@ -217,6 +217,13 @@ def gs_adam_step(params: GsParams, grads, m, v, hp: GsAdamHparams, step: int, g_
     _check(lib().gs_adam_step(C.byref(params), _ptr(grads), _ptr(m), _ptr(v), C.byref(hp), C.c_int64(step),
                               C.c_int64(g_begin), C.c_int64(g_end), C.c_int32(int(zero_grads)), _stream(stream)),
            "gs_adam_step")
+
+
+def gs_adam_step_rows(params: GsParams, grads, m_rows, v_rows, hp: GsAdamHparams, step: int, row_begin: int,
+                      row_end: int, zero_grads: bool, stream=None):
+    _check(lib().gs_adam_step_rows(C.byref(params), _ptr(grads), _ptr(m_rows), _ptr(v_rows), C.byref(hp),
+                                   C.c_int64(step), C.c_int32(row_begin), C.c_int32(row_end),
+                                   C.c_int32(int(zero_grads)), _stream(stream)), "gs_adam_step_rows")
 
 
 def gs_query_status(ws: torch.Tensor, stream=None):

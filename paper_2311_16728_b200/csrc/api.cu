@@ -342,6 +342,19 @@ gs_status gs_adam_step(gs_params *params, float *grads, float *m, float *v, cons
     return cuda_status(launch_adam(*params, grads, m, v, *hp, step, g_begin, g_end, zero_grads, (cudaStream_t)stream));
 }
 
+gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, float *v_rows, const gs_adam_hparams *hp,
+                            int64_t step, int32_t row_begin, int32_t row_end, int32_t zero_grads,
+                            gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    const int32_t K = gs_param_rows(params->sh_degree);
+    if (!grads || !hp || step < 1 || row_begin < 0 || row_end > K || row_begin > row_end) return GS_ERR_INVALID_ARG;
+    if (!hp->sgd_mode && (!m_rows || !v_rows)) return GS_ERR_INVALID_ARG;
+    if (row_begin == row_end || params->n == 0) return GS_OK;
+    return cuda_status(launch_adam(*params, grads, m_rows, v_rows, *hp, step, 0, params->n, zero_grads,
+                                   (cudaStream_t)stream, row_begin, row_end));
+}
+
 gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs) {
     if (!ws || !flags || ws_bytes < sizeof(WsHeader)) return GS_ERR_INVALID_ARG;
     WsHeader h;

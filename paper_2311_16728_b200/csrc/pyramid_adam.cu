@@ -110,12 +110,13 @@ __device__ __forceinline__ void adam1(float &p, float &g, float &m, float &v, fl
 constexpr int ADAM_THREADS = 256;
 constexpr int ADAM_UNROLL = 2;
 
-// grid (ceil(ld/4 / (256*2)), rows): the parameter class (learning rate) is uniform per CTA row
+// grid (ceil(ld/4 / (256*2)), rows): the parameter class (learning rate) is uniform per CTA row;
+// P, G, Mm, Vv point at the first row of the range, row0 is its parameter row (class lookup)
 __global__ void __launch_bounds__(ADAM_THREADS) k_adam(float *__restrict__ P, float *__restrict__ G,
                                                        float *__restrict__ Mm, float *__restrict__ Vv, int64_t ld,
-                                                       int64_t g0, int64_t g1, AdamArgs a) {
+                                                       int64_t g0, int64_t g1, int row0, AdamArgs a) {
     const int row = blockIdx.y;
-    const float lr = a.lr[row_class(row)];
+    const float lr = a.lr[row_class(row0 + row)];
     const int64_t per_row = ld / 4;
     const int64_t rbase = (int64_t)row * per_row;
     float4 *P4 = reinterpret_cast<float4 *>(P) + rbase, *G4 = reinterpret_cast<float4 *>(G) + rbase;
@@ -270,13 +271,15 @@ cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, flo
 }
 
 cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
-                        int64_t g0, int64_t g1, int zero, cudaStream_t s) {
+                        int64_t g0, int64_t g1, int zero, cudaStream_t s, int row_begin, int row_end) {
     AdamArgs a = adam_args(hp, step, zero);
-    int rows = gs_param_rows(p.sh_degree);
+    if (row_end < 0) row_end = gs_param_rows(p.sh_degree);
+    const int rows = row_end - row_begin;
     int64_t per_row = p.ld / 4;
     dim3 grid((unsigned)((per_row + ADAM_THREADS * ADAM_UNROLL - 1) / (ADAM_THREADS * ADAM_UNROLL)), rows);
     ProfScope prof("k_adam", s);
-    if (per_row > 0) k_adam<<<grid, ADAM_THREADS, 0, s>>>(p.data, g, m, v, p.ld, g0, g1, a);
+    const int64_t off = (int64_t)row_begin * p.ld;
+    if (per_row > 0 && rows > 0) k_adam<<<grid, ADAM_THREADS, 0, s>>>(p.data + off, g + off, m, v, p.ld, g0, g1, row_begin, a);
     return cudaGetLastError();
 }
 

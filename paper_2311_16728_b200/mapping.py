@@ -35,6 +35,80 @@ def reduce_gradients(grads: torch.Tensor, group=None) -> torch.Tensor:
     return grads
 
 
+def row_shard(K: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Parameter-row shard of the [K][ld] layout for the sharded optimiser:
+    R = ceil(K / world) rows per rank (the buffer is padded to world * R rows so that every
+    rank's rows are one contiguous, equally sized collective chunk); rank g owns rows
+    [g R, min(K, (g + 1) R)).  Returns (R, row_begin, row_end)."""
+    R = -(-K // world)
+    return R, min(K, rank * R), min(K, (rank + 1) * R)
+
+
+def _backend(group) -> str:
+    return dist.get_backend(group)
+
+
+def reduce_scatter_rows(buf: torch.Tensor, R: int, group=None) -> torch.Tensor:
+    """A10 (sharded): after the call rows [g R, (g + 1) R) of the padded [world R][ld] buffer hold
+    the sum over ranks (in-place NCCL reduce-scatter; other rows are left unspecified)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = buf[rank * R:(rank + 1) * R]
+    if _backend(group) == "nccl":
+        dist.reduce_scatter_tensor(mine, buf, op=dist.ReduceOp.SUM, group=group)
+    else:  # gloo has no reduce-scatter: the same sums through an all-reduce
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return mine
+
+
+def all_gather_rows(buf: torch.Tensor, R: int, group=None) -> torch.Tensor:
+    """Every rank's rows [g R, (g + 1) R) of the padded buffer to every rank (in place)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = buf[rank * R:(rank + 1) * R]
+    if _backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, mine, group=group)
+    else:
+        dist.all_gather(list(buf.chunk(world)), mine.clone(), group=group)
+    return buf
+
+
+class ShardedAdam:
+    """A11 sharded by parameter rows (SURVEY §8(e) extension f3): reduce-scatter of the gradient
+    rows, Adam on this rank's rows only (gs_adam_step_rows; m and v exist for those rows only,
+    1/world of the optimiser state), all-gather of the updated parameter rows.  Same NVLink volume
+    as the all-reduce, 1/world of the Adam bytes.  `params` / `grads` are the first K rows of
+    padded [world R][ld] buffers (`padded_params`, `padded_grads`)."""
+
+    def __init__(self, padded_params: torch.Tensor, padded_grads: torch.Tensor, n: int, sh_degree: int,
+                 cfg: AdamConfig | None = None, group=None):
+        from .core import param_rows
+        self.group = group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.K = param_rows(sh_degree)
+        self.R, self.r0, self.r1 = row_shard(self.K, self.rank, self.world)
+        assert padded_params.shape[0] == self.world * self.R and padded_grads.shape == padded_params.shape
+        self.padded_params, self.padded_grads = padded_params, padded_grads
+        self.params, self.grads = padded_params[:self.K], padded_grads[:self.K]
+        self.n, self.D = n, sh_degree
+        self.cfg = cfg or AdamConfig()
+        self.hp = self.cfg.struct()
+        ld = padded_params.shape[1]
+        self.m = torch.zeros((max(self.r1 - self.r0, 1), ld), dtype=torch.float32, device=padded_params.device)
+        self.v = torch.zeros_like(self.m)
+        self.t = 0
+
+    def _adam_rows(self):
+        from . import _lib as L
+        ps = L.params_struct(self.params, self.n, self.D)
+        L.gs_adam_step_rows(ps, self.grads, self.m, self.v, self.hp, self.t, self.r0, self.r1, True)
+
+    def step(self):
+        reduce_scatter_rows(self.padded_grads, self.R, self.group)   # A10
+        self.t += 1
+        if self.r1 > self.r0:
+            self._adam_rows()                                          # A11 on this rank's rows
+        all_gather_rows(self.padded_params, self.R, self.group)       # replicas identical again
+
+
 class MappingEngine:
     """Optimises one Gaussian map against the keyframes of this rank.
 
@@ -43,14 +117,29 @@ class MappingEngine:
     PAPER.md:568)."""
 
     def __init__(self, scene, cams, gts, n_levels: int = 2, lam: float = 0.2, adam: AdamConfig | None = None,
-                 device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0)):
+                 device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0),
+                 shard_optimizer: bool = True):
         self.device = device
         self.n = scene.means.shape[0]
         self.D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
-        self.params = pack_params(scene, device)
-        self.grads = torch.zeros_like(self.params)
+        self.group = group
+        packed = pack_params(scene, device)
+        self.sharded = None
+        if shard_optimizer and self.distributed():
+            # reduce-scatter -> row-sharded Adam -> all-gather (parameters / gradients live in
+            # the first K rows of buffers padded to world x R rows)
+            world = dist.get_world_size(group)
+            R, _, _ = row_shard(packed.shape[0], 0, world)
+            pp = torch.zeros((world * R, packed.shape[1]), dtype=torch.float32, device=device)
+            pp[:packed.shape[0]] = packed
+            self.sharded = ShardedAdam(pp, torch.zeros_like(pp), self.n, self.D, adam, group)
+            self.params, self.grads = self.sharded.params, self.sharded.grads
+        else:
+            self.params = packed
+            self.grads = torch.zeros_like(self.params)
         self.grad2d_norm = torch.zeros(self.n, dtype=torch.float32, device=device)
-        self.adam = Adam(self.params, self.n, self.D, adam)
+        # replicated optimiser state (single GPU / unsharded DP); the sharded one keeps its rows only
+        self.adam = Adam(self.params, self.n, self.D, adam) if self.sharded is None else None
         self.cams0 = list(cams)
         self.V = len(self.cams0)
         self.n_levels = n_levels
@@ -138,8 +227,11 @@ class MappingEngine:
             r.backward_adam(self.params, cams, dL, self.adam, self.grad2d_norm, self.bg)  # A8-A9 + A11
         else:
             r.backward(self.params, cams, dL, self.grads, self.grad2d_norm, self.bg)  # A8-A9
-            reduce_gradients(self.grads, self.group)                         # A10
-            self.adam.step(self.grads, zero_grads=True)                      # A11
+            if self.sharded is not None:
+                self.sharded.step()                                          # A10 + A11, row-sharded
+            else:
+                reduce_gradients(self.grads, self.group)                     # A10
+                self.adam.step(self.grads, zero_grads=True)                  # A11
         return loss
 
     def step(self) -> list:

@@ -87,3 +87,86 @@ def test_gloo_world2_allreduce_equals_batched_gradient(tmp_path):
     scene, cams, G = _views()
     batched = _flat_grad(scene, cams, G)  # one process, all views (R22: sum over the batch)
     np.testing.assert_allclose(g0, batched, rtol=1e-9, atol=1e-12 * np.abs(batched).max())
+
+
+# ------------------------------------------------------------------ sharded optimiser (f3)
+def _row_lr(row: int) -> float:
+    # per-class rates of AdamConfig() in the [K][ld] row order (R20)
+    from paper_2311_16728_b200.core import AdamConfig
+    c = AdamConfig()
+    lrs = [c.lr_means, c.lr_quats, c.lr_log_scales, c.lr_opacity, c.lr_sh_dc, c.lr_sh_rest]
+    cls = 0 if row < 3 else 1 if row < 7 else 2 if row < 10 else 3 if row == 10 else 4 if row < 14 else 5
+    return lrs[cls]
+
+
+def _oracle_adam_rows(P, G, M, V, r0, r1, step):
+    """fp64 oracle Adam on parameter rows [r0, r1) (M, V hold those rows only)."""
+    import oracle.oracle as orc
+    for r in range(r0, r1):
+        p, m, v = orc.adam(P[r].numpy(), G[r].numpy(), M[r - r0].numpy(), V[r - r0].numpy(), lr=_row_lr(r), step=step)
+        P[r] = torch.from_numpy(p)
+        M[r - r0] = torch.from_numpy(m)
+        V[r - r0] = torch.from_numpy(v)
+        G[r] = 0.0
+
+
+def _sharded_worker(rank, world, port, out_dir):
+    from paper_2311_16728_b200.mapping import ShardedAdam, row_shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        scene, cams, G = _views()
+        K, n = 14, scene.means.shape[0]  # D = 0 (tiny): 11 + 3 rows
+        mine = shard_views(len(cams), rank, world)
+        g = torch.from_numpy(_flat_grad(scene, [cams[v] for v in mine], G[mine]).reshape(K, n).copy())
+        p0 = np.concatenate([scene.means.T, scene.quats.T, scene.log_scales.T, scene.opacity_logits[None],
+                             scene.sh.reshape(n, -1).T]).astype(np.float64)
+        R, _, _ = row_shard(K, rank, world)
+        pp = torch.zeros((world * R, n), dtype=torch.float64)
+        pp[:K] = torch.from_numpy(p0)
+        pg = torch.zeros_like(pp)
+        opt = ShardedAdam(pp, pg, n, 0)
+        opt.m = torch.zeros((opt.r1 - opt.r0, n), dtype=torch.float64)
+        opt.v = torch.zeros_like(opt.m)
+        opt._adam_rows = lambda: _oracle_adam_rows(opt.params, opt.grads, opt.m, opt.v, opt.r0, opt.r1, opt.t)
+        for _ in range(2):  # two steps with the same per-rank gradients
+            pg[:K] = g
+            opt.step()
+        np.save(os.path.join(out_dir, f"sp{rank}.npy"), opt.params.numpy())
+        np.save(os.path.join(out_dir, f"rows{rank}.npy"), np.array([opt.r0, opt.r1]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_shard_partition():
+    from paper_2311_16728_b200.mapping import row_shard
+    for K in (14, 59):
+        for world in (1, 2, 3, 8):
+            rows = [row_shard(K, r, world) for r in range(world)]
+            R = rows[0][0]
+            assert all(x[0] == R for x in rows) and R * world >= K
+            covered = [i for _, a, b in rows for i in range(a, b)]
+            assert covered == list(range(K))
+
+
+def test_gloo_world2_sharded_adam_equals_replicated(tmp_path):
+    """reduce-scatter -> row-sharded Adam -> all-gather gives every rank the parameters of the
+    replicated all-reduce + full Adam path, bit for bit (the update is elementwise)."""
+    world = 2
+    mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    s0, s1 = np.load(tmp_path / "sp0.npy"), np.load(tmp_path / "sp1.npy")
+    assert np.array_equal(s0, s1)
+    r0, r1 = np.load(tmp_path / "rows0.npy"), np.load(tmp_path / "rows1.npy")
+    assert r0[0] == 0 and r0[1] == r1[0] and r1[1] == 14
+    # replicated reference: batched gradient (sum over all views), full Adam on every row
+    scene, cams, G = _views()
+    K, n = 14, scene.means.shape[0]
+    g = torch.from_numpy(_flat_grad(scene, cams, G).reshape(K, n).copy())
+    P = torch.from_numpy(np.concatenate([scene.means.T, scene.quats.T, scene.log_scales.T,
+                                         scene.opacity_logits[None], scene.sh.reshape(n, -1).T]).astype(np.float64))
+    M, V = torch.zeros_like(P), torch.zeros_like(P)
+    for step in (1, 2):
+        Gr = g.clone()
+        _oracle_adam_rows(P, Gr, M, V, 0, K, step)
+    np.testing.assert_allclose(s0, P.numpy(), rtol=1e-12, atol=1e-15)

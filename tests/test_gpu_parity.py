@@ -418,6 +418,36 @@ def test_fused_backward_adam_equals_separate(cfg, n, D):
     assert e.value.status == L.GS_ERR_STALE_STATE
 
 
+def test_adam_step_rows_equals_full_step_on_its_rows():
+    """gs_adam_step_rows (row-sharded optimiser) = gs_adam_step restricted to its rows,
+    bit for bit, with the moments of those rows only; the other rows are untouched."""
+    scene = make_scene("tum", n=5000)
+    params = pack_params(scene)
+    K, ld = params.shape
+    gen = torch.Generator("cuda").manual_seed(3)
+    grads = torch.randn(params.shape, device="cuda", generator=gen)
+    full = Adam(params.clone(), scene.n, 3, AdamConfig(lr_means=1e-3))
+    full.m.normal_(generator=gen)
+    full.v.uniform_(generator=gen)
+    m0, v0 = full.m.clone(), full.v.clone()
+    full.t = 2
+    full.step(grads.clone(), zero_grads=True)
+    for r0, r1 in ((0, 11), (11, 14), (14, K), (5, 23)):
+        p = params.clone()
+        g = grads.clone()
+        m, v = m0[r0:r1].clone(), v0[r0:r1].clone()
+        ps = L.params_struct(p, scene.n, 3)
+        L.gs_adam_step_rows(ps, g, m, v, full.hp, 3, r0, r1, True)
+        torch.cuda.synchronize()
+        assert torch.equal(p[r0:r1, :scene.n], full.params[r0:r1, :scene.n])
+        assert torch.equal(m[:, :scene.n], full.m[r0:r1, :scene.n])
+        assert torch.equal(v[:, :scene.n], full.v[r0:r1, :scene.n])
+        assert torch.equal(p[:r0], params[:r0]) and torch.equal(p[r1:], params[r1:])
+        assert (g[r0:r1, :scene.n] == 0).all() and torch.equal(g[r1:], grads[r1:])
+    with pytest.raises(L.GsError):
+        L.gs_adam_step_rows(L.params_struct(params, scene.n, 3), grads, m0, v0, full.hp, 1, 3, K + 1, False)
+
+
 def test_graph_replay_matches_eager_steps():
     """A captured step (device-resident Adam step counter) replayed gives the same trajectory as
     eager steps: 1 warm-up + 2 replays == 3 eager steps (up to atomic-order rounding)."""
