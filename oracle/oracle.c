@@ -877,3 +877,89 @@ void orc_adam(int64_t cnt, double *p, const double *g, double *m, double *v, dou
         p[i] -= lr * mh / (sqrt(vh) + eps);
     }
 }
+
+/* ---------------------------- densify and prune ------------------- */
+/* SPEC.md:463-471 densify_and_prune ("splitting or cloning hyper primitives with
+   large loss gradients similar to [kerbl2023]"), with DESIGN.md readings R27-R30:
+   per Gaussian i (record rec[i][K] = P xyz | q wxyz | log s | logit | SH, the parameter rows of
+   one Gaussian), statistics grad_accum[i] = sum of ||dL/dmean2d|| (pixels) over the visible
+   (iteration, view) pairs, vis_count[i] = their number, max_radius[i] = the largest pixel radius;
+   decisions in fp32 (the same IEEE operations as the GPU):
+     mean  = vis_count > 0 ? grad_accum / vis_count : 0;   high = mean >= grad_thr
+     large = max_j (float)exp((double)log s_j) > percent_dense * extent
+     prune = logit < (float)log(op_thr / (1 - op_thr))  or  max_radius > max_screen
+   class: prune -> 3 (removed); else high && !large -> 1 (clone); high && large -> 2 (split);
+   else 0 (keep).  New map (row order): the kept and cloned originals in index order (bitwise
+   copies), then one clone per clone parent (parent order), then two children per split parent
+   (parent order, child 0 then 1).  A clone is the parent with P + R(q) diag(e^s) z[i][0]; split
+   child c has P + R(q) diag(e^s) z[i][c] and log s - ln 1.6 (scale / 1.6); every other field
+   (quaternion, opacity, SH) is copied.  New Gaussians get m = v = 0, originals keep theirs.
+   z: [n][2][3] standard-normal samples (an input: the randomness the method draws).
+   counts[4] = (clone, split, prune, n_new).  out_* may be NULL (counts only); otherwise they
+   hold n_new records (double). */
+void orc_densify(int64_t n, int K, const float *rec, const float *m, const float *v, const float *grad_accum,
+                 const float *vis_count, const int32_t *max_radius, const float *z, float grad_thr,
+                 float percent_dense, float extent, float op_thr, int32_t max_screen, int8_t *cls,
+                 int64_t counts[4], double *out_rec, double *out_m, double *out_v) {
+    const float logit_thr = (float)log((double)op_thr / (1.0 - (double)op_thr));
+    const float big = percent_dense * extent;
+    int64_t nc = 0, ns = 0, np_ = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const float *r = rec + i * K;
+        const float mean = vis_count[i] > 0.f ? grad_accum[i] / vis_count[i] : 0.f;
+        const int high = mean >= grad_thr;
+        float maxs = 0.f;
+        for (int j = 0; j < 3; j++) {
+            const float e = (float)exp((double)r[7 + j]);
+            if (e > maxs) maxs = e;
+        }
+        const int large = maxs > big;
+        const int prune = r[10] < logit_thr || max_radius[i] > max_screen;
+        cls[i] = prune ? 3 : (high && !large) ? 1 : (high && large) ? 2 : 0;
+        nc += cls[i] == 1;
+        ns += cls[i] == 2;
+        np_ += cls[i] == 3;
+    }
+    counts[0] = nc;
+    counts[1] = ns;
+    counts[2] = np_;
+    counts[3] = n - np_ + nc + ns;
+    if (!out_rec) return;
+    int64_t o = 0;
+    for (int64_t i = 0; i < n; i++)  /* kept and cloned originals */
+        if (cls[i] == 0 || cls[i] == 1) {
+            for (int k = 0; k < K; k++) {
+                out_rec[o * K + k] = rec[i * K + k];
+                out_m[o * K + k] = m[i * K + k];
+                out_v[o * K + k] = v[i * K + k];
+            }
+            o++;
+        }
+    for (int pass = 1; pass <= 2; pass++)  /* clones, then split children */
+        for (int64_t i = 0; i < n; i++) {
+            if (cls[i] != pass) continue;
+            const float *r = rec + i * K;
+            double q[4] = {r[3], r[4], r[5], r[6]}, Rq[9];
+            const double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            for (int j = 0; j < 4; j++) q[j] = qn > 0.0 ? q[j] / qn : (j == 0);
+            quat_to_rot(q, Rq);
+            double e[3];
+            for (int j = 0; j < 3; j++) e[j] = exp((double)r[7 + j]);
+            for (int c = 0; c < pass; c++) {
+                const float *zz = z + (i * 2 + c) * 3;
+                for (int k = 0; k < K; k++) {
+                    out_rec[o * K + k] = r[k];
+                    out_m[o * K + k] = 0.0;
+                    out_v[o * K + k] = 0.0;
+                }
+                for (int a = 0; a < 3; a++) {
+                    double d = 0.0;
+                    for (int j = 0; j < 3; j++) d += Rq[3 * a + j] * e[j] * zz[j];
+                    out_rec[o * K + a] = (double)r[a] + d;
+                }
+                if (pass == 2)
+                    for (int j = 0; j < 3; j++) out_rec[o * K + 7 + j] = (double)r[7 + j] - log(1.6);
+                o++;
+            }
+        }
+}

@@ -230,6 +230,39 @@ def sh_basis(D, dirs):
     return Y, dY
 
 
+def scene_records(scene) -> np.ndarray:
+    """Per-Gaussian parameter records [n][K] (P xyz | q wxyz | log s | logit | SH coefficient-major,
+    the row order of the parameter layout) from a synth.Scene."""
+    n = scene.means.shape[0]
+    return np.ascontiguousarray(np.concatenate([scene.means, scene.quats, scene.log_scales,
+                                                scene.opacity_logits[:, None], scene.sh.reshape(n, -1)], 1),
+                                np.float32)
+
+
+def densify(rec, m, v, grad_accum, vis_count, max_radius, z, grad_thr, percent_dense, extent, op_thr,
+            max_screen) -> dict:
+    """SPEC.md:463-471 densify_and_prune on per-Gaussian records [n][K] (see oracle.c)."""
+    rec = np.ascontiguousarray(rec, np.float32)
+    n, K = rec.shape
+    m = np.ascontiguousarray(m, np.float32)
+    v = np.ascontiguousarray(v, np.float32)
+    ga = np.ascontiguousarray(grad_accum, np.float32)
+    vc = np.ascontiguousarray(vis_count, np.float32)
+    mr = np.ascontiguousarray(max_radius, np.int32)
+    z = np.ascontiguousarray(z, np.float32).reshape(n, 2, 3)
+    cls = np.zeros(n, np.int8)
+    counts = np.zeros(4, np.int64)
+    args = (C.c_int64(n), C.c_int(K), _p(rec), _p(m), _p(v), _p(ga), _p(vc), _p(mr), _p(z), C.c_float(grad_thr),
+            C.c_float(percent_dense), C.c_float(extent), C.c_float(op_thr), C.c_int32(max_screen), _p(cls),
+            _p(counts))
+    lib().orc_densify(*args, None, None, None)
+    nn = int(counts[3])
+    out, om, ov = (np.zeros((max(nn, 1), K)) for _ in range(3))
+    lib().orc_densify(*args, _p(out), _p(om), _p(ov))
+    return dict(cls=cls, n_clone=int(counts[0]), n_split=int(counts[1]), n_prune=int(counts[2]), n_new=nn,
+                rec=out[:nn], m=om[:nn], v=ov[:nn])
+
+
 def exp_scale_f32(s):
     s = np.ascontiguousarray(s, np.float32)
     out = np.zeros_like(s)
