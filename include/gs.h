@@ -150,6 +150,48 @@ gs_status gs_render_backward_adam(gs_params *params, const gs_camera *cams, int3
                                   const gs_adam_hparams *hp, int64_t step, int64_t *step_dev,
                                   float *grad2d_norm_accum, gs_stream_t stream);
 
+/* ---- densify and prune ("splitting or cloning
+   hyper primitives with large loss gradients similar to [kerbl2023]").  Readings R27-R30 in
+   DESIGN.md.  Statistics of a densify interval, per Gaussian: grad_accum = the backward's
+   grad2d_norm_accum (sum of ||dL/dmean2d|| in pixels over visible (iteration, view) pairs),
+   vis_count = number of those pairs, max_radius = largest pixel radius (gs_densify_stats). */
+typedef struct {
+    float grad_threshold;    /* mean ||dL/dmean2d|| (pixels) at or above which a Gaussian densifies */
+    float percent_dense;     /* "large" = max scale > percent_dense * scene_extent (SPEC: 1 %) */
+    float scene_extent;
+    float opacity_threshold; /* prune sigmoid(logit) < this (SPEC default 0.005) */
+    int32_t max_screen_px;   /* prune max_radius > this (SPEC: 0.5 x image dimension) */
+} gs_densify_cfg;
+
+/* Bytes of the temp buffer gs_densify_plan / gs_densify_apply use for n Gaussians. */
+gs_status gs_densify_temp_size(int64_t n, size_t *bytes);
+
+/* After gs_preprocess (or a forward) on ws: vis_count[i] += number of views Gaussian i is
+   visible in, max_radius[i] = max(max_radius[i], its pixel radius).  float[n] / int32[n],
+   device.  GS_ERR_STALE_STATE if ws was not preprocessed with these params and cameras. */
+gs_status gs_densify_stats(const gs_params *params, const gs_camera *cams, int32_t n_views, const void *ws,
+                           size_t ws_bytes, float *vis_count, int32_t *max_radius, gs_stream_t stream);
+
+/* Classify every Gaussian (decisions in fp32: mean = grad_accum / vis_count (0 if never visible),
+   high = mean >= grad_threshold, large = max_j (float)exp((double)log s_j) > percent_dense *
+   scene_extent, prune = logit < (float)log(t / (1 - t)) or max_radius > max_screen_px; prune
+   wins, else high && !large = clone, high && large = split) into temp and return, on the host,
+   counts = {n_clone, n_split, n_prune, n_new} (n_new = n - n_prune + n_clone + n_split).
+   Synchronises the stream (the caller must allocate the new map). */
+gs_status gs_densify_plan(const gs_params *params, const float *grad_accum, const float *vis_count,
+                          const int32_t *max_radius, const gs_densify_cfg *cfg, void *temp, size_t temp_bytes,
+                          int64_t counts[4], gs_stream_t stream);
+
+/* Write the densified map planned in temp into out (out->n = counts[3], same sh_degree, its own
+   ld): kept and cloned originals in index order (bitwise copies, with their Adam moments m, v),
+   then one clone per clone parent, then two children per split parent (parent order).  A new
+   Gaussian is its parent with position P + R(q) diag(e^s) z[i][c] and zero moments; split
+   children also get log s - ln 1.6 (scale / 1.6).  z: device float[n][2][3] standard-normal
+   samples (the method's randomness, an input).  m, v, out_m, out_v may all be NULL (no
+   optimiser state). */
+gs_status gs_densify_apply(const gs_params *params, const float *m, const float *v, const float *z, const void *temp,
+                           size_t temp_bytes, gs_params *out, float *out_m, float *out_v, gs_stream_t stream);
+
 /* A0: Gaussian pyramid (Eq. 5): level l+1 = even rows/cols of the level-l
    image blurred by [1,4,6,4,1]/16 horizontally then vertically with a reflect-101 border
    (R18); sizes ceil-halved.  img [n_images][C][H][W]; out = levels 1..n_levels concatenated,

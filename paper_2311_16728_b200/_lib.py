@@ -25,7 +25,8 @@ GS_TILE = 16
 # every symbol declared in include/gs.h
 EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess", "gs_render_forward",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
-           "gs_pyramid", "gs_adam_step", "gs_adam_step_rows",
+           "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
+           "gs_densify_plan", "gs_densify_apply",
            "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
@@ -49,6 +50,11 @@ class GsParams(C.Structure):
 class GsAdamHparams(C.Structure):
     _fields_ = [("lr", C.c_float * 6), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("sgd_mode", C.c_int32)]
+
+
+class GsDensifyCfg(C.Structure):
+    _fields_ = [("grad_threshold", C.c_float), ("percent_dense", C.c_float), ("scene_extent", C.c_float),
+                ("opacity_threshold", C.c_float), ("max_screen_px", C.c_int32)]
 
 
 class GsWsView(C.Structure):
@@ -224,6 +230,34 @@ def gs_adam_step_rows(params: GsParams, grads, m_rows, v_rows, hp: GsAdamHparams
     _check(lib().gs_adam_step_rows(C.byref(params), _ptr(grads), _ptr(m_rows), _ptr(v_rows), C.byref(hp),
                                    C.c_int64(step), C.c_int32(row_begin), C.c_int32(row_end),
                                    C.c_int32(int(zero_grads)), _stream(stream)), "gs_adam_step_rows")
+
+
+def gs_densify_temp_size(n: int) -> int:
+    b = C.c_size_t()
+    _check(lib().gs_densify_temp_size(C.c_int64(n), C.byref(b)), "gs_densify_temp_size")
+    return b.value
+
+
+def gs_densify_stats(params: GsParams, cams, ws: torch.Tensor, vis_count: torch.Tensor, max_radius: torch.Tensor,
+                     stream=None):
+    ca = camera_struct(cams)
+    _check(lib().gs_densify_stats(C.byref(params), ca, C.c_int32(len(ca)), _ptr(ws), C.c_size_t(ws.numel()),
+                                  _ptr(vis_count), _ptr(max_radius), _stream(stream)), "gs_densify_stats")
+
+
+def gs_densify_plan(params: GsParams, grad_accum, vis_count, max_radius, cfg: GsDensifyCfg, temp: torch.Tensor,
+                    stream=None) -> tuple:
+    """-> (n_clone, n_split, n_prune, n_new); synchronises the stream."""
+    counts = (C.c_int64 * 4)()
+    _check(lib().gs_densify_plan(C.byref(params), _ptr(grad_accum), _ptr(vis_count), _ptr(max_radius), C.byref(cfg),
+                                 _ptr(temp), C.c_size_t(temp.numel()), counts, _stream(stream)), "gs_densify_plan")
+    return tuple(int(x) for x in counts)
+
+
+def gs_densify_apply(params: GsParams, m, v, z: torch.Tensor, temp: torch.Tensor, out: GsParams, out_m, out_v,
+                     stream=None):
+    _check(lib().gs_densify_apply(C.byref(params), _ptr(m), _ptr(v), _ptr(z), _ptr(temp), C.c_size_t(temp.numel()),
+                                  C.byref(out), _ptr(out_m), _ptr(out_v), _stream(stream)), "gs_densify_apply")
 
 
 def gs_query_status(ws: torch.Tensor, stream=None):

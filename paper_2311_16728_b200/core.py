@@ -202,3 +202,35 @@ class Adam:
         ps = L.params_struct(self.params, self.n, self.D)
         L.gs_adam_step(ps, grads, self.m, self.v, self.hp, self.t, g_begin, self.n if g_end is None else g_end,
                        zero_grads)
+
+
+@dataclass
+class DensifyConfig:
+    """Densify-and-prune hyper-parameters (R27-R30)."""
+    grad_threshold: float = 2e-4   # mean ||dL/dmean2d|| in pixels
+    percent_dense: float = 0.01    # "large" above 1 % of the scene extent (SPEC)
+    scene_extent: float = 1.0
+    opacity_threshold: float = 0.005
+    max_screen_frac: float = 0.5   # prune a pixel radius above this fraction of max(W, H)
+
+    def struct(self, width: int, height: int) -> L.GsDensifyCfg:
+        c = L.GsDensifyCfg()
+        c.grad_threshold, c.percent_dense, c.scene_extent = self.grad_threshold, self.percent_dense, self.scene_extent
+        c.opacity_threshold = self.opacity_threshold
+        c.max_screen_px = int(self.max_screen_frac * max(width, height))
+        return c
+
+
+def densify(params: torch.Tensor, n: int, sh_degree: int, m, v, grad_accum: torch.Tensor, vis_count: torch.Tensor,
+            max_radius: torch.Tensor, z: torch.Tensor, cfg: L.GsDensifyCfg):
+    """SURVEY f1 densify and prune: returns (new params [K, ld'], new m, new v, counts) with counts =
+    (n_clone, n_split, n_prune, n_new).  m, v may be None (no optimiser state)."""
+    ps = L.params_struct(params, n, sh_degree)
+    temp = torch.empty(max(L.gs_densify_temp_size(n), 1), dtype=torch.uint8, device=params.device)
+    counts = L.gs_densify_plan(ps, grad_accum, vis_count, max_radius, cfg, temp)
+    nn = counts[3]
+    out = torch.zeros((param_rows(sh_degree), L.param_ld(max(nn, 1))), dtype=torch.float32, device=params.device)
+    om = torch.zeros_like(out) if m is not None else None
+    ov = torch.zeros_like(out) if v is not None else None
+    L.gs_densify_apply(ps, m, v, z, temp, L.params_struct(out, nn, sh_degree), om, ov)
+    return out, om, ov, counts

@@ -7,6 +7,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cmath>
+
 #include "gs_internal.cuh"
 
 namespace gsk {
@@ -353,6 +355,69 @@ gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, floa
     if (row_begin == row_end || params->n == 0) return GS_OK;
     return cuda_status(launch_adam(*params, grads, m_rows, v_rows, *hp, step, 0, params->n, zero_grads,
                                    (cudaStream_t)stream, row_begin, row_end));
+}
+
+gs_status gs_densify_temp_size(int64_t n, size_t *bytes) {
+    if (!bytes || n < 0) return GS_ERR_INVALID_ARG;
+    *bytes = densify_temp_bytes(n);
+    return GS_OK;
+}
+
+gs_status gs_densify_stats(const gs_params *params, const gs_camera *cams, int32_t n_views, const void *ws,
+                           size_t ws_bytes, float *vis_count, int32_t *max_radius, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    static thread_local CamBatch cb;
+    if ((st = check_views(cams, n_views, &cb))) return st;
+    if (!ws || (params->n > 0 && (!vis_count || !max_radius))) return GS_ERR_INVALID_ARG;
+    Layout L;
+    if (!layout_for_bytes(params->n, n_views, cams[0].width, cams[0].height, ws_bytes, &L)) return GS_ERR_SHAPE;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        auto it = g_tokens.find(ws);
+        if (it == g_tokens.end() || it->second.stage < 1 || it->second.stage > 2 ||
+            !same(it->second, make_token(params, cams, n_views, 1)))
+            return GS_ERR_STALE_STATE;
+    }
+    return cuda_status(launch_densify_stats(at<int32_t>(const_cast<void *>(ws), L.radius), params->n, n_views,
+                                            vis_count, max_radius, (cudaStream_t)stream));
+}
+
+gs_status gs_densify_plan(const gs_params *params, const float *grad_accum, const float *vis_count,
+                          const int32_t *max_radius, const gs_densify_cfg *cfg, void *temp, size_t temp_bytes,
+                          int64_t counts[4], gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    if (!cfg || !counts || !temp || (params->n > 0 && (!grad_accum || !vis_count || !max_radius)))
+        return GS_ERR_INVALID_ARG;
+    if (!(cfg->opacity_threshold > 0.f && cfg->opacity_threshold < 1.f)) return GS_ERR_INVALID_ARG;
+    if (temp_bytes < densify_temp_bytes(params->n)) return GS_ERR_SHAPE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const float logit_thr =
+        (float)std::log((double)cfg->opacity_threshold / (1.0 - (double)cfg->opacity_threshold));
+    const float big = cfg->percent_dense * cfg->scene_extent;
+    cudaError_t e = launch_densify_plan(*params, grad_accum, vis_count, max_radius, cfg->grad_threshold, big,
+                                        logit_thr, cfg->max_screen_px, temp, s);
+    if (e != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return GS_ERR_CUDA;
+    uint32_t tot[3] = {0, 0, 0};
+    if (params->n > 0) densify_totals(temp, params->n, tot);
+    counts[0] = tot[1];
+    counts[1] = tot[2];
+    counts[2] = params->n - (int64_t)tot[0] - (int64_t)tot[2];
+    counts[3] = (int64_t)tot[0] + tot[1] + 2 * (int64_t)tot[2];
+    return cuda_status(cudaGetLastError());
+}
+
+gs_status gs_densify_apply(const gs_params *params, const float *m, const float *v, const float *z, const void *temp,
+                           size_t temp_bytes, gs_params *out, float *out_m, float *out_v, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    if ((st = check_params(out))) return st;
+    if (!temp || (params->n > 0 && !z) || out->sh_degree != params->sh_degree) return GS_ERR_INVALID_ARG;
+    if ((m == nullptr) != (out_m == nullptr) || (v == nullptr) != (out_v == nullptr) || (m == nullptr) != (v == nullptr))
+        return GS_ERR_INVALID_ARG;
+    if (temp_bytes < densify_temp_bytes(params->n)) return GS_ERR_SHAPE;
+    return cuda_status(launch_densify_apply(*params, m, v, z, temp, *out, out_m, out_v, (cudaStream_t)stream));
 }
 
 gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs) {

@@ -136,6 +136,16 @@ cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws
 // fused A11: Adam over all Gaussians with the gradient gathered from the scratch (0 if invisible)
 cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, float *m, float *v,
                               const gs_adam_hparams &hp, int64_t step, const int64_t *step_dev, cudaStream_t s);
+// densify and prune (densify.cu)
+size_t densify_temp_bytes(int64_t n);
+cudaError_t launch_densify_stats(const int32_t *radius, int64_t n, int V, float *vis_count, int32_t *max_radius,
+                                 cudaStream_t s);
+cudaError_t launch_densify_plan(const gs_params &p, const float *grad_accum, const float *vis_count,
+                                const int32_t *max_radius, float grad_thr, float big, float logit_thr,
+                                int32_t max_screen, void *temp, cudaStream_t s);
+void densify_totals(const void *temp, int64_t n, uint32_t tot[3]);
+cudaError_t launch_densify_apply(const gs_params &p, const float *m, const float *v, const float *z, const void *temp,
+                                 const gs_params &out, float *out_m, float *out_v, cudaStream_t s);
 cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int W, float lambda, float *loss,
                         float *dL, void *ws, cudaStream_t s);
 size_t loss_ws_bytes(int V, int H, int W);

@@ -10,9 +10,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from synth import scaled_camera
+from synth import densify_samples, scaled_camera
 
-from .core import Adam, AdamConfig, PhotometricLoss, Renderer, gaussian_pyramid, level_shapes, pack_params
+from . import _lib as L
+from .core import (Adam, AdamConfig, DensifyConfig, PhotometricLoss, Renderer, densify, gaussian_pyramid, level_shapes,
+                   pack_params)
 
 
 def gp_level(iteration: int, n_levels: int, iters_per_level: int) -> int:
@@ -118,7 +120,7 @@ class MappingEngine:
 
     def __init__(self, scene, cams, gts, n_levels: int = 2, lam: float = 0.2, adam: AdamConfig | None = None,
                  device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0),
-                 shard_optimizer: bool = True):
+                 shard_optimizer: bool = True, densify_cfg: DensifyConfig | None = None):
         self.device = device
         self.n = scene.means.shape[0]
         self.D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
@@ -138,6 +140,10 @@ class MappingEngine:
             self.params = packed
             self.grads = torch.zeros_like(self.params)
         self.grad2d_norm = torch.zeros(self.n, dtype=torch.float32, device=device)
+        # densification statistics: visible (iteration, view) pairs and max pixel radius
+        self.densify_cfg = densify_cfg
+        self.vis_count = torch.zeros(self.n, dtype=torch.float32, device=device)
+        self.max_radius = torch.zeros(self.n, dtype=torch.int32, device=device)
         # replicated optimiser state (single GPU / unsharded DP); the sharded one keeps its rows only
         self.adam = Adam(self.params, self.n, self.D, adam) if self.sharded is None else None
         self.cams0 = list(cams)
@@ -220,6 +226,9 @@ class MappingEngine:
         r = self.renderers[level]
         cams = self.cams[level]
         rgb, _ = r.forward(self.params, cams, self.bg)                       # A1-A6
+        if self.densify_cfg is not None:                                     # f1 statistics
+            L.gs_densify_stats(L.params_struct(self.params, self.n, self.D), cams, r.ws.buf, self.vis_count,
+                               self.max_radius)
         loss, dL = self.losses[level](rgb, self._pyramid(level))             # A7
         if fused is None:
             fused = not self.distributed()
@@ -237,6 +246,39 @@ class MappingEngine:
     def step(self) -> list:
         """One pass of the Eq. 5 schedule: iterations at levels n, n-1, ..., 0."""
         return [self.iteration(l) for l in range(self.n_levels, -1, -1)]
+
+    # ------------------------------------------------------------------ densify and prune (f1)
+    def densify_and_prune(self, seed: int) -> tuple:
+        """SPEC.md:463-471 with the statistics gathered since the last call (needs densify_cfg):
+        clone / split / prune, the Adam moments follow their Gaussians (new ones start at 0), the
+        statistics are reset and the level workspaces re-sized.  Returns (n_cloned, n_split,
+        n_pruned).  With replicated data parallelism the statistics are combined first (sum /
+        max) so every rank takes the same decisions with the same samples."""
+        if self.densify_cfg is None:
+            raise RuntimeError("densify_and_prune needs MappingEngine(densify_cfg=...)")
+        if self.sharded is not None:
+            raise NotImplementedError("densify with the row-sharded optimiser (use shard_optimizer=False)")
+        if self.distributed():
+            dist.all_reduce(self.grad2d_norm, group=self.group)
+            dist.all_reduce(self.vis_count, group=self.group)
+            dist.all_reduce(self.max_radius, op=dist.ReduceOp.MAX, group=self.group)
+        z = torch.from_numpy(densify_samples(self.n, seed)).to(self.params.device)
+        H, W = self.shapes[0]
+        cfg = self.densify_cfg.struct(W, H)
+        p, m, v, counts = densify(self.params, self.n, self.D, self.adam.m, self.adam.v, self.grad2d_norm,
+                                  self.vis_count, self.max_radius, z, cfg)
+        self.n = counts[3]
+        self.params = p
+        self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, self.n
+        self.grads = torch.zeros_like(p)
+        dev = p.device
+        self.grad2d_norm = torch.zeros(max(self.n, 1), dtype=torch.float32, device=dev)
+        self.vis_count = torch.zeros(max(self.n, 1), dtype=torch.float32, device=dev)
+        self.max_radius = torch.zeros(max(self.n, 1), dtype=torch.int32, device=dev)
+        self.renderers = [None] * (self.n_levels + 1)
+        self.graph = None  # a captured step refers to the old buffers
+        self.calibrate()
+        return counts[:3]
 
     # ------------------------------------------------------------------ CUDA graphs
     def capture(self, gts_pinned: torch.Tensor | None = None, out_pinned: torch.Tensor | None = None):

@@ -337,3 +337,10 @@ def perturb(scene: Scene, seed: int) -> Scene:
     s.sh[:, 0, :] += rng.normal(0.0, 0.2, size=(n, 3)).astype(np.float32)
     s.opacity_logits += rng.normal(0.0, 0.5, size=n).astype(np.float32)
     return s
+
+
+def densify_samples(n: int, seed: int) -> np.ndarray:
+    """Standard-normal samples [n][2][3] float32: the randomness densify draws (one offset per
+    clone, two per split), generated here and passed to both sides as an input."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    return rng.normal(size=(n, 2, 3)).astype(np.float32)
