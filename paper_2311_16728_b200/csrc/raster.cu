@@ -155,6 +155,50 @@ __device__ __forceinline__ void warp_block(int &tile_x, int &wx0, int &wy0, int 
     ly = wy0 + (lane >> 3);
 }
 
+// Per-pixel outputs of the forward: colour (+ T_final bg), T, last position, composited count;
+// with CHUNKED the reverse pass turning the per-chunk records into (T after the chunk,
+// normalised colour behind it) for the chunked backward.
+template <bool CHUNKED>
+__device__ __forceinline__ void fwd_finish(int view, int px, int py, int W, int H, float T, float c0, float c1,
+                                           float c2, uint32_t last, uint32_t composited, float bg0, float bg1,
+                                           float bg2, float *out_rgb, float *out_T, float *T_keep,
+                                           uint32_t *ncontrib, uint32_t *ncomp, size_t chunk_base_tile, int lpix,
+                                           float4 *chunk_bwd) {
+    const int64_t HW = (int64_t)H * W;
+    const int64_t pix = (int64_t)py * W + px;
+    float *o = out_rgb + (int64_t)view * 3 * HW + pix;
+    o[0] = c0 + T * bg0;
+    o[HW] = c1 + T * bg1;
+    o[2 * HW] = c2 + T * bg2;
+    if (out_T) out_T[(int64_t)view * HW + pix] = T;
+    T_keep[(int64_t)view * HW + pix] = T;
+    ncontrib[(int64_t)view * HW + pix] = last;
+    ncomp[(int64_t)view * HW + pix] = composited;
+    if (CHUNKED && last > 0) {
+        // reverse pass over the chunks up to the last composited one: normalised colour behind
+        // each chunk, acc_end(k) = behind(k) / T_after(k), behind(k) = sum of the later chunks'
+        // colour + T_final bg (positive terms only -- no cancellation); eight chunks per round,
+        // their loads issued together before any store
+        float e0 = T * bg0, e1 = T * bg1, e2 = T * bg2;
+        float4 *col = chunk_bwd + chunk_base_tile * TILE_PIX + lpix;
+        for (int k = (int)((last - 1) / CHUNK); k >= 0; k -= 8) {
+            float4 e[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (k - u >= 0) e[u] = col[(size_t)(k - u) * TILE_PIX];
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (k - u >= 0) {
+                    const float inv = 1.0f / e[u].x;
+                    col[(size_t)(k - u) * TILE_PIX] = make_float4(e[u].x, e0 * inv, e1 * inv, e2 * inv);
+                    e0 += e[u].y;
+                    e1 += e[u].z;
+                    e2 += e[u].w;
+                }
+        }
+    }
+}
+
 template <int WARPS, bool CHUNKED>
 __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restrict__ ranges,
                                                            const float4 *__restrict__ prec, int W, int H, int TX,
@@ -282,42 +326,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     }
     // never leave with a bulk copy still writing into this CTA's shared memory
     if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], (phases >> inflight) & 1u);
-    if (inside) {
-        int64_t HW = (int64_t)H * W;
-        int64_t pix = (int64_t)py * W + px;
-        float *o = out_rgb + (int64_t)view * 3 * HW + pix;
-        o[0] = c0 + T * bg0;
-        o[HW] = c1 + T * bg1;
-        o[2 * HW] = c2 + T * bg2;
-        if (out_T) out_T[(int64_t)view * HW + pix] = T;
-        T_keep[(int64_t)view * HW + pix] = T;
-        ncontrib[(int64_t)view * HW + pix] = last;
-        ncomp[(int64_t)view * HW + pix] = composited;
-        if (CHUNKED && last > 0) {
-            // reverse pass over the chunks up to the last composited one: normalised colour
-            // behind each chunk, acc_end(k) = behind(k) / T_after(k), behind(k) = sum of the later
-            // chunks' colour + T_final bg (positive terms only -- no cancellation)
-            const size_t cb = chunk_base[view * tiles + tile];
-            float e0 = T * bg0, e1 = T * bg1, e2 = T * bg2;
-            // eight chunks per round: their loads are issued together, before any store
-            float4 *col = chunk_bwd + cb * TILE_PIX + ly * TILE + lx;
-            for (int k = (int)((last - 1) / CHUNK); k >= 0; k -= 8) {
-                float4 e[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (k - u >= 0) e[u] = col[(size_t)(k - u) * TILE_PIX];
-#pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (k - u >= 0) {
-                        const float inv = 1.0f / e[u].x;
-                        col[(size_t)(k - u) * TILE_PIX] = make_float4(e[u].x, e0 * inv, e1 * inv, e2 * inv);
-                        e0 += e[u].y;
-                        e1 += e[u].z;
-                        e2 += e[u].w;
-                    }
-            }
-        }
-    }
+    if (inside)
+        fwd_finish<CHUNKED>(view, px, py, W, H, T, c0, c1, c2, last, composited, bg0, bg1, bg2, out_rgb, out_T, T_keep,
+                            ncontrib, ncomp, CHUNKED ? chunk_base[view * tiles + tile] : 0, ly * TILE + lx,
+                            chunk_bwd);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
