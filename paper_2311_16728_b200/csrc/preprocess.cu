@@ -335,6 +335,9 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     const int32_t *radius = at<const int32_t>(ws, L.radius);
     float4 *g2d = at<float4>(ws, L.grad2d);
     float *S = at<float>(ws, L.scratch);  // [row][n], column t
+    // loads whose values are needed only late, issued up front (the kernel is latency-bound)
+    const float gnorm_old = gnorm ? gnorm[i] : 0.f;
+    const int32_t rad0 = radius[i];  // view 0 (the common single-view case)
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
                           P[9 * ld + i]);
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     // ---- geometry: conic -> Sigma2 -> (Sigma3, J) -> (q, s), mean2d -> P
     for (int v = 0; v < V; v++) {
         int64_t m = (int64_t)v * n + i;
-        if (radius[m] <= 0) continue;
+        if ((v == 0 ? rad0 : radius[m]) <= 0) continue;
         const gs_camera &cam = cams.c[v];
         Proj p = project_recipe(cam, px, py, pz, cv, L.TX, L.TY);
         float4 ga = g2d[3 * m], gb = g2d[3 * m + 1];
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         }
         for (int v = 0; v < V; v++) {
             int64_t m = (int64_t)v * n + i;
-            if (radius[m] <= 0) continue;
+            if ((v == 0 ? rad0 : radius[m]) <= 0) continue;
             const float *gcol4 = reinterpret_cast<const float *>(g2d + 3 * m);
             float gcol = gcol4[6 + ch];  // record [.. | C, sigma, r, g | b ..]
             float Cc[3];
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     S[8 * n + t] = gs[1];
     S[9 * n + t] = gs[2];
     S[10 * n + t] = sig * (1.f - sig) * gop;
-    if (gnorm) gnorm[i] += norm_acc;
+    if (gnorm) gnorm[i] = gnorm_old + norm_acc;
 }
 
 cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
