@@ -211,6 +211,11 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
                                                const CamBatch &cams, int V, const Layout &L, char *ws,
                                                bool count_tiles, bool smem_cnt, uint32_t *s_cnt, int64_t i) {
     constexpr int NC = (D + 1) * (D + 1);
+    // every load of the Gaussian is issued before the projection chain (the kernel is bound by
+    // memory latency; culled lanes' SH sectors are fetched for the warp's visible lanes anyway)
+    float shc[3 * NC];
+#pragma unroll
+    for (int k = 0; k < 3 * NC; k++) shc[k] = P[(11 + k) * ld + i];
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
                           P[9 * ld + i]);
@@ -247,7 +252,7 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
         for (int ch = 0; ch < 3; ch++) {
             float acc = 0.5f;
 #pragma unroll
-            for (int l = 0; l < NC; l++) acc += P[(11 + 3 * l + ch) * ld + i] * Y[l];
+            for (int l = 0; l < NC; l++) acc += shc[3 * l + ch] * Y[l];
             rgb[ch] = fmaxf(acc, 0.0f);
         }
         rec0[m] = make_float4(p.u, p.v, p.A, p.B);
