@@ -8,6 +8,7 @@
 #include <vector>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "gs_internal.cuh"
 
@@ -134,6 +135,14 @@ static gs_status check_views(const gs_camera *cams, int V, CamBatch *cb) {
 }
 
 static gs_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GS_OK : GS_ERR_CUDA; }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("GS_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 static int g_binning_mode = 0;
 int binning_mode() { return g_binning_mode; }

@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
                                                      uint32_t *__restrict__ cursor, int64_t n, int V, int TX,
                                                      int tiles, int64_t cap, uint64_t *__restrict__ tmp,
                                                      WsHeader *hdr) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     extern __shared__ uint32_t s_bins[];  // [0, VT): counts then running slot; [VT, 2 VT): base
     const int VT = V * tiles;
     const bool use_smem = VT <= SMEM_BINS;  // uniform (the launch passes 2*VT words of dynamic smem)
@@ -215,6 +217,8 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_tile_sort_small(
     const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, int64_t cap,
     const uint64_t *__restrict__ tmp, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
     uint2 *__restrict__ ranges, uint32_t *__restrict__ big_tiles, WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ uint64_t sk[256];
     const int gt = blockIdx.x;
     rs.vbase = (int64_t)(gt / tiles) * n;
@@ -241,6 +245,8 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t 
                                                                  const uint32_t *__restrict__ big_tiles,
                                                                  uint64_t *__restrict__ big, const WsHeader *hdr,
                                                                  RecSrc rs, int64_t n, int tiles) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ uint64_t sk[TS_SMEM_KEYS];
     const uint32_t nb = hdr->n_big;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
@@ -285,13 +291,13 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
         attr = true;
     }
     if (L.n > 0)
-        k_bin_scatter<<<(unsigned)((L.n + 255) / 256), 256, smem, s>>>(
+        launch_pdl(k_bin_scatter, (unsigned)((L.n + 255) / 256), 256, smem, s, 
             at<int4>(ws, L.rect), at<int32_t>(ws, L.radius), at<float>(ws, L.depth), at<uint32_t>(ws, L.vis_list),
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
     ProfScope prof("k_tile_sort", s);
     const RecSrc rs{at<float4>(ws, L.rec0), at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), at<float4>(ws, L.prec), 0};
-    k_tile_sort_small<<<(unsigned)VT, SG_WARPS * 32, 0, s>>>(
+    launch_pdl(k_tile_sort_small, (unsigned)VT, SG_WARPS * 32, 0, s, 
         at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), L.cap, at<uint64_t>(ws, L.keys1),
         at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.big_tiles),
         at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
@@ -301,7 +307,7 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    k_tile_sort_big<<<(unsigned)std::min<int64_t>(VT, 2 * sms), BG_WARPS * 32, 0, s>>>(
+    launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT, 2 * sms), BG_WARPS * 32, 0, s, 
         at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
         at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
         at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);

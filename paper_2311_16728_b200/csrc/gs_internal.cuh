@@ -73,6 +73,41 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap);
 // largest layout (capacity) fitting in ws_bytes; returns false if even cap = 0 does not fit
 bool layout_for_bytes(int64_t n, int V, int W, int H, size_t ws_bytes, Layout *out);
 
+// ---- Programmatic dependent launch (PDL): kernels of the per-iteration chain are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs are scheduled while its
+// predecessor drains.  Every such kernel calls pdl_wait() before touching global memory (it
+// returns once the predecessor grid has completed and its writes are visible -- so completion
+// stays transitive along the chain) and pdl_trigger() to let its own successor be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // api.cu: on unless the environment sets GS_PDL=0 (A/B measurements)
+
+// Eager launches only: measured on B200, PDL shortens the eager mapping step by ~7 % but slows
+// the replay of a captured CUDA graph (whose launches are already pipelined) by ~2 %, so launches
+// recorded into a graph stay plain.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (!pdl_enabled() || cap != cudaStreamCaptureStatusNone) {
+        kernel<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <typename T>
 __host__ __device__ inline T *at(void *ws, size_t off) {
     return reinterpret_cast<T *>(reinterpret_cast<char *>(ws) + off);

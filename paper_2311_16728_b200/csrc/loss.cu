@@ -74,6 +74,8 @@ __device__ __forceinline__ void load_patches(float (*dst)[SH][SWP], const float 
 __global__ void __launch_bounds__(NT) k_ssim_fwd(const float *__restrict__ X, const float *__restrict__ Y, int H,
                                                  int W, Win win, float *__restrict__ dA, float *__restrict__ dB,
                                                  float *__restrict__ dC, float2 *__restrict__ part) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ float sxy[2][SH][SWP];
     __shared__ float hm[5][SH][TW + 1];
     float (*sx)[SWP] = sxy[0];
@@ -211,6 +213,8 @@ __device__ __forceinline__ void finalize_view(const float2 *__restrict__ part, i
 // loss only (no gradient requested): one CTA per view
 __global__ void __launch_bounds__(256) k_loss_final(const float2 *__restrict__ part, int nbt, float lambda, float invN,
                                                     float *loss) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     finalize_view(part, blockIdx.x, nbt, lambda, invN, loss);
 }
 
@@ -219,6 +223,8 @@ __global__ void __launch_bounds__(NT) k_ssim_bwd(const float *__restrict__ X, co
                                                  const float *__restrict__ dA, const float *__restrict__ dB,
                                                  const float *__restrict__ dC, float *__restrict__ dL,
                                                  const float2 *__restrict__ part, float *__restrict__ loss) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ float s[3][SH][SWP];
     __shared__ float hm[3][SH][TW + 1];
     const int plane = blockIdx.z;
@@ -311,11 +317,11 @@ cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int 
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, V * 3);
     const int nbt = grid.x * grid.y;
     float invN = (float)(1.0 / (3.0 * H * W));
-    k_ssim_fwd<<<grid, NT, 0, s>>>(render, gt, H, W, win, dA, dB, dC, part);
+    launch_pdl(k_ssim_fwd, grid, NT, 0, s, render, gt, H, W, win, dA, dB, dC, part);
     if (dL)
-        k_ssim_bwd<<<grid, NT, 0, s>>>(render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);
+        launch_pdl(k_ssim_bwd, grid, NT, 0, s, render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);
     else
-        k_loss_final<<<V, 256, 0, s>>>(part, nbt, lambda, invN, loss);
+        launch_pdl(k_loss_final, V, 256, 0, s, part, nbt, lambda, invN, loss);
     return cudaGetLastError();
 }
 

@@ -302,6 +302,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P, int64_t n, int64_t ld,
                                                     const CamBatch cams, int V, Layout L, char *ws,
                                                     bool count_tiles) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ uint32_t s_cnt[SMEM_BINS];
     const int VT = V * L.tiles;
     const bool smem_cnt = count_tiles && VT <= SMEM_BINS;  // uniform
@@ -331,6 +333,8 @@ template <int D>
 __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict__ P, int64_t n, int64_t ld,
                                                         const CamBatch cams, int V, Layout L, char *ws,
                                                         float *__restrict__ gnorm, int64_t *step_inc) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     constexpr int NC = (D + 1) * (D + 1);
     if (step_inc && blockIdx.x == 0 && threadIdx.x == 0) *step_inc += 1;  // device step for the fused Adam
     const uint32_t nvis = at<WsHeader>(ws, L.hdr)->vis_count;
@@ -510,10 +514,10 @@ cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, c
     if (blocks == 0) return cudaGetLastError();
     ProfScope prof("k_preprocess", s);
     switch (p.sh_degree) {
-        case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        default: k_preprocess<3><<<blocks, 256, 0, s>>>(p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 0: launch_pdl(k_preprocess<0>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 1: launch_pdl(k_preprocess<1>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 2: launch_pdl(k_preprocess<2>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        default: launch_pdl(k_preprocess<3>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
     }
     return cudaGetLastError();
 }
@@ -525,10 +529,10 @@ cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int 
     char *w = (char *)ws;
     ProfScope prof("k_preprocess_bwd", s);
     switch (p.sh_degree) {
-        case 0: k_preprocess_bwd<0><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
-        case 1: k_preprocess_bwd<1><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
-        case 2: k_preprocess_bwd<2><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
-        default: k_preprocess_bwd<3><<<blocks, 128, 0, s>>>(p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        case 0: launch_pdl(k_preprocess_bwd<0>, blocks, 128, 0, s, p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        case 1: launch_pdl(k_preprocess_bwd<1>, blocks, 128, 0, s, p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        case 2: launch_pdl(k_preprocess_bwd<2>, blocks, 128, 0, s, p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
+        default: launch_pdl(k_preprocess_bwd<3>, blocks, 128, 0, s, p.data, p.n, p.ld, cams, V, L, w, grad2d_norm, step_inc); break;
     }
     return cudaGetLastError();
 }

@@ -115,6 +115,8 @@ constexpr int ADAM_UNROLL = 2;
 __global__ void __launch_bounds__(ADAM_THREADS) k_adam(float *__restrict__ P, float *__restrict__ G,
                                                        float *__restrict__ Mm, float *__restrict__ Vv, int64_t ld,
                                                        int64_t g0, int64_t g1, int row0, AdamArgs a) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     const int row = blockIdx.y;
     const float lr = a.lr[row_class(row0 + row)];
     const int64_t per_row = ld / 4;
@@ -179,6 +181,8 @@ __device__ __forceinline__ bool load_slots(const uint32_t *slot, int64_t i0, int
 __global__ void __launch_bounds__(COL_THREADS) k_grad_accumulate(float *__restrict__ G, int64_t ld, int64_t n,
                                                                  int rows, const uint32_t *__restrict__ slot,
                                                                  const float *__restrict__ S) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     const int64_t c4 = (int64_t)blockIdx.x * COL_THREADS + threadIdx.x;
     const int64_t i0 = c4 * 4;
     if (i0 >= n) return;
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(COL_THREADS) k_adam_fused(float *__restrict__ 
                                                             float *__restrict__ Vv, int64_t ld, int64_t n, int rows,
                                                             const uint32_t *__restrict__ slot,
                                                             const float *__restrict__ S, AdamArgs a) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     adam_device_step(a);
     const int64_t c4 = (int64_t)blockIdx.x * COL_THREADS + threadIdx.x;
     const int64_t i0 = c4 * 4;
@@ -237,7 +243,7 @@ cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws
     int64_t cols4 = (p.n + 3) / 4;
     if (cols4 == 0) return cudaGetLastError();
     dim3 grid((unsigned)((cols4 + COL_THREADS - 1) / COL_THREADS), ROW_GROUPS);
-    k_grad_accumulate<<<grid, COL_THREADS, 0, s>>>(grads, p.ld, p.n, gs_param_rows(p.sh_degree),
+    launch_pdl(k_grad_accumulate, grid, COL_THREADS, 0, s, grads, p.ld, p.n, gs_param_rows(p.sh_degree),
                                                    at<uint32_t>(ws, L.slot), at<float>(ws, L.scratch));
     return cudaGetLastError();
 }
@@ -265,7 +271,7 @@ cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, flo
     if (cols4 == 0) return cudaGetLastError();
     dim3 grid((unsigned)((cols4 + COL_THREADS - 1) / COL_THREADS), ROW_GROUPS);
     ProfScope prof("k_adam_fused", s);
-    k_adam_fused<<<grid, COL_THREADS, 0, s>>>(p.data, m, v, p.ld, p.n, gs_param_rows(p.sh_degree),
+    launch_pdl(k_adam_fused, grid, COL_THREADS, 0, s, p.data, m, v, p.ld, p.n, gs_param_rows(p.sh_degree),
                                               at<uint32_t>(ws, L.slot), at<float>(ws, L.scratch), a);
     return cudaGetLastError();
 }
@@ -279,7 +285,7 @@ cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const 
     dim3 grid((unsigned)((per_row + ADAM_THREADS * ADAM_UNROLL - 1) / (ADAM_THREADS * ADAM_UNROLL)), rows);
     ProfScope prof("k_adam", s);
     const int64_t off = (int64_t)row_begin * p.ld;
-    if (per_row > 0 && rows > 0) k_adam<<<grid, ADAM_THREADS, 0, s>>>(p.data + off, g + off, m, v, p.ld, g0, g1, row_begin, a);
+    if (per_row > 0 && rows > 0) launch_pdl(k_adam, grid, ADAM_THREADS, 0, s, p.data + off, g + off, m, v, p.ld, g0, g1, row_begin, a);
     return cudaGetLastError();
 }
 

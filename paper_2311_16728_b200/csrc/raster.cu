@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                                                            uint32_t *__restrict__ ncomp,
                                                            const uint32_t *__restrict__ chunk_base,
                                                            float4 *__restrict__ chunk_bwd) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     constexpr int NT = WARPS * 32;
     __shared__ __align__(128) RasterSmem S;
     constexpr int SEG = CHUNKED ? CHUNK : BATCH;  // list segment = unit of chunk recording
@@ -379,6 +381,8 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
                                                       uint32_t *__restrict__ chunk_base,
                                                       uint32_t *__restrict__ chunk_tile, WsHeader *hdr,
                                                       int64_t max_chunks) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ uint32_t s[1024];
     const int t = threadIdx.x;
     uint32_t nch = 0;
@@ -478,6 +482,8 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
                                                      const float *__restrict__ T_keep,
                                                      const uint32_t *__restrict__ ncontrib,
                                                      float4 *__restrict__ g2d) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ __align__(128) RasterSmem S;
     __shared__ uint8_t wl[4][BATCH];
     __shared__ uint32_t s_maxlast;
@@ -580,6 +586,8 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
                                                            const uint32_t *__restrict__ ncontrib,
                                                            const float4 *__restrict__ chunk_bwd,
                                                            float4 *__restrict__ g2d) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ __align__(128) float4 rec[CHUNK * 3];
     __shared__ uint64_t bar;
     __shared__ uint8_t wl[4][CHUNK];
@@ -695,7 +703,7 @@ static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_
                        const uint32_t *cbase, float4 *cbwd, cudaStream_t s) {
     dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
     auto kern = cbwd ? k_raster_fwd<WARPS, true> : k_raster_fwd<WARPS, false>;
-    kern<<<grid, WARPS * 32, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX, L.tiles, bg[0],
+    launch_pdl(kern, grid, WARPS * 32, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX, L.tiles, bg[0],
                                      bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
                                      at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd);
 }
@@ -707,7 +715,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
     uint32_t *cbase = nullptr;
     float4 *cbwd = nullptr;
     if (L.max_chunks > 0) {  // few tiles: record per-chunk state for the chunk-parallel backward
-        k_chunk_index<<<1, 1024, 0, s>>>(at<uint2>(ws, L.ranges), L.V * L.tiles, at<uint32_t>(ws, L.chunk_base),
+        launch_pdl(k_chunk_index, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles, at<uint32_t>(ws, L.chunk_base),
                                          at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.max_chunks);
         cbase = at<uint32_t>(ws, L.chunk_base);
         cbwd = at<float4>(ws, L.chunk_bwd);
@@ -723,7 +731,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     ProfScope prof("k_raster_bwd", s);
     if (L.max_chunks > 0) {  // chunked path (few tiles): every chunk replayed independently
-        k_raster_bwd2_chunk<<<(unsigned)L.max_chunks, 128, 0, s>>>(
+        launch_pdl(k_raster_bwd2_chunk, (unsigned)L.max_chunks, 128, 0, s, 
             at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
             at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
@@ -731,7 +739,7 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
     }
     // many tiles: two pixels per lane, packed fp32x2
     dim3 grid(L.TX, L.TY, L.V);
-    k_raster_bwd2<<<grid, 128, 0, s>>>(at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
+    launch_pdl(k_raster_bwd2, grid, 128, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
                                        L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
                                        at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
     return cudaGetLastError();

@@ -39,6 +39,8 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
                                                        int64_t M, uint64_t *flags, WsHeader *hdr, int stride) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_warp[SCAN_THREADS / 32];
     __shared__ uint64_t s_prefix;
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const uint32_t *__restric
 cudaError_t launch_scan_u32(const uint32_t *in, uint32_t *out, int64_t count, uint64_t *flags, WsHeader *hdr,
                             cudaStream_t s, int in_stride) {
     if (count == 0) return cudaGetLastError();
-    k_scan<<<(unsigned)((count + SCAN_TILE - 1) / SCAN_TILE), SCAN_THREADS, 0, s>>>(in, out, count, flags, hdr,
+    launch_pdl(k_scan, (unsigned)((count + SCAN_TILE - 1) / SCAN_TILE), SCAN_THREADS, 0, s, in, out, count, flags, hdr,
                                                                                     in_stride);
     return cudaGetLastError();
 }
