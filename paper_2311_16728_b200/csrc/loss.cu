@@ -43,27 +43,37 @@ constexpr float SS_C1 = 0.01f * 0.01f;
 constexpr float SS_C2 = 0.03f * 0.03f;
 
 // Load the (TH + 10) x (TW + 10) patches of M maps around the tile into smem (zero outside the
-// image).  All global loads are issued before the first shared store, so their latencies overlap.
+// image).  Warp w takes patch rows w, w + 8, ...; lanes cover the 42 columns in two steps (no
+// index division).  All global loads are issued before the first shared store.
 template <int M>
 __device__ __forceinline__ void load_patches(float (*dst)[SH][SWP], const float *const (&src)[M], int H, int W,
                                              int x0, int y0) {
-    constexpr int IT = (SH * SW + NT - 1) / NT;
-    float v[M][IT];
+    constexpr int NW = NT / 32, RPW = (SH + NW - 1) / NW;  // rows per warp
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float v[M][RPW][2];
 #pragma unroll
-    for (int i = 0; i < IT; i++) {
-        const int k = threadIdx.x + i * NT;
-        const int r = k / SW, c = k % SW;
-        const int gy = y0 + r, gx = x0 + c;
-        const bool ok = k < SH * SW && gy >= 0 && gy < H && gx >= 0 && gx < W;
+    for (int i = 0; i < RPW; i++) {
+        const int r = warp + i * NW;
+        const int gy = y0 + r;
 #pragma unroll
-        for (int m = 0; m < M; m++) v[m][i] = ok ? __ldg(src[m] + (int64_t)gy * W + gx) : 0.f;
+        for (int h = 0; h < 2; h++) {
+            const int c = lane + 32 * h;
+            const int gx = x0 + c;
+            const bool ok = r < SH && c < SW && gy >= 0 && gy < H && gx >= 0 && gx < W;
+#pragma unroll
+            for (int m = 0; m < M; m++) v[m][i][h] = ok ? __ldg(src[m] + (int64_t)gy * W + gx) : 0.f;
+        }
     }
 #pragma unroll
-    for (int i = 0; i < IT; i++) {
-        const int k = threadIdx.x + i * NT;
-        if (k < SH * SW)
+    for (int i = 0; i < RPW; i++) {
+        const int r = warp + i * NW;
 #pragma unroll
-            for (int m = 0; m < M; m++) dst[m][k / SW][k % SW] = v[m][i];
+        for (int h = 0; h < 2; h++) {
+            const int c = lane + 32 * h;
+            if (r < SH && c < SW)
+#pragma unroll
+                for (int m = 0; m < M; m++) dst[m][r][c] = v[m][i][h];
+        }
     }
 }
 
@@ -145,10 +155,11 @@ __global__ void __launch_bounds__(NT) k_ssim_fwd(const float *__restrict__ X, co
             const float sxx = mom[2][o] - mx * mx, syy = mom[3][o] - my * my, sxy = mom[4][o] - mx * my;
             const float a1 = 2.f * mx * my + SS_C1, a2 = 2.f * sxy + SS_C2;
             const float b1 = mx * mx + my * my + SS_C1, b2 = sxx + syy + SS_C2;
-            const float ib = 1.f / (b1 * b2);
+            // SFU reciprocals (rel. error ~1e-7; b1, b2 >= C1, C2 > 0)
+            const float ib = __fdividef(1.f, b1 * b2);
             const float S = a1 * a2 * ib;
-            const float dS_dmx = 2.f * my * a2 * ib - S * 2.f * mx / b1;
-            const float dS_dsxx = -S / b2;
+            const float dS_dmx = 2.f * my * a2 * ib - __fdividef(S * 2.f * mx, b1);
+            const float dS_dsxx = -__fdividef(S, b2);
             const float dS_dsxy = 2.f * a1 * ib;
             const int64_t o_ = plane * HW + (int64_t)gy * W + gx;
             dA[o_] = dS_dmx + dS_dsxx * (-2.f * mx) + dS_dsxy * (-my);
