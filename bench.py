@@ -183,11 +183,12 @@ def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
     binning 0: bucket scatter, short- and long-bucket tile sorts with the pair-record gather (3) /
     binning 1: duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, pair gather
-    (5 + passes); raster fwd (1), + chunk index on levels with few tiles (chunked raster path);
+    (5 + passes); raster fwd (1) after the chunk index (levels with few tiles, chunked raster path)
+    or the longest-first tile order (other levels) (1);
     loss (2); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
     binning_kernels = 3 if binning == 0 else 5 + passes
-    return 2 + binning_kernels + 1 + (1 if chunked else 0) + 2 + (3 if fused else 4)
+    return 2 + binning_kernels + 1 + 1 + 2 + (3 if fused else 4)
 
 
 def run_ours(args):

@@ -63,6 +63,7 @@ struct Layout {
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
     size_t tile_count, tile_start, tile_cursor, bin_big, big_tiles;  // bucket binning (bin.cu)
+    size_t tile_order;  // (view, tile) indices, longest list first (raster.cu)
     size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
     int64_t max_chunks;  // chunked raster path (0 if unused)
     size_t chunk_base, chunk_tile, chunk_bwd;

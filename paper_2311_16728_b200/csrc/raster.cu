@@ -143,10 +143,10 @@ struct RasterSmem {
 
 // CTA = WARPS warps of one 16x16 tile: blockIdx.x = tile_x * (8 / WARPS) + sub-tile.
 template <int WARPS>
-__device__ __forceinline__ void warp_block(int &tile_x, int &wx0, int &wy0, int &lx, int &ly) {
+__device__ __forceinline__ void warp_block(int bxi, int &tile_x, int &wx0, int &wy0, int &lx, int &ly) {
     constexpr int SUB = 8 / WARPS;
-    const int sub = blockIdx.x % SUB;
-    tile_x = blockIdx.x / SUB;
+    const int sub = bxi % SUB;
+    tile_x = bxi / SUB;
     const int wg = sub * WARPS + (threadIdx.x >> 5);  // warp block index 0..7 within the tile
     const int lane = threadIdx.x & 31;
     wx0 = (wg & 1) * 8;
@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                                                            float *__restrict__ T_keep, uint32_t *__restrict__ ncontrib,
                                                            uint32_t *__restrict__ ncomp,
                                                            const uint32_t *__restrict__ chunk_base,
-                                                           float4 *__restrict__ chunk_bwd) {
+                                                           float4 *__restrict__ chunk_bwd,
+                                                           const uint32_t *__restrict__ order) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     constexpr int NT = WARPS * 32;
@@ -216,15 +217,23 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     constexpr int NSEG = BATCH / SEG;
     __shared__ __align__(16) uint8_t wl[WARPS][BATCH];  // segment s's selection at [s * SEG, ...)
     __shared__ int segn[WARPS][NSEG];
-    const int view = blockIdx.z;
+    // one CTA per tile (WARPS == 8) takes its tile from the longest-first order (shorter lists
+    // end the kernel: less tail); otherwise blockIdx decides
+    int view = blockIdx.z, tile_y = blockIdx.y, bxi = blockIdx.x;
+    if (WARPS == 8 && order) {
+        const uint32_t gt = order[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+        view = gt / tiles;
+        tile_y = (gt % tiles) / TX;
+        bxi = (gt % tiles) % TX;
+    }
     int tile_x, bx0, by0, lx, ly;
-    warp_block<WARPS>(tile_x, bx0, by0, lx, ly);
-    const int tile = blockIdx.y * TX + tile_x;
+    warp_block<WARPS>(bxi, tile_x, bx0, by0, lx, ly);
+    const int tile = tile_y * TX + tile_x;
     const int tid = threadIdx.x;
     const int px = tile_x * TILE + lx;
-    const int py = blockIdx.y * TILE + ly;
+    const int py = tile_y * TILE + ly;
     const float wx0 = (float)(tile_x * TILE + bx0);
-    const float wy0 = (float)(blockIdx.y * TILE + by0);
+    const float wy0 = (float)(tile_y * TILE + by0);
     const bool inside = px < W && py < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const int todo_all = (int)(range.y - range.x);
@@ -481,19 +490,26 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
                                                      const float *__restrict__ dL_drgb,
                                                      const float *__restrict__ T_keep,
                                                      const uint32_t *__restrict__ ncontrib,
-                                                     float4 *__restrict__ g2d) {
+                                                     float4 *__restrict__ g2d, const uint32_t *__restrict__ order) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ __align__(128) RasterSmem S;
     __shared__ uint8_t wl[4][BATCH];
     __shared__ uint32_t s_maxlast;
-    const int view = blockIdx.z;
-    const int tile = blockIdx.y * TX + blockIdx.x;
+    // tiles in longest-list-first order (less tail); blockIdx decides without an order
+    int view = blockIdx.z, ty = blockIdx.y, tx = blockIdx.x;
+    if (order) {
+        const uint32_t gt = order[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+        view = gt / tiles;
+        ty = (gt % tiles) / TX;
+        tx = (gt % tiles) % TX;
+    }
+    const int tile = ty * TX + tx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
-    const int px = blockIdx.x * TILE + bx + (lane & 7);
-    const int pyA = blockIdx.y * TILE + by + (lane >> 3), pyB = pyA + 4;
-    const float wx0 = (float)(blockIdx.x * TILE + bx), wy0 = (float)(blockIdx.y * TILE + by);
+    const int px = tx * TILE + bx + (lane & 7);
+    const int pyA = ty * TILE + by + (lane >> 3), pyB = pyA + 4;
+    const float wx0 = (float)(tx * TILE + bx), wy0 = (float)(ty * TILE + by);
     const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const float fx = (float)px;
@@ -673,6 +689,48 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
     }
 }
 
+// (view, tile) indices ordered by decreasing list length (bucketed by length / 8): launched in
+// this order the long tiles start first and the short ones fill the end of the kernel.
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ ranges, int VT,
+                                                     uint32_t *__restrict__ order) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
+    __shared__ uint32_t hist[256];
+    const int tid = threadIdx.x;
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    for (int t = tid; t < VT; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        atomicAdd(&hist[255 - min(255u, (r.y - r.x) >> 3)], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 256 bucket counts by one warp
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = hist[tid * 8 + k];
+            s += v[k];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += u;
+        }
+        uint32_t run = incl - s;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            hist[tid * 8 + k] = run;
+            run += v[k];
+        }
+    }
+    __syncthreads();
+    for (int t = tid; t < VT; t += blockDim.x) {
+        const uint2 r = ranges[t];
+        order[atomicAdd(&hist[255 - min(255u, (r.y - r.x) >> 3)], 1u)] = (uint32_t)t;
+    }
+}
+
 // Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
 // tile) at pyramid levels with few tiles so that every SM gets work.
 static int raster_warps(const Layout &L) {
@@ -700,12 +758,12 @@ cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s) {
 
 template <int WARPS>
 static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
-                       const uint32_t *cbase, float4 *cbwd, cudaStream_t s) {
+                       const uint32_t *cbase, float4 *cbwd, const uint32_t *order, cudaStream_t s) {
     dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
     auto kern = cbwd ? k_raster_fwd<WARPS, true> : k_raster_fwd<WARPS, false>;
     launch_pdl(kern, grid, WARPS * 32, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX, L.tiles, bg[0],
                                      bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
-                                     at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd);
+                                     at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd, order);
 }
 
 
@@ -720,10 +778,16 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
         cbase = at<uint32_t>(ws, L.chunk_base);
         cbwd = at<float4>(ws, L.chunk_bwd);
     }
+    const uint32_t *order = nullptr;
+    if (L.max_chunks == 0) {  // many tiles: longest lists first, for this forward and the backward
+        launch_pdl(k_tile_order, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
+                   at<uint32_t>(ws, L.tile_order));
+        order = at<uint32_t>(ws, L.tile_order);
+    }
     switch (raster_warps(L)) {
-        case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
-        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
-        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, s); break;
+        case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
+        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, nullptr, s); break;
+        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, nullptr, s); break;
     }
     return cudaGetLastError();
 }
@@ -741,7 +805,7 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
     dim3 grid(L.TX, L.TY, L.V);
     launch_pdl(k_raster_bwd2, grid, 128, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
                                        L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
-                                       at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d));
+                                       at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d), at<uint32_t>(ws, L.tile_order));
     return cudaGetLastError();
 }
 

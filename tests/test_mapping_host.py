@@ -45,9 +45,9 @@ def test_pack_unpack_roundtrip():
 def test_launch_accounting_matches_design():
     import bench
     # bucket binning: preprocess, scan, scatter, short + long tile sorts (with the record gather),
-    # raster, 2 loss, 3 fused bwd (+ chunk index on levels with few tiles)
-    assert bench.launches_per_iteration(43, True) == 11
+    # chunk index or tile order, raster, 2 loss, 3 fused bwd
+    assert bench.launches_per_iteration(43, True) == 12
     assert bench.launches_per_iteration(43, True, chunked=True) == 12
-    assert bench.launches_per_iteration(43, False) == 12
+    assert bench.launches_per_iteration(43, False) == 13
     # radix binning, 43 key bits -> 6 digit passes, + separate gather
-    assert bench.launches_per_iteration(43, True, binning=1) == 2 + (4 + 6 + 1) + 1 + 2 + 3
+    assert bench.launches_per_iteration(43, True, binning=1) == 2 + (4 + 6 + 1) + 1 + 1 + 2 + 3
