@@ -183,8 +183,8 @@ def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
     binning 0: bucket scatter, short- and long-bucket tile sorts with the pair-record gather (3) /
     binning 1: duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, pair gather
-    (5 + passes); raster fwd (1) after the chunk index (levels with few tiles, chunked raster path)
-    or the longest-first tile order (other levels) (1);
+    (5 + passes); raster fwd (1) after the longest-first tile order or, on levels with few tiles
+    (chunked raster path), the chunk index (1);
     loss (2); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
     binning_kernels = 3 if binning == 0 else 5 + passes

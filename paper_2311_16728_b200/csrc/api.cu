@@ -69,6 +69,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.max_chunks = use_chunked((int64_t)V * L.tiles) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;
     L.chunk_base = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.chunk_tile = take((size_t)std::max<int64_t>(L.max_chunks, 1) * sizeof(uint32_t));
+    L.chunk_order = take((size_t)std::max<int64_t>(L.max_chunks, 1) * sizeof(uint32_t));
     L.chunk_bwd = take((size_t)L.max_chunks * TILE_PIX * sizeof(float4));
     L.sort_look = take((size_t)SORT_MAX_PASSES * std::max<int64_t>(L.sort_blocks, 1) * SORT_RADIX * sizeof(uint32_t));
     L.total = o;

@@ -66,7 +66,7 @@ struct Layout {
     size_t tile_order;  // (view, tile) indices, longest list first (raster.cu)
     size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
     int64_t max_chunks;  // chunked raster path (0 if unused)
-    size_t chunk_base, chunk_tile, chunk_bwd;
+    size_t chunk_base, chunk_tile, chunk_bwd, chunk_order;
     size_t keys0, keys1, vals0, vals1, sort_look, ranges, ncontrib, ncomp, Tfinal, total;
 };
 

@@ -217,14 +217,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     constexpr int NSEG = BATCH / SEG;
     __shared__ __align__(16) uint8_t wl[WARPS][BATCH];  // segment s's selection at [s * SEG, ...)
     __shared__ int segn[WARPS][NSEG];
-    // one CTA per tile (WARPS == 8) takes its tile from the longest-first order (shorter lists
-    // end the kernel: less tail); otherwise blockIdx decides
+    // tiles in longest-list-first order (shorter lists end the kernel: less tail); without an
+    // order blockIdx decides
     int view = blockIdx.z, tile_y = blockIdx.y, bxi = blockIdx.x;
-    if (WARPS == 8 && order) {
-        const uint32_t gt = order[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+    if (order) {
+        constexpr int SUB = 8 / WARPS;  // CTAs per tile
+        const int64_t lin = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const uint32_t gt = order[lin / SUB];
         view = gt / tiles;
         tile_y = (gt % tiles) / TX;
-        bxi = (gt % tiles) % TX;
+        bxi = (int)((gt % tiles) % TX) * SUB + (int)(lin % SUB);
     }
     int tile_x, bx0, by0, lx, ly;
     warp_block<WARPS>(bxi, tile_x, bx0, by0, lx, ly);
@@ -388,7 +390,8 @@ __device__ __forceinline__ float warp_sum8_transposed(float a[8], int lane) {
 
 __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ ranges, int VT,
                                                       uint32_t *__restrict__ chunk_base,
-                                                      uint32_t *__restrict__ chunk_tile, WsHeader *hdr,
+                                                      uint32_t *__restrict__ chunk_tile,
+                                                      uint32_t *__restrict__ chunk_order, WsHeader *hdr,
                                                       int64_t max_chunks) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
@@ -412,6 +415,39 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
     if (t == 1023) hdr->nchunks = (uint32_t)min((int64_t)s[1023], max_chunks);
     for (uint32_t k = 0; k < nch; k++)
         if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
+    // chunk order for the backward: by position in the tile list, first chunks first (most
+    // pixels are still active there: the longest replays start first)
+    __syncthreads();
+    uint32_t *cnt = s;  // reuse: [0, 256) counts per position class, then running offsets
+    if (t < 256) cnt[t] = 0;
+    __syncthreads();
+    for (uint32_t k = 0; k < nch; k++) atomicAdd(&cnt[min(k, 255u)], 1u);
+    __syncthreads();
+    if (t < 32) {  // exclusive scan of the 256 class counts by one warp
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            v[k] = cnt[t * 8 + k];
+            sum += v[k];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (t >= o) incl += u;
+        }
+        uint32_t run = incl - sum;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            cnt[t * 8 + k] = run;
+            run += v[k];
+        }
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < nch; k++) {
+        const uint32_t pos = atomicAdd(&cnt[min(k, 255u)], 1u);
+        if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
+    }
 }
 
 // ================================================================ two-pixel packed backward
@@ -601,14 +637,15 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
                                                            const float *__restrict__ dL_drgb,
                                                            const uint32_t *__restrict__ ncontrib,
                                                            const float4 *__restrict__ chunk_bwd,
-                                                           float4 *__restrict__ g2d) {
+                                                           float4 *__restrict__ g2d,
+                                                           const uint32_t *__restrict__ chunk_order) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ __align__(128) float4 rec[CHUNK * 3];
     __shared__ uint64_t bar;
     __shared__ uint8_t wl[4][CHUNK];
-    const int c = blockIdx.x;
-    if (c >= (int)hdr->nchunks) return;
+    if ((int)blockIdx.x >= (int)hdr->nchunks) return;
+    const int c = chunk_order[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t gt = chunk_tile[c];
     const int view = gt / tiles, tl = gt % tiles;
@@ -773,21 +810,24 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
     uint32_t *cbase = nullptr;
     float4 *cbwd = nullptr;
     if (L.max_chunks > 0) {  // few tiles: record per-chunk state for the chunk-parallel backward
-        launch_pdl(k_chunk_index, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles, at<uint32_t>(ws, L.chunk_base),
-                                         at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.max_chunks);
+        launch_pdl(k_chunk_index, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
+                   at<uint32_t>(ws, L.chunk_base), at<uint32_t>(ws, L.chunk_tile), at<uint32_t>(ws, L.chunk_order),
+                   at<WsHeader>(ws, L.hdr), L.max_chunks);
         cbase = at<uint32_t>(ws, L.chunk_base);
         cbwd = at<float4>(ws, L.chunk_bwd);
     }
+    // many tiles: longest tile lists first, for this forward and the backward (the chunked levels
+    // order their backward chunks in k_chunk_index instead)
     const uint32_t *order = nullptr;
-    if (L.max_chunks == 0) {  // many tiles: longest lists first, for this forward and the backward
+    if (L.max_chunks == 0) {
         launch_pdl(k_tile_order, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
                    at<uint32_t>(ws, L.tile_order));
         order = at<uint32_t>(ws, L.tile_order);
     }
     switch (raster_warps(L)) {
         case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
-        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, nullptr, s); break;
-        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, nullptr, s); break;
+        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
+        default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
     }
     return cudaGetLastError();
 }
@@ -798,7 +838,8 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
         launch_pdl(k_raster_bwd2_chunk, (unsigned)L.max_chunks, 128, 0, s, 
             at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
             at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
-            at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d));
+            at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d),
+            at<uint32_t>(ws, L.chunk_order));
         return cudaGetLastError();
     }
     // many tiles: two pixels per lane, packed fp32x2

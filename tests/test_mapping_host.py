@@ -45,7 +45,7 @@ def test_pack_unpack_roundtrip():
 def test_launch_accounting_matches_design():
     import bench
     # bucket binning: preprocess, scan, scatter, short + long tile sorts (with the record gather),
-    # chunk index or tile order, raster, 2 loss, 3 fused bwd
+    # tile order or chunk index, raster, 2 loss, 3 fused bwd
     assert bench.launches_per_iteration(43, True) == 12
     assert bench.launches_per_iteration(43, True, chunked=True) == 12
     assert bench.launches_per_iteration(43, False) == 13
