@@ -313,11 +313,38 @@ class MappingEngine:
     def replay(self):
         self.graph.replay()
 
-    def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor):
+    def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor,
+                  next_gts_pinned: torch.Tensor | None = None):
         """End-to-end public API: new keyframe targets from pinned host memory (H2D), A0,
-        the Eq. 5 pass, per-level losses back to pinned host memory (D2H)."""
-        self.gt0.copy_(gts_pinned, non_blocking=True)
+        the Eq. 5 pass, per-level losses back to pinned host memory (D2H).
+
+        next_gts_pinned: the targets of the NEXT call, copied on a copy stream into a second
+        device buffer while this step computes (double buffering); the next call then starts
+        from them instead of copying gts_pinned.  Every call still moves its targets host->device
+        and its losses device->host."""
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_staged", None) is not None:  # prefetched by the previous call
+            buf, ev = self._staged
+            cur.wait_event(ev)
+            self._gt_spare, self.gt0 = self.gt0, buf
+            self._staged = None
+        else:
+            self.gt0.copy_(gts_pinned, non_blocking=True)
         self.build_pyramids(overlap=True)
+        if next_gts_pinned is not None:
+            if getattr(self, "_copy_stream", None) is None:
+                self._copy_stream = torch.cuda.Stream(device=self.gt0.device)
+            if getattr(self, "_gt_spare", None) is None:
+                self._gt_spare = torch.empty_like(self.gt0)
+            free = torch.cuda.Event()
+            free.record(cur)  # the spare buffer's last reader (the previous step) is queued before this
+            self._copy_stream.wait_event(free)
+            with torch.cuda.stream(self._copy_stream):
+                self._gt_spare.copy_(next_gts_pinned, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record()
+            self._staged = (self._gt_spare, done)
+            self._gt_spare = None
         losses = self.step()
         out_pinned.copy_(torch.stack(losses), non_blocking=True)
         return out_pinned
