@@ -23,7 +23,6 @@
 
 namespace gsk {
 
-constexpr int TS_SMEM_KEYS = 4096;  // 32 KB of u64 keys per CTA
 
 // One thread per visible Gaussian (compacted list).  When the V*tiles table fits in shared
 // memory, a CTA first counts its pairs per tile there, reserves each tile's sub-range with one
@@ -84,26 +83,6 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
     }
 }
 
-// Bitonic network over `len` (power of two) keys at `a`, CTA-wide: every stage is len/2
-// compare-exchanges indexed by pair q (no idle lanes), separated by barriers.
-__device__ __forceinline__ void bitonic(uint64_t *a, int len) {
-    const int half = len >> 1;
-    for (int k = 2; k <= len; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int q = threadIdx.x; q < half; q += blockDim.x) {
-                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
-                const int p = i + j;
-                uint64_t x = a[i], y = a[p];
-                const bool up = (i & k) == 0;
-                if ((x > y) == up) {
-                    a[i] = y;
-                    a[p] = x;
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
 
 // ---- group bitonic sort: a group of W warps holds lp = 32 E W keys in registers; key g (its
 // bitonic index) = w * 32 E + e * 32 + lane (striped, so loads and stores coalesce).  Distances
@@ -160,30 +139,25 @@ struct RecSrc {  // per-(view, Gaussian) record sources for the fused pair-recor
     int64_t vbase;  // view * n of the bucket's view
 };
 
+// One merge step k of the network on the window of LP = 32 E W keys held in registers (x, key
+// (base + gw + e * 32 + lane)), for the distances j = min(k / 2, LP / 2) ... 1: j >= 32 E through
+// shared memory (group barrier per stage), j < 32 E in registers.  base is the window's offset in
+// the whole (padded) bucket; directions use the global index, so windows compose into one network.
 template <int E, int W>
-__device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len,
-                                           uint64_t hi, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
-                                           uint64_t *sk, int gt_idx, int bar_id, const RecSrc &rs) {
+__device__ __forceinline__ void merge_window(uint64_t (&x)[E], uint64_t *sk, int gt_idx, int bar_id, int base, int k) {
     constexpr int LP = 32 * E * W, NTH = 32 * W;
     const int lane = gt_idx & 31;
     const int gw = (gt_idx >> 5) * 32 * E;
-    uint64_t x[E];
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const uint32_t g = gw + e * 32 + lane;
-        x[e] = g < len ? tmp[start + g] : ~0ull;
-    }
-    sort_regs<E, 2>(x, lane, gw);
-    for (int k = 64 * E; k <= LP; k <<= 1) {
+    if (k >= 64 * E) {
 #pragma unroll
         for (int e = 0; e < E; e++) sk[gw + e * 32 + lane] = x[e];
         group_bar(bar_id, NTH);
-        for (int j = k >> 1; j >= 32 * E; j >>= 1) {
+        for (int j = min(k, LP) >> 1; j >= 32 * E; j >>= 1) {
             for (int q = gt_idx; q < LP / 2; q += NTH) {
                 const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
                 const int p = i + j;
                 const uint64_t a = sk[i], c = sk[p];
-                if ((a > c) == ((i & k) == 0)) {
+                if ((a > c) == (((base + i) & k) == 0)) {
                     sk[i] = c;
                     sk[p] = a;
                 }
@@ -192,23 +166,110 @@ __device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uin
         }
 #pragma unroll
         for (int e = 0; e < E; e++) x[e] = sk[gw + e * 32 + lane];
-        merge_regs<E, 16 * E>(x, lane, gw, k);
-        group_bar(bar_id, NTH);  // sk is rewritten by the next round
-    }
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        const uint32_t g = gw + e * 32 + lane;
-        if (g < len) {
-            const uint32_t gi = (uint32_t)x[e];
-            vals[start + g] = gi;
-            keys[start + g] = hi | (x[e] >> 32);
-            write_pair_record(rs.prec, start + g, rs.rec0, rs.rec1, rs.rec2, rs.vbase + gi, gi);
-        }
+        merge_regs<E, 16 * E>(x, lane, base + gw, k);
+        group_bar(bar_id, NTH);  // sk is rewritten by the next step
+    } else {
+        merge_regs<E, 16 * E>(x, lane, base + gw, k);  // (only reached with k < 64 E from sort_window)
     }
 }
 
+// Sort the window (merge steps k = 2 .. LP) in place in registers.
+template <int E, int W>
+__device__ __forceinline__ void sort_window(uint64_t (&x)[E], uint64_t *sk, int gt_idx, int bar_id, int base) {
+    constexpr int LP = 32 * E * W;
+    const int lane = gt_idx & 31;
+    const int gw = (gt_idx >> 5) * 32 * E;
+    sort_regs<E, 2>(x, lane, base + gw);  // k = 2 .. 32 E
+    for (int k = 64 * E; k <= LP; k <<= 1) merge_window<E, W>(x, sk, gt_idx, bar_id, base, k);
+}
+
+__device__ __forceinline__ void emit_pair(uint64_t k, uint32_t pos, uint64_t hi, uint64_t *keys, uint32_t *vals,
+                                          const RecSrc &rs) {
+    const uint32_t gi = (uint32_t)k;
+    vals[pos] = gi;
+    keys[pos] = hi | (k >> 32);
+    write_pair_record(rs.prec, pos, rs.rec0, rs.rec1, rs.rec2, rs.vbase + gi, gi);
+}
+
+// Sort the bucket tmp[start, start + len) (len <= 32 E W) with a group of W warps (group-local
+// thread index gt_idx, named barrier bar_id; sk = 32 E W keys of shared memory) and write the
+// sorted values, full keys (hi | depth bits) and pair records.
+template <int E, int W>
+__device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len,
+                                           uint64_t hi, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                                           uint64_t *sk, int gt_idx, int bar_id, const RecSrc &rs) {
+    const int lane = gt_idx & 31;
+    const int gw = (gt_idx >> 5) * 32 * E;
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t g = gw + e * 32 + lane;
+        x[e] = g < len ? tmp[start + g] : ~0ull;
+    }
+    sort_window<E, W>(x, sk, gt_idx, bar_id, 0);
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t g = gw + e * 32 + lane;
+        if (g < len) emit_pair(x[e], start + g, hi, keys, vals, rs);
+    }
+}
+
+// A bucket longer than one window (LP = 32 E W keys): the same network on the padded bucket in
+// global scratch g (its own region of the overflow buffer): every LP-window sorted in registers
+// / shared memory, then each merge step k > LP as its global stages j >= LP followed by one
+// register / shared-memory pass per window for j < LP.
+template <int E, int W>
+__device__ void long_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len, uint64_t hi,
+                          uint64_t *__restrict__ keys, uint32_t *__restrict__ vals, uint64_t *sk, uint64_t *g,
+                          int gt_idx, const RecSrc &rs) {
+    constexpr int LP = 32 * E * W, NTH = 32 * W;
+    const int lane = gt_idx & 31;
+    const int gw = (gt_idx >> 5) * 32 * E;
+    int lp = LP;
+    while (lp < (int)len) lp <<= 1;
+    uint64_t x[E];
+    for (int base = 0; base < lp; base += LP) {
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const uint32_t i = base + gw + e * 32 + lane;
+            x[e] = i < len ? tmp[start + i] : ~0ull;
+        }
+        sort_window<E, W>(x, sk, gt_idx, 1, base);
+#pragma unroll
+        for (int e = 0; e < E; e++) g[base + gw + e * 32 + lane] = x[e];
+    }
+    __threadfence_block();
+    __syncthreads();
+    for (int k = 2 * LP; k <= lp; k <<= 1) {
+        for (int j = k >> 1; j >= LP; j >>= 1) {
+            for (int q = gt_idx; q < lp / 2; q += NTH) {
+                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+                const int p = i + j;
+                const uint64_t a = g[i], c = g[p];
+                if ((a > c) == ((i & k) == 0)) {
+                    g[i] = c;
+                    g[p] = a;
+                }
+            }
+            __threadfence_block();
+            __syncthreads();
+        }
+        for (int base = 0; base < lp; base += LP) {
+#pragma unroll
+            for (int e = 0; e < E; e++) x[e] = g[base + gw + e * 32 + lane];
+            merge_window<E, W>(x, sk, gt_idx, 1, base, k);
+#pragma unroll
+            for (int e = 0; e < E; e++) g[base + gw + e * 32 + lane] = x[e];
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+    for (int i = gt_idx; i < (int)len; i += NTH) emit_pair(g[i], start + i, hi, keys, vals, rs);
+}
+
 constexpr int SG_WARPS = 2;   // warps of the small-bucket CTA (<= 256 pairs)
-constexpr int BG_WARPS = 16;  // warps of the long-bucket CTA (<= 4096 pairs)
+constexpr int BG_WARPS = 16;   // warps of the long-bucket CTA (<= 4096 pairs)
+constexpr int BG_MAX = 4096;    // longest bucket sorted in one register / shared-memory window
 
 // Pass 1: one 2-warp CTA per (view, tile) (tile = blockIdx.x, so every branch below is provably
 // uniform and the shuffles need no warp re-convergence).  Writes the range; sorts buckets of
@@ -235,19 +296,16 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_tile_sort_small(
     else if (threadIdx.x == 0) big_tiles[atomicAdd(&hdr->n_big, 1u)] = (uint32_t)gt;
 }
 
-// Pass 2: one CTA per queued bucket (grid-stride).  Buckets beyond 4096 pairs use the plain
-// network in global memory.
-__global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t *__restrict__ tile_start,
-                                                                 const uint32_t *__restrict__ tile_count,
-                                                                 const uint64_t *__restrict__ tmp,
-                                                                 uint64_t *__restrict__ keys,
-                                                                 uint32_t *__restrict__ vals,
-                                                                 const uint32_t *__restrict__ big_tiles,
-                                                                 uint64_t *__restrict__ big, const WsHeader *hdr,
-                                                                 RecSrc rs, int64_t n, int tiles) {
+// Pass 2: one CTA of 16 warps per queued bucket (grid-stride): up to 4096 pairs in registers and
+// shared memory, longer buckets with long_sort (4096-pair windows + global merge stages).
+__global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(
+    const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, const uint64_t *__restrict__ tmp,
+    uint64_t *__restrict__ keys, uint32_t *__restrict__ vals, const uint32_t *__restrict__ big_tiles,
+    uint64_t *__restrict__ big, const WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
-    __shared__ uint64_t sk[TS_SMEM_KEYS];
+    constexpr int W = BG_WARPS;
+    __shared__ __align__(16) uint64_t sk[BG_MAX];
     const uint32_t nb = hdr->n_big;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
         const uint32_t gt = big_tiles[b];
@@ -255,27 +313,12 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(const uint32_t 
         const uint32_t len = tile_count[(size_t)gt * CNT_STRIDE];
         const uint64_t hi = (uint64_t)gt << 32;
         rs.vbase = (int64_t)(gt / tiles) * n;
-        if (len <= 512) group_sort<1, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-        else if (len <= 1024) group_sort<2, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-        else if (len <= 2048) group_sort<4, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-        else if (len <= 4096) group_sort<8, BG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-        else {
-            // very long bucket: on a padded copy in this bucket's own region
-            // [2*start, 2*start + 2*len) of the overflow buffer (lp <= 2*len; disjoint per bucket)
-            int lp = 1;
-            while (lp < (int)len) lp <<= 1;
-            uint64_t *g = big + 2 * (size_t)start;
-            for (int i = threadIdx.x; i < lp; i += blockDim.x) g[i] = i < (int)len ? tmp[start + i] : ~0ull;
-            __threadfence_block();
-            __syncthreads();
-            bitonic(g, lp);
-            for (int i = threadIdx.x; i < (int)len; i += blockDim.x) {
-                const uint32_t gi = (uint32_t)g[i];
-                vals[start + i] = gi;
-                keys[start + i] = hi | (g[i] >> 32);
-                write_pair_record(rs.prec, start + i, rs.rec0, rs.rec1, rs.rec2, rs.vbase + gi, gi);
-            }
-        }
+        if (len <= 512) group_sort<1, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= 1024) group_sort<2, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= 2048) group_sort<4, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else if (len <= BG_MAX) group_sort<8, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
+        else  // padded copy in this bucket's own region [2 start, 2 start + 2 len) of the overflow buffer
+            long_sort<8, W>(tmp, start, len, hi, keys, vals, sk, big + 2 * (size_t)start, threadIdx.x, rs);
         __syncthreads();
     }
 }
@@ -297,20 +340,21 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
     ProfScope prof("k_tile_sort", s);
     const RecSrc rs{at<float4>(ws, L.rec0), at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), at<float4>(ws, L.prec), 0};
-    launch_pdl(k_tile_sort_small, (unsigned)VT, SG_WARPS * 32, 0, s, 
-        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), L.cap, at<uint64_t>(ws, L.keys1),
-        at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.big_tiles),
-        at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
+    launch_pdl(k_tile_sort_small, (unsigned)VT, SG_WARPS * 32, 0, s,
+               at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), L.cap, at<uint64_t>(ws, L.keys1),
+               at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges),
+               at<uint32_t>(ws, L.big_tiles), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT, 2 * sms), BG_WARPS * 32, 0, s, 
-        at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
-        at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
-        at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
+    // 16-warp CTAs: up to 4 resident per SM
+    launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT, 4 * sms), BG_WARPS * 32, 0, s,
+               at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
+               at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
+               at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
     return cudaGetLastError();
 }
 

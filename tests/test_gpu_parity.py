@@ -155,12 +155,12 @@ def _check_colour(got_rgb, got_T, ref, pixels_mask=None):
     assert d[flag].max(initial=0) <= 1.1e-2
 
 
-def test_long_tile_bucket_global_fallback():
-    """A tile list longer than the in-tile shared-memory sort (4096 pairs) takes the global-memory
-    network; it must still match the oracle's binning exactly."""
+@pytest.mark.parametrize("n", [6000, 12000, 20000])
+def test_long_tile_bucket_sorts(n):
+    """Tile lists longer than one 4096-pair window are sorted window by window with global merge
+    stages in between (2, 3 and 5 windows here); they must match the oracle's binning exactly."""
     from tests.helpers import camera, scene_of
     rng = np.random.default_rng(5)
-    n = 6000
     means = np.stack([rng.uniform(-0.02, 0.02, n), rng.uniform(-0.02, 0.02, n), rng.uniform(1.0, 3.0, n)], 1)
     scene = scene_of(means, log_scales=np.full((n, 3), np.log(0.002)), D=0)
     scene.depth_ties = None
