@@ -220,21 +220,23 @@ __global__ void __launch_bounds__(COL_THREADS) k_adam_fused(float *__restrict__ 
     for (int row = r0; row < r1; row++) {
         const float lr = a.lr[row_class(row)];
         const int64_t q = (int64_t)row * (ld / 4) + c4;
+        // m and v are streamed (evict-first loads and stores), so the updated parameters -- read
+        // again by the next iteration's projection -- tend to stay in L2
         float4 p = reinterpret_cast<float4 *>(P)[q];
-        float4 m = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4 *>(Mm)[q];
-        float4 v = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<float4 *>(Vv)[q];
+        float4 m = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcs(reinterpret_cast<float4 *>(Mm) + q);
+        float4 v = a.sgd ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldcs(reinterpret_cast<float4 *>(Vv) + q);
         const float *Sr = S + (int64_t)row * n;
         float g[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) g[k] = sl[k] != 0xFFFFFFFFu ? Sr[sl[k]] : 0.f;
+        for (int k = 0; k < 4; k++) g[k] = sl[k] != 0xFFFFFFFFu ? __ldcs(Sr + sl[k]) : 0.f;
         float *pp = &p.x, *mm = &m.x, *vv = &v.x;
 #pragma unroll
         for (int k = 0; k < 4; k++)
             if (i0 + k < n) adam1(pp[k], g[k], mm[k], vv[k], lr, a);
         reinterpret_cast<float4 *>(P)[q] = p;
         if (!a.sgd) {
-            reinterpret_cast<float4 *>(Mm)[q] = m;
-            reinterpret_cast<float4 *>(Vv)[q] = v;
+            __stcs(reinterpret_cast<float4 *>(Mm) + q, m);
+            __stcs(reinterpret_cast<float4 *>(Vv) + q, v);
         }
     }
 }
