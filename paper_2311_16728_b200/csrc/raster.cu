@@ -40,6 +40,7 @@ constexpr float ALPHA_MIN = 1.0f / 255.0f;
 constexpr float T_STOP = 1e-4f;
 constexpr float POWER_CUT = -4.5f;
 constexpr int BATCH = 256;  // records per staged batch (list indices fit in a byte)
+constexpr int FEW_CHUNK = 5;  // chunked backward: per-lane atomics for entries with <= 5 contributing lanes
 
 // power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order
 __device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float C, float &dx, float &dy) {
@@ -474,6 +475,8 @@ struct Pix2 {
 // recover T before it, dL/dalpha = T sum_c g_c (c - acc), then the gradient moments
 // S(a), S(b), S(a dx), S(a dy), S(b dy) with a = dL/dpower dx, b = dL/dpower dy, dL/dsigma and
 // dL/dcolour summed over the warp and added to the Gaussian's per-view record.
+// FEW: at most this many contributing lanes -> per-lane atomics instead of the warp reduction
+template <int FEW>
 __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint32_t position, float fx,
                                            float2 fy2, int lane, int64_t vbase, float4 *g2d) {
     const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
@@ -512,10 +515,20 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
     const float2 qc = __fmul2_rn(b2, dy2);
     float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
                       qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
-    const float mine = warp_sum8_transposed(vals8, lane);
-    const float bsum = warp_sum(db.x + db.y);
     const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
     float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
+    if (FEW > 0 && __popc(__ballot_sync(0xffffffffu, vA || vB)) <= FEW) {
+        // few contributing lanes (an entry touching the block's edge): their own atomics are
+        // cheaper than the warp reduction
+        if (vA || vB) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) atomicAdd(dst + k, vals8[k]);
+            atomicAdd(dst + 8, db.x + db.y);
+        }
+        return;
+    }
+    const float mine = warp_sum8_transposed(vals8, lane);
+    const float bsum = warp_sum(db.x + db.y);
     if ((lane & 3) == 0) atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
     if (lane == 1) atomicAdd(dst + 8, bsum);
 }
@@ -621,7 +634,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         __syncwarp();
         for (int t = 0; t < nsel; t++) {
             const int j = wl[warp][t];
-            bwd2_entry(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, vbase, g2d);
+            bwd2_entry<2>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, vbase, g2d);
         }
     }
 }
@@ -722,7 +735,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
     const int64_t vbase = (int64_t)view * n;
     for (int t = 0; t < nsel; t++) {
         const int j = wl[warp][t];
-        bwd2_entry(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, vbase, g2d);
+        bwd2_entry<FEW_CHUNK>(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, vbase, g2d);
     }
 }
 
