@@ -177,18 +177,22 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 CHUNK_MAX_TILES = 600  # views x tiles below this use the chunked raster path (gs_internal.cuh)
+FUSED_SCHEDULE_TILES = 8192  # views x tiles up to this: one-CTA tile scan + schedule (raster.cu)
 
 
-def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked: bool = False) -> int:
+def launches_per_iteration(key_bits: int, fused: bool, binning: int = 0, chunked: bool = False,
+                           view_tiles: int = 0) -> int:
     """Kernels libgs.so launches per mapping iteration (api.cu sequencing): preprocess + scan (2);
     binning 0: bucket scatter, short- and long-bucket tile sorts with the pair-record gather (3) /
     binning 1: duplicate, sort histogram, one pass per 8-bit digit, fixup, ranges, pair gather
-    (5 + passes); raster fwd (1) after the longest-first tile order or, on levels with few tiles
-    (chunked raster path), the chunk index (1);
-    loss (2); fused: raster bwd + preprocess bwd + Adam (3), else + gradient accumulate (4)."""
+    (5 + passes); raster fwd (1); the raster schedule (chunk index on levels with few tiles, else
+    the longest-first tile order) (1) -- built inside the bucket path's tile scan when
+    views x tiles <= 8192 (0); loss (2); fused: raster bwd + preprocess bwd + Adam (3), else +
+    gradient accumulate (4)."""
     passes = (key_bits + 7) // 8
     binning_kernels = 3 if binning == 0 else 5 + passes
-    return 2 + binning_kernels + 1 + 1 + 2 + (3 if fused else 4)
+    schedule = 0 if binning == 0 and view_tiles <= FUSED_SCHEDULE_TILES else 1
+    return 2 + binning_kernels + 1 + schedule + 2 + (3 if fused else 4)
 
 
 def run_ours(args):
@@ -421,7 +425,7 @@ def run_ours(args):
     for r in eng.renderers:
         t = r.ws.tiles_x * r.ws.tiles_y * len(cams)
         bits = 32 + max(1, math.ceil(math.log2(max(t, 2))))
-        launches_step += launches_per_iteration(bits, world == 1, chunked=t < CHUNK_MAX_TILES)
+        launches_step += launches_per_iteration(bits, world == 1, chunked=t < CHUNK_MAX_TILES, view_tiles=t)
     launches = args.steps * launches_step
 
     cpu = None

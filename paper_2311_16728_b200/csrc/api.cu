@@ -221,7 +221,9 @@ gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t 
         cudaMemsetAsync(at<char>(ws, L.tile_count), 0, (size_t)n_views * L.tiles * CNT_STRIDE * sizeof(uint32_t), s);
     cudaError_t e = launch_preprocess(*params, cb, n_views, L, ws, buckets, s);
     if (e == cudaSuccess) {
-        if (buckets)  // tile ranges straight from the per-tile counts
+        if (buckets && fused_tile_schedule(L))  // tile starts + raster schedule, one CTA
+            e = launch_tile_scan(L, ws, s);
+        else if (buckets)  // tile ranges straight from the per-tile counts
             e = launch_scan_u32(at<uint32_t>(ws, L.tile_count), at<uint32_t>(ws, L.tile_start),
                                 (int64_t)n_views * L.tiles, at<uint64_t>(ws, L.scan_flags), hdr, s, CNT_STRIDE);
         else  // pair offsets of every (view, Gaussian) for key duplication
@@ -264,7 +266,7 @@ gs_status gs_render_forward(const gs_params *params, const gs_camera *cams, int3
         if (e == cudaSuccess) e = launch_ranges(L, ws, s);
         if (e == cudaSuccess) e = launch_gather_pairs(L, ws, s);  // bucket sort gathers itself
     }
-    if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s);
+    if (e == cudaSuccess) e = launch_raster_fwd(L, ws, bg, out_rgb, out_T, s, it_mode(ws) == 0 && fused_tile_schedule(L));
     if (e != cudaSuccess) return GS_ERR_CUDA;
     std::lock_guard<std::mutex> g(g_mu);
     g_tokens[ws] = make_token(params, cams, n_views, 2);

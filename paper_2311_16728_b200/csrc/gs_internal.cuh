@@ -161,8 +161,12 @@ cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, 
                         cudaStream_t s);
 cudaError_t launch_ranges(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s);
+// scheduled: the tile scan (launch_tile_scan) already built the chunk tables / tile order
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
-                              cudaStream_t s);
+                              cudaStream_t s, bool scheduled = false);
+// A2 for the bucket binning fused with the raster schedule (one CTA; V * tiles <= 8192)
+bool fused_tile_schedule(const Layout &L);
+cudaError_t launch_tile_scan(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);
 // A9 into the compacted scratch (one row per parameter, one column per visible Gaussian)
 cudaError_t launch_preprocess_bwd(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,

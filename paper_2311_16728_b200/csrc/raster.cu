@@ -781,6 +781,118 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
     }
 }
 
+// ---------------------------------------------------------------- A2 + raster schedule, fused
+// Bucket binning with V * tiles <= 8192: one CTA scans the per-(view, tile) pair counts into the
+// tile starts and the pair total P (A2), and from the same counts builds the raster schedule --
+// the chunk tables and first-chunk-first order of the chunked path (levels with few tiles) or the
+// longest-list-first tile order -- so neither needs a launch of its own.
+constexpr int TSCAN_ITEMS = 8;  // counts per thread (1024 threads: up to 8192 tiles)
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    __syncthreads();  // s_warp may still be read by a previous call
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += u;
+        }
+        s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    total = s_warp[32];
+    return s_warp[warp] + incl - v;
+}
+
+__global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__ counts, int VT, int64_t cap,
+                                                    uint32_t *__restrict__ tile_start, WsHeader *hdr, int chunked,
+                                                    uint32_t *__restrict__ chunk_base, uint32_t *__restrict__ chunk_tile,
+                                                    uint32_t *__restrict__ chunk_order, int64_t max_chunks,
+                                                    uint32_t *__restrict__ tile_order) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
+    __shared__ uint32_t s_warp[33];
+    __shared__ uint32_t hist[256];
+    const int t = threadIdx.x;
+    uint32_t c[TSCAN_ITEMS], sum = 0;
+#pragma unroll
+    for (int k = 0; k < TSCAN_ITEMS; k++) {
+        const int i = t * TSCAN_ITEMS + k;
+        c[k] = i < VT ? counts[(size_t)i * CNT_STRIDE] : 0u;
+        sum += c[k];
+    }
+    uint32_t P;
+    uint32_t run = block_exclusive_scan(sum, s_warp, P);
+#pragma unroll
+    for (int k = 0; k < TSCAN_ITEMS; k++) {
+        const int i = t * TSCAN_ITEMS + k;
+        if (i < VT) tile_start[i] = run;
+        run += c[k];
+    }
+    if (t == 0) hdr->P = P;
+    const bool ok = (int64_t)P <= cap;  // overflow: nothing is binned, nothing to schedule
+    if (t < 256) hist[t] = 0;
+    __syncthreads();
+    if (chunked) {  // VT < CHUNK_MAX_TILES <= 1024: tile t = thread t (its counts are c[] of thread t / 8)
+        const uint32_t len = t < VT ? counts[(size_t)t * CNT_STRIDE] : 0u;
+        const uint32_t nch = ok ? (len + CHUNK - 1) / CHUNK : 0u;
+        uint32_t total;
+        const uint32_t base = block_exclusive_scan(nch, s_warp, total);
+        if (t < VT) chunk_base[t] = base;
+        if (t == 0) hdr->nchunks = (uint32_t)min((int64_t)total, max_chunks);
+        for (uint32_t k = 0; k < nch; k++)
+            if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
+        // first chunks first: counts per position in the list, scanned, then scattered
+        for (uint32_t k = 0; k < nch; k++) atomicAdd(&hist[min(k, 255u)], 1u);
+        __syncthreads();
+        const uint32_t hv = t < 256 ? hist[t] : 0u;
+        uint32_t dummy;
+        const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
+        if (t < 256) hist[t] = hb;
+        __syncthreads();
+        for (uint32_t k = 0; k < nch; k++) {
+            const uint32_t pos = atomicAdd(&hist[min(k, 255u)], 1u);
+            if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
+        }
+    } else {  // longest list first: bucket by length / 8, descending
+#pragma unroll
+        for (int k = 0; k < TSCAN_ITEMS; k++)
+            if (t * TSCAN_ITEMS + k < VT) atomicAdd(&hist[255 - min(255u, c[k] >> 3)], 1u);
+        __syncthreads();
+        const uint32_t hv = t < 256 ? hist[t] : 0u;
+        uint32_t dummy;
+        const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
+        if (t < 256) hist[t] = hb;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < TSCAN_ITEMS; k++) {
+            const int i = t * TSCAN_ITEMS + k;
+            if (i < VT) tile_order[atomicAdd(&hist[255 - min(255u, c[k] >> 3)], 1u)] = (uint32_t)i;
+        }
+    }
+}
+
+bool fused_tile_schedule(const Layout &L) { return (int64_t)L.V * L.tiles <= 1024 * TSCAN_ITEMS; }
+
+cudaError_t launch_tile_scan(const Layout &L, void *ws, cudaStream_t s) {
+    launch_pdl(k_tile_scan, 1, 1024, 0, s, at<uint32_t>(ws, L.tile_count), L.V * L.tiles, L.cap,
+               at<uint32_t>(ws, L.tile_start), at<WsHeader>(ws, L.hdr), L.max_chunks > 0 ? 1 : 0,
+               at<uint32_t>(ws, L.chunk_base), at<uint32_t>(ws, L.chunk_tile), at<uint32_t>(ws, L.chunk_order),
+               L.max_chunks, at<uint32_t>(ws, L.tile_order));
+    return cudaGetLastError();
+}
+
 // Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
 // tile) at pyramid levels with few tiles so that every SM gets work.
 static int raster_warps(const Layout &L) {
@@ -818,12 +930,13 @@ static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_
 
 
 cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
-                              cudaStream_t s) {
+                              cudaStream_t s, bool scheduled) {
     ProfScope prof("k_raster_fwd", s);
     uint32_t *cbase = nullptr;
     float4 *cbwd = nullptr;
     if (L.max_chunks > 0) {  // few tiles: record per-chunk state for the chunk-parallel backward
-        launch_pdl(k_chunk_index, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
+        if (!scheduled)
+            launch_pdl(k_chunk_index, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
                    at<uint32_t>(ws, L.chunk_base), at<uint32_t>(ws, L.chunk_tile), at<uint32_t>(ws, L.chunk_order),
                    at<WsHeader>(ws, L.hdr), L.max_chunks);
         cbase = at<uint32_t>(ws, L.chunk_base);
@@ -833,8 +946,9 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
     // order their backward chunks in k_chunk_index instead)
     const uint32_t *order = nullptr;
     if (L.max_chunks == 0) {
-        launch_pdl(k_tile_order, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
-                   at<uint32_t>(ws, L.tile_order));
+        if (!scheduled)
+            launch_pdl(k_tile_order, 1, 1024, 0, s, at<uint2>(ws, L.ranges), L.V * L.tiles,
+                       at<uint32_t>(ws, L.tile_order));
         order = at<uint32_t>(ws, L.tile_order);
     }
     switch (raster_warps(L)) {

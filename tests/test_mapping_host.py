@@ -44,10 +44,11 @@ def test_pack_unpack_roundtrip():
 
 def test_launch_accounting_matches_design():
     import bench
-    # bucket binning: preprocess, scan, scatter, short + long tile sorts (with the record gather),
-    # tile order or chunk index, raster, 2 loss, 3 fused bwd
-    assert bench.launches_per_iteration(43, True) == 12
-    assert bench.launches_per_iteration(43, True, chunked=True) == 12
-    assert bench.launches_per_iteration(43, False) == 13
-    # radix binning, 43 key bits -> 6 digit passes, + separate gather
+    # bucket binning: preprocess, tile scan (+ raster schedule when views x tiles <= 8192),
+    # scatter, short + long tile sorts (with the record gather), raster, 2 loss, 3 fused bwd
+    assert bench.launches_per_iteration(43, True, view_tiles=1200) == 11
+    assert bench.launches_per_iteration(43, True, chunked=True, view_tiles=80) == 11
+    assert bench.launches_per_iteration(43, False, view_tiles=1200) == 12
+    assert bench.launches_per_iteration(43, True, view_tiles=20000) == 12  # separate schedule kernel
+    # radix binning, 43 key bits -> 6 digit passes, + separate gather and schedule
     assert bench.launches_per_iteration(43, True, binning=1) == 2 + (4 + 6 + 1) + 1 + 1 + 2 + 3
