@@ -364,6 +364,30 @@ def run_ours(args):
     torch.cuda.synchronize()
     render_ms = a.elapsed_time(b) / nr
 
+    # ---- context for BASELINE.md's only comparable paper number (Table 1 render FPS on Replica
+    # 1200x680, 911-1084 FPS on an RTX 4090 with ~130-140K trained Gaussians): A1-A6 of one
+    # Replica-like keyframe view (500K Gaussians, SH 3) on this GPU
+    replica = None
+    if rank == 0 and world == 1 and not args.no_replica:
+        rscene = make_scene("replica")
+        rcam = make_cameras("replica", 1)
+        rr = Renderer(rscene.n, 3, 1, rcam[0].width, rcam[0].height, 1 << 23)
+        rp = pack_params(rscene)
+        for _ in range(3):
+            rr.forward(rp, rcam)
+        torch.cuda.synchronize()
+        st, flags, pairs = rr.ws.status()
+        a.record(stream)
+        for _ in range(nr):
+            rr.forward(rp, rcam)
+        b.record(stream)
+        torch.cuda.synchronize()
+        replica = {"workload": "replica 1200x680, 500000 Gaussians, SH 3, 1 view", "pairs": int(pairs),
+                   "render_fps": 1000.0 * nr / a.elapsed_time(b),
+                   "paper_render_fps_rtx4090": [911.262, 1084.017],
+                   "paper_note": "PAPER.md:416-417,444-445 (mono, RGB-D; trained maps of 31-35 MB): context only"}
+        del rr, rp
+
     # ---- e2e through the public API: pinned H2D of every step's targets + D2H of its losses
     # (MappingEngine.step_host, eager launches; step k+1's targets are copied on a copy stream
     # while step k computes -- the first step's copy is inside the timed region, the last step
@@ -467,6 +491,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "render_fps": 1000.0 / render_ms * len(cams) * world,
+            "render_replica": replica,
             "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
             "timing": {"headline": "CUDA graph replay per step" if use_graph else "eager launches",
                        "eager_ms_per_step": eager_ms / args.steps},
@@ -485,6 +510,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="tum")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-replica", action="store_true", help="skip the Replica render-FPS context line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-pixels", type=int, default=4096)
     ap.add_argument("--launch-list", action="store_true", help="profile exactly one step (ncu range)")
