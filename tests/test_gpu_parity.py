@@ -352,9 +352,11 @@ def test_backward_parity_tiny():
                                atol=1e-5 * ref["grad2d_norm"].max())
 
 
-@pytest.mark.parametrize("cfg,views,level,D", [("tum", 1, 0, 3), ("tum", 1, 2, 3), ("euroc", 3, 1, 3)])
+@pytest.mark.parametrize("cfg,views,level,D", [("tum", 1, 0, 3), ("tum", 1, 2, 3), ("euroc", 3, 1, 3),
+                                                ("euroc", 6, 2, 3), ("euroc", 16, 2, 3)])
 def test_backward_parity_sampled(cfg, views, level, D):
-    """dL/dI masked to 4096 sampled pixels on both sides (SURVEY §8(d) 'Parity runs')."""
+    """dL/dI masked to 4096 sampled pixels on both sides (SURVEY §8(d) 'Parity runs'), up to 16
+    views per call (the EuRoC keyframe batch of one GPU)."""
     scene = make_scene(cfg)
     cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
     r, params, D = _renderer(scene, cams)
