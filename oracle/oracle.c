@@ -963,3 +963,93 @@ void orc_densify(int64_t n, int K, const float *rec, const float *m, const float
             }
         }
 }
+
+/* ---------------------------- geometry-based densification -------- */
+/* SPEC.md:473-481 geometry_densify ("actively create additional temporary hyper
+   primitives based on the inactive 2D feature points"), initialisation as create_map_points
+   (SPEC.md:261), with DESIGN.md readings R31-R33.  Keypoint k at pixel (u, v); active[k] != 0 if
+   it observes a map primitive (its camera-space depth kp_depth[k]).  For every INACTIVE keypoint,
+   in index order:
+     RGB-D (mode 1): d = depth_map[round(v)][round(u)] (nearest pixel); skipped if d <= 0;
+     mono (mode 0): among active keypoints with squared pixel distance <= rho^2 (fp32:
+       fmaf(dx, dx, dy * dy)), the K = 4 nearest (ties: lower index) -> d = sum(w_i d_i) / sum(w_i)
+       with w_i = 1 / dist_i (an exactly coincident neighbour: the mean of the coincident depths);
+       skipped if none.
+   New primitive: P = R^T (d ((u - cx) / fx, (v - cy) / fy, 1) - t); q = (1, 0, 0, 0);
+   log s = log(d / fx) on all three axes; logit = logit(0.1); SH DC c = (pixel colour - 0.5) / C0
+   with the nearest pixel's colour (so the degree-0 colour equals the pixel), higher SH 0.
+   out_rec [count][K] (K = 11 + 3(D+1)^2, NULL: count only); src[count] = keypoint index.
+   Returns count. */
+int64_t orc_geometry_densify(const orc_camera *cam, int64_t nk, const float *uv, const int32_t *active,
+                             const float *kp_depth, const float *depth_map, const float *image, int mode, int D,
+                             float rho, double *out_rec, int32_t *src) {
+    const int K = 11 + 3 * (D + 1) * (D + 1);
+    const int W = cam->width, H = cam->height;
+    const double C0 = 0.28209479177387814;
+    int64_t cnt = 0;
+    for (int64_t k = 0; k < nk; k++) {
+        if (active[k]) continue;
+        const float u = uv[2 * k], v = uv[2 * k + 1];
+        const int px = (int)lrintf(u), py = (int)lrintf(v);
+        if (px < 0 || px >= W || py < 0 || py >= H) continue;
+        double d = 0.0;
+        if (mode == 1) {
+            d = depth_map[(int64_t)py * W + px];
+            if (!(d > 0.0)) continue;
+        } else {
+            int best[4];
+            float bd[4];
+            int nb = 0;
+            const float r2 = rho * rho;
+            for (int64_t j = 0; j < nk; j++) {
+                if (!active[j]) continue;
+                const float dx = uv[2 * j] - u, dy = uv[2 * j + 1] - v;
+                const float d2 = fmaf(dx, dx, dy * dy);
+                if (!(d2 <= r2)) continue;
+                /* insert into the sorted top-4 (strictly smaller distance moves ahead; equal
+                   distances keep index order because j ascends) */
+                int pos = nb;
+                while (pos > 0 && d2 < bd[pos - 1]) pos--;
+                if (pos >= 4) continue;
+                for (int q = (nb < 4 ? nb : 3); q > pos; q--) {
+                    bd[q] = bd[q - 1];
+                    best[q] = best[q - 1];
+                }
+                bd[pos] = d2;
+                best[pos] = (int)j;
+                if (nb < 4) nb++;
+            }
+            if (nb == 0) continue;
+            double sw = 0.0, swd = 0.0, zsum = 0.0;
+            int nz = 0;
+            for (int q = 0; q < nb; q++) {
+                if (bd[q] == 0.f) {
+                    zsum += kp_depth[best[q]];
+                    nz++;
+                }
+                const double w = 1.0 / sqrt((double)bd[q]);
+                sw += w;
+                swd += w * kp_depth[best[q]];
+            }
+            d = nz ? zsum / nz : swd / sw;
+        }
+        if (out_rec) {
+            double *o = out_rec + cnt * K;
+            for (int q = 0; q < K; q++) o[q] = 0.0;
+            const double xc[3] = {d * ((double)u - cam->cx) / cam->fx, d * ((double)v - cam->cy) / cam->fy, d};
+            for (int a = 0; a < 3; a++) { /* P = R^T (p_c - t) */
+                double s = 0.0;
+                for (int b = 0; b < 3; b++) s += (double)cam->R[3 * b + a] * (xc[b] - (double)cam->t[b]);
+                o[a] = s;
+            }
+            o[3] = 1.0;
+            for (int a = 0; a < 3; a++) o[7 + a] = log(d / cam->fx);
+            o[10] = log(0.1 / 0.9);
+            for (int ch = 0; ch < 3; ch++)
+                o[11 + ch] = ((double)image[(int64_t)ch * H * W + (int64_t)py * W + px] - 0.5) / C0;
+            src[cnt] = (int32_t)k;
+        }
+        cnt++;
+    }
+    return cnt;
+}

@@ -263,6 +263,26 @@ def densify(rec, m, v, grad_accum, vis_count, max_radius, z, grad_thr, percent_d
                 rec=out[:nn], m=om[:nn], v=ov[:nn])
 
 
+def geometry_densify(cam, uv, active, kp_depth, depth_map, image, mode, D=3, rho=100.0) -> dict:
+    """SPEC.md:473-481 geometry_densify (see oracle.c): new temporary primitives for the inactive
+    keypoints; rec [count][K] per-Gaussian records (fp64), src = keypoint index of each."""
+    ca, _ = _cams(cam)
+    uv = np.ascontiguousarray(uv, np.float32).reshape(-1, 2)
+    nk = uv.shape[0]
+    act = np.ascontiguousarray(active, np.int32)
+    kd = np.ascontiguousarray(kp_depth, np.float32)
+    dm = None if depth_map is None else np.ascontiguousarray(depth_map, np.float32)
+    img = np.ascontiguousarray(image, np.float32)
+    K = 11 + 3 * (D + 1) ** 2
+    lib().orc_geometry_densify.restype = C.c_int64
+    args = (ca, C.c_int64(nk), _p(uv), _p(act), _p(kd), _p(dm), _p(img), C.c_int(mode), C.c_int(D), C.c_float(rho))
+    cnt = lib().orc_geometry_densify(*args, None, None)
+    rec = np.zeros((max(cnt, 1), K))
+    src = np.zeros(max(cnt, 1), np.int32)
+    lib().orc_geometry_densify(*args, _p(rec), _p(src))
+    return dict(count=int(cnt), rec=rec[:cnt], src=src[:cnt])
+
+
 def exp_scale_f32(s):
     s = np.ascontiguousarray(s, np.float32)
     out = np.zeros_like(s)
