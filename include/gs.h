@@ -192,6 +192,28 @@ gs_status gs_densify_plan(const gs_params *params, const float *grad_accum, cons
 gs_status gs_densify_apply(const gs_params *params, const float *m, const float *v, const float *z, const void *temp,
                            size_t temp_bytes, gs_params *out, float *out_m, float *out_v, gs_stream_t stream);
 
+/* Carry a per-Gaussian byte tag (e.g. the temporary flag of geometry densification) through the
+   densification planned in temp: tags_out[new row] = tags_in[source Gaussian] for kept and cloned
+   originals, clones and split children.  tags_out: device uint8[n_new]. */
+gs_status gs_densify_tags(int64_t n, const void *temp, size_t temp_bytes, const uint8_t *tags_in, uint8_t *tags_out,
+                          gs_stream_t stream);
+
+/* ---- geometry-based densification ("actively
+   create additional temporary hyper primitives based on the inactive 2D feature points").
+   Readings R31-R33 in DESIGN.md.  For each INACTIVE keypoint (active[k] == 0), in index order,
+   at its nearest pixel (round-half-even; skipped outside the image): depth d from depth_map
+   (mode 1, RGB-D; skipped if <= 0) or (mode 0, mono) the inverse-distance-weighted depth of the
+   <= 4 nearest active keypoints within rho pixels (kp_depth[j]: camera-space depth of active
+   keypoint j; skipped if none); new primitive (create_map_points): P = R^T (d K^-1
+   (u, v, 1) - t), q = (1, 0, 0, 0), log s = log(d / fx) x 3, logit(0.1), SH DC = (pixel colour -
+   0.5) / C0, higher SH 0.  cam: host, one view; uv: device float[n][2]; active: device int32[n];
+   kp_depth: device float[n] (mono); depth_map: device float[H][W] (RGB-D); image: device float
+   [3][H][W].  out: parameter layout with capacity out->n >= n_keypoints rows (same sh_degree as
+   the map); rows [0, *count) are written; src[r] = keypoint of row r; count: device int32. */
+gs_status gs_geometry_densify(const gs_camera *cam, const float *uv, const int32_t *active, const float *kp_depth,
+                              const float *depth_map, const float *image, int32_t n_keypoints, int32_t mode, float rho,
+                              gs_params *out, int32_t *src, int32_t *count, gs_stream_t stream);
+
 /* A0: Gaussian pyramid (Eq. 5): level l+1 = even rows/cols of the level-l
    image blurred by [1,4,6,4,1]/16 horizontally then vertically with a reflect-101 border
    (R18); sizes ceil-halved.  img [n_images][C][H][W]; out = levels 1..n_levels concatenated,

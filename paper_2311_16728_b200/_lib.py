@@ -26,7 +26,7 @@ GS_TILE = 16
 EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess", "gs_render_forward",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
            "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
-           "gs_densify_plan", "gs_densify_apply",
+           "gs_densify_plan", "gs_densify_apply", "gs_densify_tags", "gs_geometry_densify",
            "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
@@ -258,6 +258,19 @@ def gs_densify_apply(params: GsParams, m, v, z: torch.Tensor, temp: torch.Tensor
                      stream=None):
     _check(lib().gs_densify_apply(C.byref(params), _ptr(m), _ptr(v), _ptr(z), _ptr(temp), C.c_size_t(temp.numel()),
                                   C.byref(out), _ptr(out_m), _ptr(out_v), _stream(stream)), "gs_densify_apply")
+
+
+def gs_densify_tags(n: int, temp: torch.Tensor, tags_in: torch.Tensor, tags_out: torch.Tensor, stream=None):
+    _check(lib().gs_densify_tags(C.c_int64(n), _ptr(temp), C.c_size_t(temp.numel()), _ptr(tags_in), _ptr(tags_out),
+                                 _stream(stream)), "gs_densify_tags")
+
+
+def gs_geometry_densify(cam, uv: torch.Tensor, active: torch.Tensor, kp_depth, depth_map, image: torch.Tensor,
+                        mode: int, rho: float, out: GsParams, src: torch.Tensor, count: torch.Tensor, stream=None):
+    ca = camera_struct([cam])
+    _check(lib().gs_geometry_densify(ca, _ptr(uv), _ptr(active), _ptr(kp_depth), _ptr(depth_map), _ptr(image),
+                                     C.c_int32(uv.shape[0]), C.c_int32(mode), C.c_float(rho), C.byref(out),
+                                     _ptr(src), _ptr(count), _stream(stream)), "gs_geometry_densify")
 
 
 def gs_query_status(ws: torch.Tensor, stream=None):

@@ -222,9 +222,10 @@ class DensifyConfig:
 
 
 def densify(params: torch.Tensor, n: int, sh_degree: int, m, v, grad_accum: torch.Tensor, vis_count: torch.Tensor,
-            max_radius: torch.Tensor, z: torch.Tensor, cfg: L.GsDensifyCfg):
-    """SURVEY f1 densify and prune: returns (new params [K, ld'], new m, new v, counts) with counts =
-    (n_clone, n_split, n_prune, n_new).  m, v may be None (no optimiser state)."""
+            max_radius: torch.Tensor, z: torch.Tensor, cfg: L.GsDensifyCfg, tags: torch.Tensor | None = None):
+    """SURVEY f1 densify and prune: returns (new params [K, ld'], new m, new v, counts[, new tags]) with
+    counts = (n_clone, n_split, n_prune, n_new).  m, v may be None (no optimiser state); tags: an
+    optional per-Gaussian uint8 tensor carried to the new map."""
     ps = L.params_struct(params, n, sh_degree)
     temp = torch.empty(max(L.gs_densify_temp_size(n), 1), dtype=torch.uint8, device=params.device)
     counts = L.gs_densify_plan(ps, grad_accum, vis_count, max_radius, cfg, temp)
@@ -233,4 +234,23 @@ def densify(params: torch.Tensor, n: int, sh_degree: int, m, v, grad_accum: torc
     om = torch.zeros_like(out) if m is not None else None
     ov = torch.zeros_like(out) if v is not None else None
     L.gs_densify_apply(ps, m, v, z, temp, L.params_struct(out, nn, sh_degree), om, ov)
-    return out, om, ov, counts
+    if tags is None:
+        return out, om, ov, counts
+    new_tags = torch.zeros(max(nn, 1), dtype=torch.uint8, device=params.device)
+    L.gs_densify_tags(n, temp, tags, new_tags)
+    return out, om, ov, counts, new_tags
+
+
+def geometry_densify(cam, uv: torch.Tensor, active: torch.Tensor, kp_depth, depth_map, image: torch.Tensor,
+                     mode: int, sh_degree: int, rho: float = 100.0):
+    """new temporary primitives for the inactive keypoints of one
+    keyframe.  Returns (params [K, ld] with `count` valid columns, count, src keypoint indices)."""
+    nk = int(uv.shape[0])
+    dev = uv.device
+    out = torch.zeros((param_rows(sh_degree), L.param_ld(max(nk, 1))), dtype=torch.float32, device=dev)
+    src = torch.zeros(max(nk, 1), dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int32, device=dev)
+    L.gs_geometry_densify(cam, uv, active, kp_depth, depth_map, image, mode, rho,
+                          L.params_struct(out, nk, sh_degree), src, count)
+    c = int(count.item())
+    return out, c, src[:c]

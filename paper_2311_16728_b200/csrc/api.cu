@@ -433,6 +433,28 @@ gs_status gs_densify_apply(const gs_params *params, const float *m, const float 
     return cuda_status(launch_densify_apply(*params, m, v, z, temp, *out, out_m, out_v, (cudaStream_t)stream));
 }
 
+gs_status gs_densify_tags(int64_t n, const void *temp, size_t temp_bytes, const uint8_t *tags_in, uint8_t *tags_out,
+                          gs_stream_t stream) {
+    if (n < 0 || !temp || (n > 0 && (!tags_in || !tags_out))) return GS_ERR_INVALID_ARG;
+    if (temp_bytes < densify_temp_bytes(n)) return GS_ERR_SHAPE;
+    return cuda_status(launch_densify_tags(n, temp, tags_in, tags_out, (cudaStream_t)stream));
+}
+
+gs_status gs_geometry_densify(const gs_camera *cam, const float *uv, const int32_t *active, const float *kp_depth,
+                              const float *depth_map, const float *image, int32_t n_keypoints, int32_t mode, float rho,
+                              gs_params *out, int32_t *src, int32_t *count, gs_stream_t stream) {
+    if (!cam || n_keypoints < 0 || !count || (mode != 0 && mode != 1)) return GS_ERR_INVALID_ARG;
+    gs_status st = check_params(out);
+    if (st) return st;
+    if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0.f) || !(cam->fy > 0.f)) return GS_ERR_INVALID_ARG;
+    if (n_keypoints > 0 && (!uv || !active || !image || !src || (mode == 1 && !depth_map) ||
+                            (mode == 0 && !kp_depth) || !(rho > 0.f)))
+        return GS_ERR_INVALID_ARG;
+    if (out->n < n_keypoints || out->sh_degree < 0) return GS_ERR_SHAPE;
+    return cuda_status(launch_geometry_densify(*cam, uv, active, kp_depth, depth_map, image, n_keypoints, mode, rho,
+                                               *out, src, count, (cudaStream_t)stream));
+}
+
 gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs) {
     if (!ws || !flags || ws_bytes < sizeof(WsHeader)) return GS_ERR_INVALID_ARG;
     WsHeader h;

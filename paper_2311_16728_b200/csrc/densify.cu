@@ -184,6 +184,33 @@ void densify_totals(const void *temp, int64_t n, uint32_t tot[3]) {
     }
 }
 
+// per-Gaussian byte tags through the planned densification: a kept or cloned original keeps its
+// tag, its clone and split children inherit it
+__global__ void __launch_bounds__(256) k_densify_tags(const uint8_t *__restrict__ cls, int64_t n,
+                                                      const uint32_t *__restrict__ o_keep,
+                                                      const uint32_t *__restrict__ o_clone,
+                                                      const uint32_t *__restrict__ o_split, const WsHeader *h_keep,
+                                                      const WsHeader *h_clone, const uint8_t *__restrict__ tin,
+                                                      uint8_t *__restrict__ tout) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t c = cls[i], tag = tin[i];
+    const int64_t n_keep = h_keep->P, n_clone = h_clone->P;
+    if (c <= 1) tout[o_keep[i]] = tag;
+    if (c == 1) tout[n_keep + o_clone[i]] = tag;
+    if (c == 2) tout[n_keep + n_clone + 2 * (int64_t)o_split[i]] = tout[n_keep + n_clone + 2 * (int64_t)o_split[i] + 1] = tag;
+}
+
+cudaError_t launch_densify_tags(int64_t n, const void *temp, const uint8_t *tin, uint8_t *tout, cudaStream_t s) {
+    const DensifyTemp t = densify_temp(n);
+    if (n == 0) return cudaGetLastError();
+    void *tp = const_cast<void *>(temp);
+    k_densify_tags<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        at<uint8_t>(tp, t.cls), n, at<uint32_t>(tp, t.off[0]), at<uint32_t>(tp, t.off[1]), at<uint32_t>(tp, t.off[2]),
+        at<WsHeader>(tp, t.hdr[0]), at<WsHeader>(tp, t.hdr[1]), tin, tout);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_densify_apply(const gs_params &p, const float *m, const float *v, const float *z, const void *temp,
                                  const gs_params &out, float *out_m, float *out_v, cudaStream_t s) {
     const DensifyTemp t = densify_temp(p.n);
@@ -193,6 +220,138 @@ cudaError_t launch_densify_apply(const gs_params &p, const float *m, const float
         p.data, m, v, p.n, p.ld, gs_param_rows(p.sh_degree), z, at<uint8_t>(tp, t.cls), at<uint32_t>(tp, t.off[0]),
         at<uint32_t>(tp, t.off[1]), at<uint32_t>(tp, t.off[2]), at<WsHeader>(tp, t.hdr[0]),
         at<WsHeader>(tp, t.hdr[1]), out.data, out_m, out_v, out.ld);
+    return cudaGetLastError();
+}
+
+}  // namespace gsk
+
+namespace gsk {
+
+// ---------------------------------------------------------------- f2: geometry-based densification
+// SPEC.md:473-481 with the create_map_points initialisation;
+// readings R31-R33 in DESIGN.md.  One CTA walks the keypoints in chunks of 1024, in order: a thread
+// per keypoint decides (inactive, pixel inside the image, depth from the depth map or from the
+// K = 4 nearest active keypoints within rho, inverse-distance weighted), a block scan of the
+// decisions gives each new primitive its row (keypoint order), and the thread writes it.
+constexpr int GD_THREADS = 1024;
+
+__global__ void __launch_bounds__(GD_THREADS) k_geometry_densify(const gs_camera cam, const float2 *__restrict__ uv,
+                                                                 const int32_t *__restrict__ active,
+                                                                 const float *__restrict__ kp_depth,
+                                                                 const float *__restrict__ depth_map,
+                                                                 const float *__restrict__ image, int nk, int mode,
+                                                                 float rho, int K, float *__restrict__ out,
+                                                                 int64_t ldo, int32_t *__restrict__ src,
+                                                                 int32_t *__restrict__ count) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_base;
+    const int W = cam.width, H = cam.height;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < nk; c0 += GD_THREADS) {
+        const int k = c0 + threadIdx.x;
+        bool ok = k < nk && !active[k];
+        float u = 0.f, v = 0.f;
+        int px = 0, py = 0;
+        double d = 0.0;
+        if (ok) {
+            const float2 p = uv[k];
+            u = p.x;
+            v = p.y;
+            px = __float2int_rn(u);
+            py = __float2int_rn(v);
+            ok = px >= 0 && px < W && py >= 0 && py < H;
+        }
+        if (ok && mode == 1) {
+            d = depth_map[(int64_t)py * W + px];
+            ok = d > 0.0;
+        } else if (ok) {
+            // K = 4 nearest active keypoints within rho (fp32 squared distances, ties by index)
+            int best[4];
+            float bd[4];
+            int nb = 0;
+            const float r2 = __fmul_rn(rho, rho);
+            for (int j = 0; j < nk; j++) {
+                if (!active[j]) continue;
+                const float2 q = uv[j];
+                const float dx = __fsub_rn(q.x, u), dy = __fsub_rn(q.y, v);
+                const float d2 = __fmaf_rn(dx, dx, __fmul_rn(dy, dy));
+                if (!(d2 <= r2)) continue;
+                int pos = nb;
+                while (pos > 0 && d2 < bd[pos - 1]) pos--;
+                if (pos >= 4) continue;
+                for (int t = (nb < 4 ? nb : 3); t > pos; t--) {
+                    bd[t] = bd[t - 1];
+                    best[t] = best[t - 1];
+                }
+                bd[pos] = d2;
+                best[pos] = j;
+                if (nb < 4) nb++;
+            }
+            ok = nb > 0;
+            if (ok) {
+                double sw = 0.0, swd = 0.0, zsum = 0.0;
+                int nz = 0;
+                for (int t = 0; t < nb; t++) {
+                    if (bd[t] == 0.f) {
+                        zsum += kp_depth[best[t]];
+                        nz++;
+                    }
+                    const double w = 1.0 / sqrt((double)bd[t]);
+                    sw += w;
+                    swd += w * kp_depth[best[t]];
+                }
+                d = nz ? zsum / nz : swd / sw;
+            }
+        }
+        // block-wide exclusive scan of the decisions -> rows in keypoint order
+        const unsigned b = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) s_warp[warp] = __popc(b);
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = s_warp[lane];
+            uint32_t incl = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += x;
+            }
+            s_warp[lane] = incl - w;
+        }
+        __syncthreads();
+        const uint32_t row = s_base + s_warp[warp] + __popc(b & ((1u << lane) - 1u));
+        if (ok) {
+            const double xc[3] = {d * ((double)u - cam.cx) / cam.fx, d * ((double)v - cam.cy) / cam.fy, d};
+            for (int a = 0; a < 3; a++) {  // P = R^T (p_c - t)
+                double s = 0.0;
+                for (int bb = 0; bb < 3; bb++) s += (double)cam.R[3 * bb + a] * (xc[bb] - (double)cam.t[bb]);
+                out[a * ldo + row] = (float)s;
+            }
+            out[3 * ldo + row] = 1.f;
+            out[4 * ldo + row] = out[5 * ldo + row] = out[6 * ldo + row] = 0.f;
+            const float ls = (float)log(d / cam.fx);
+            out[7 * ldo + row] = out[8 * ldo + row] = out[9 * ldo + row] = ls;
+            out[10 * ldo + row] = (float)log(0.1 / 0.9);
+            for (int ch = 0; ch < 3; ch++)
+                out[(11 + ch) * ldo + row] =
+                    (float)(((double)image[(int64_t)ch * H * W + (int64_t)py * W + px] - 0.5) / 0.28209479177387814);
+            for (int r = 14; r < K; r++) out[r * ldo + row] = 0.f;
+            src[row] = k;
+        }
+        __syncthreads();
+        if (threadIdx.x == GD_THREADS - 1) s_base = row + (ok ? 1u : 0u);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = (int32_t)s_base;
+}
+
+cudaError_t launch_geometry_densify(const gs_camera &cam, const float *uv, const int32_t *active, const float *kp_depth,
+                                    const float *depth_map, const float *image, int nk, int mode, float rho,
+                                    const gs_params &out, int32_t *src, int32_t *count, cudaStream_t s) {
+    k_geometry_densify<<<1, GD_THREADS, 0, s>>>(cam, reinterpret_cast<const float2 *>(uv), active, kp_depth, depth_map,
+                                                image, nk, mode, rho, gs_param_rows(out.sh_degree), out.data, out.ld,
+                                                src, count);
     return cudaGetLastError();
 }
 

@@ -184,8 +184,13 @@ cudaError_t launch_densify_plan(const gs_params &p, const float *grad_accum, con
                                 const int32_t *max_radius, float grad_thr, float big, float logit_thr,
                                 int32_t max_screen, void *temp, cudaStream_t s);
 void densify_totals(const void *temp, int64_t n, uint32_t tot[3]);
+cudaError_t launch_densify_tags(int64_t n, const void *temp, const uint8_t *tin, uint8_t *tout, cudaStream_t s);
 cudaError_t launch_densify_apply(const gs_params &p, const float *m, const float *v, const float *z, const void *temp,
                                  const gs_params &out, float *out_m, float *out_v, cudaStream_t s);
+// geometry-based densification (densify.cu)
+cudaError_t launch_geometry_densify(const gs_camera &cam, const float *uv, const int32_t *active, const float *kp_depth,
+                                    const float *depth_map, const float *image, int nk, int mode, float rho,
+                                    const gs_params &out, int32_t *src, int32_t *count, cudaStream_t s);
 cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int W, float lambda, float *loss,
                         float *dL, void *ws, cudaStream_t s);
 size_t loss_ws_bytes(int V, int H, int W);

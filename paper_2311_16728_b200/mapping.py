@@ -13,8 +13,8 @@ import torch.distributed as dist
 from synth import densify_samples, scaled_camera
 
 from . import _lib as L
-from .core import (Adam, AdamConfig, DensifyConfig, PhotometricLoss, Renderer, densify, gaussian_pyramid, level_shapes,
-                   pack_params)
+from .core import (Adam, AdamConfig, DensifyConfig, PhotometricLoss, Renderer, densify, gaussian_pyramid,
+                   geometry_densify, level_shapes, pack_params)
 
 
 def gp_level(iteration: int, n_levels: int, iters_per_level: int) -> int:
@@ -144,6 +144,8 @@ class MappingEngine:
         self.densify_cfg = densify_cfg
         self.vis_count = torch.zeros(self.n, dtype=torch.float32, device=device)
         self.max_radius = torch.zeros(self.n, dtype=torch.int32, device=device)
+        # 1 = temporary primitive from geometry-based densification
+        self.temporary = torch.zeros(self.n, dtype=torch.uint8, device=device)
         # replicated optimiser state (single GPU / unsharded DP); the sharded one keeps its rows only
         self.adam = Adam(self.params, self.n, self.D, adam) if self.sharded is None else None
         self.cams0 = list(cams)
@@ -265,8 +267,9 @@ class MappingEngine:
         z = torch.from_numpy(densify_samples(self.n, seed)).to(self.params.device)
         H, W = self.shapes[0]
         cfg = self.densify_cfg.struct(W, H)
-        p, m, v, counts = densify(self.params, self.n, self.D, self.adam.m, self.adam.v, self.grad2d_norm,
-                                  self.vis_count, self.max_radius, z, cfg)
+        p, m, v, counts, tags = densify(self.params, self.n, self.D, self.adam.m, self.adam.v, self.grad2d_norm,
+                                        self.vis_count, self.max_radius, z, cfg, tags=self.temporary)
+        self.temporary = tags
         self.n = counts[3]
         self.params = p
         self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, self.n
@@ -279,6 +282,46 @@ class MappingEngine:
         self.graph = None  # a captured step refers to the old buffers
         self.calibrate()
         return counts[:3]
+
+    # ------------------------------------------------------------------ geometry densification (f2)
+    def add_keyframe_features(self, view: int, uv, active, kp_depth, depth_map, image, mode: int,
+                              rho: float = 100.0) -> int:
+        """temporary primitives for the inactive keypoints of keyframe `view`
+        (level-0 camera), appended to the map with zero Adam moments; the workspaces are re-sized.
+        uv [n, 2], active [n] (0/1), kp_depth [n] (mono), depth_map [H, W] (RGB-D, mode 1),
+        image [3, H, W]; numpy or device tensors.  Returns the number of primitives added."""
+        if self.sharded is not None:
+            raise NotImplementedError("geometry densification with the row-sharded optimiser")
+        dev = self.params.device
+        t = lambda a, dt: None if a is None else torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a,  # noqa: E731
+                                                                 dtype=dt).to(dev).contiguous()
+        newp, cnt, _ = geometry_densify(self.cams0[view], t(uv, torch.float32), t(active, torch.int32),
+                                        t(kp_depth, torch.float32), t(depth_map, torch.float32),
+                                        t(image, torch.float32), mode, self.D, rho)
+        if cnt == 0:
+            return 0
+        n0, n1 = self.n, self.n + cnt
+        K = self.params.shape[0]
+        ld = L.param_ld(n1)
+        p = torch.zeros((K, ld), dtype=torch.float32, device=dev)
+        p[:, :n0] = self.params[:, :n0]
+        p[:, n0:n1] = newp[:, :cnt]
+        m = torch.zeros_like(p)
+        v = torch.zeros_like(p)
+        m[:, :n0] = self.adam.m[:, :n0]
+        v[:, :n0] = self.adam.v[:, :n0]
+        grow = lambda a, fill: torch.cat([a[:n0], torch.full((cnt,), fill, dtype=a.dtype, device=dev)])  # noqa: E731
+        self.temporary = grow(self.temporary, 1)
+        self.grad2d_norm, self.vis_count, self.max_radius = (grow(self.grad2d_norm, 0), grow(self.vis_count, 0),
+                                                             grow(self.max_radius, 0))
+        self.n = n1
+        self.params = p
+        self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, n1
+        self.grads = torch.zeros_like(p)
+        self.renderers = [None] * (self.n_levels + 1)
+        self.graph = None
+        self.calibrate()
+        return cnt
 
     # ------------------------------------------------------------------ CUDA graphs
     def capture(self, gts_pinned: torch.Tensor | None = None, out_pinned: torch.Tensor | None = None):

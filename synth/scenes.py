@@ -344,3 +344,24 @@ def densify_samples(n: int, seed: int) -> np.ndarray:
     clone, two per split), generated here and passed to both sides as an input."""
     rng = np.random.default_rng(np.random.PCG64(seed))
     return rng.normal(size=(n, 2, 3)).astype(np.float32)
+
+
+def make_keypoints(cam: Camera, n: int, seed: int, active_frac: float = 0.3):
+    """Synthetic keyframe features for geometry-based densification: n keypoint
+    pixels (uniform, rounded pixel inside the image), an `active` flag (fraction active_frac,
+    PAPER.md:231 "less than 30% ... are active"), a smooth depth map in [0.8, 4] m with 5 % invalid
+    (0) pixels, the active keypoints' depths read from it, and a smooth keyframe image."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    W, H = cam.width, cam.height
+    uv = rng.uniform([0.0, 0.0], [W - 1.0, H - 1.0], size=(n, 2)).astype(np.float32)
+    active = (rng.uniform(size=n) < active_frac).astype(np.int32)
+    y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+    depth = 2.4 + 0.8 * np.sin(x / W * 3.0 + rng.uniform(0, 6)) * np.cos(y / H * 2.0 + rng.uniform(0, 6))
+    depth += 0.4 * (x / W) - 0.2 * (y / H)
+    depth = np.clip(depth, 0.8, 4.0).astype(np.float32)
+    depth[rng.uniform(size=(H, W)) < 0.05] = 0.0
+    px = np.rint(uv[:, 0]).astype(int)
+    py = np.rint(uv[:, 1]).astype(int)
+    kp_depth = np.where(active == 1, np.maximum(depth[py, px], 0.8), 0.0).astype(np.float32)
+    image = noise_image(H, W, seed + 17)
+    return uv, active, kp_depth, depth, image

@@ -111,3 +111,68 @@ def test_mapping_engine_densify_and_prune():
         eng.build_pyramids()
         losses.append([x.item() for x in eng.step()])
     assert np.isfinite(np.array(losses)).all()
+
+
+# ------------------------------------------------------------------ f2: geometry-based densification
+@pytest.mark.parametrize("mode", [0, 1])
+def test_geometry_densify_matches_oracle(mode):
+    from paper_2311_16728_b200.core import geometry_densify
+    from synth import make_keypoints
+    cam = make_cameras("tum", 1)[0]
+    uv, active, kd, depth, img = make_keypoints(cam, 1500, 5)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    out, cnt, src = geometry_densify(cam, cu(uv), cu(active), cu(kd), cu(depth) if mode else None, cu(img), mode, 3)
+    ref = orc.geometry_densify(cam, uv, active, kd, depth if mode else None, img, mode, D=3)
+    assert cnt == ref["count"] > 100
+    assert np.array_equal(src.cpu().numpy(), ref["src"])
+    got = _records(out, cnt).astype(np.float64)
+    r = ref["rec"]
+    np.testing.assert_allclose(got[:, :3], r[:, :3], rtol=2e-7, atol=1e-6)        # back-projection (fp64 -> fp32)
+    assert np.array_equal(got[:, 3:7], r[:, 3:7])
+    np.testing.assert_allclose(got[:, 7:14], r[:, 7:14], rtol=2e-7, atol=1e-6)   # log s, logit, SH DC
+    assert (got[:, 14:] == 0).all()
+
+
+def test_densify_tags_follow_their_gaussians():
+    scene = make_scene("tum", n=3000)
+    n = scene.n
+    rng = np.random.default_rng(9)
+    vis = np.full(n, 2, np.float32)
+    ga = (rng.uniform(0, 2e-3, n) * 2).astype(np.float32)
+    mr = np.zeros(n, np.int32)
+    scene.opacity_logits[rng.choice(n, 100, replace=False)] = -7.0
+    small = rng.choice(n, n // 2, replace=False)
+    scene.log_scales[small] = np.log(0.002)
+    z = densify_samples(n, 4)
+    params = pack_params(scene)
+    tags = torch.from_numpy(rng.integers(0, 200, n).astype(np.uint8)).cuda()
+    c = DensifyConfig(grad_threshold=5e-4, scene_extent=1.0).struct(640, 480)
+    cuda = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    _, _, _, counts, new_tags = densify(params, n, 3, None, None, cuda(ga), cuda(vis), cuda(mr), cuda(z), c, tags=tags)
+    ref = orc.densify(orc.scene_records(scene), np.zeros((n, 59), np.float32), np.zeros((n, 59), np.float32), ga, vis,
+                      mr, z, c.grad_threshold, c.percent_dense, c.scene_extent, c.opacity_threshold, c.max_screen_px)
+    cls, t = ref["cls"], tags.cpu().numpy()
+    expect = np.concatenate([t[cls <= 1], t[cls == 1], np.repeat(t[cls == 2], 2)])
+    assert counts[3] == expect.size and np.array_equal(new_tags[:counts[3]].cpu().numpy(), expect)
+
+
+def test_mapping_engine_geometry_densify():
+    from synth import make_keypoints
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    params = pack_params(scene)
+    r = Renderer(scene.n, 0, 1, cams[0].width, cams[0].height, 1 << 16)
+    gt = r.forward(params, cams)[0].clone()
+    eng = MappingEngine(perturb(scene, 4), cams, gt, n_levels=1,
+                        densify_cfg=DensifyConfig(grad_threshold=1e-3, scene_extent=1.0))
+    uv, active, kd, depth, img = make_keypoints(cams[0], 120, 2)
+    n0 = eng.n
+    added = eng.add_keyframe_features(0, uv, active, kd, depth, img, mode=1)
+    assert added > 0 and eng.n == n0 + added
+    assert int(eng.temporary.sum().item()) == added and eng.temporary[:n0].sum().item() == 0
+    for _ in range(3):
+        eng.build_pyramids()
+        losses = [x.item() for x in eng.step()]
+    assert np.isfinite(losses).all()
+    nc, ns, npr = eng.densify_and_prune(seed=1)
+    assert eng.temporary.shape[0] >= eng.n
