@@ -393,6 +393,39 @@ static int cmp_pair(const void *pa, const void *pb) {
 }
 
 /* Returns the pair count; if keys != NULL fills sorted keys/vals and ranges[V*tiles][2]. */
+/* Exact ellipse-tile test (SURVEY §8(f) f3 "exact ellipse-tile binning", R10'): can the
+   3-sigma ellipse d^T Q d <= 9 (R9) reach a pixel centre of tile (tx, ty)?  Minimum of the
+   quadratic form over the tile's box of pixel centres [16 tx, 16 tx + 15] x [16 ty, 16 ty + 15]:
+   0 if the mean is inside, else the smallest of the four edge minima (y* = -B X / C clamped),
+   compared with 9.01 (0.1 % margin over the per-pixel cutoff, so a tile holding a pixel the
+   Gaussian can reach is never dropped).  fp32 IEEE operations in a fixed order (explicit fmaf,
+   -ffp-contract=off): the GPU takes the same decision bit for bit. */
+static int tile_hits_ellipse(float u, float v, float A, float B, float C, int tx, int ty) {
+    const float ax = (float)(tx * ORC_TILE) - u, bx = (float)(tx * ORC_TILE + ORC_TILE - 1) - u;
+    const float ay = (float)(ty * ORC_TILE) - v, by = (float)(ty * ORC_TILE + ORC_TILE - 1) - v;
+    if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return 1;
+    float best = INFINITY;
+    for (int e = 0; e < 2; e++) {
+        const float X = e ? bx : ax;
+        const float y = fminf(fmaxf(-(B * X) / C, ay), by);
+        const float fx_ = fmaf(C * y, y, fmaf((2.f * B) * X, y, (A * X) * X));
+        best = fminf(best, fx_);
+        const float Y = e ? by : ay;
+        const float x = fminf(fmaxf(-(B * Y) / A, ax), bx);
+        const float fy_ = fmaf(C * Y, Y, fmaf((2.f * B) * x, Y, (A * x) * x));
+        best = fminf(best, fy_);
+    }
+    return best <= 9.01f;
+}
+
+static int64_t tiles_of_gaussian(const orc_proj *o) {
+    int64_t c = 0;
+    for (int ty = o->rect[1]; ty < o->rect[3]; ty++)
+        for (int tx = o->rect[0]; tx < o->rect[2]; tx++)
+            c += tile_hits_ellipse(o->u_f, o->v_f, o->A_f, o->B_f, o->C_f, tx, ty);
+    return c;
+}
+
 int64_t orc_bin(int64_t n, int D, const float *means, const float *quats, const float *log_scales,
                 const float *opac, const float *sh, int V, const orc_camera *cams, uint64_t *keys,
                 uint32_t *vals, uint32_t *ranges, int32_t *tiles_touched) {
@@ -405,7 +438,7 @@ int64_t orc_bin(int64_t n, int D, const float *means, const float *quats, const 
         prs[v] = project_all(ORC_RECIPE, &s, cams + v);
         for (int64_t i = 0; i < n; i++) {
             orc_proj *o = prs[v] + i;
-            int64_t tt = o->radius > 0 ? (int64_t)(o->rect[2] - o->rect[0]) * (o->rect[3] - o->rect[1]) : 0;
+            int64_t tt = o->radius > 0 ? tiles_of_gaussian(o) : 0;
             if (tiles_touched) tiles_touched[(int64_t)v * n + i] = (int32_t)tt;
             P += tt;
         }
@@ -420,6 +453,7 @@ int64_t orc_bin(int64_t n, int D, const float *means, const float *quats, const 
                 uint32_t bits; memcpy(&bits, &o->depth_f, 4);
                 for (int ty = o->rect[1]; ty < o->rect[3]; ty++)
                     for (int tx = o->rect[0]; tx < o->rect[2]; tx++) {
+                        if (!tile_hits_ellipse(o->u_f, o->v_f, o->A_f, o->B_f, o->C_f, tx, ty)) continue;
                         uint64_t gt = (uint64_t)v * tiles + (uint64_t)ty * TXv + tx;
                         pairs[k].key = (gt << 32) | bits;
                         pairs[k].val = (uint32_t)i;

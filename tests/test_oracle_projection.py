@@ -155,6 +155,47 @@ def test_rect_is_conservative_for_cutoff():
         assert not (inside & ~in_rect).any(), i
 
 
+@pytest.mark.parametrize("cfg,n", [("tiny", None), ("tum", 20000)])
+def test_ellipse_tile_binning_is_exact_and_conservative(cfg, n):
+    """Exact ellipse-tile binning: a (Gaussian, tile) pair is binned iff the 3-sigma
+    ellipse can reach one of the tile's pixel centres (Mahalanobis^2 <= 9 + 0.1 %), checked by brute
+    force over all pixel centres in fp64 -- every pixel inside the ellipse keeps its tile, tiles the
+    ellipse cannot reach are dropped -- and far fewer pairs than the square rect."""
+    s = make_scene(cfg, n=n)
+    cam = make_cameras(cfg, 1)[0]
+    out = orc.project(s, cam, "recipe")
+    keys, vals, ranges, tt = orc.bin_pairs(s, [cam])
+    TX = (cam.width + 15) // 16
+    binned = set(zip(vals.tolist(), (keys >> np.uint64(32)).astype(np.int64).tolist()))
+    rect_pairs = 0
+    rng = np.random.default_rng(0)
+    vis = np.nonzero(out["radius"] > 0)[0]
+    for i in (vis if cfg == "tiny" else rng.choice(vis, 400, replace=False)):
+        u, v = out["mean2d"][i]
+        A, B, Cc = out["conic"][i]
+        x0, y0, x1, y1 = out["rect"][i]
+        rect_pairs += (x1 - x0) * (y1 - y0)
+        got = 0
+        for ty in range(y0, y1):
+            for tx in range(x0, x1):
+                ys, xs = np.mgrid[ty * 16:ty * 16 + 16, tx * 16:tx * 16 + 16]
+                dx, dy = xs - u, ys - v
+                q = (A * dx * dx + 2 * B * dx * dy + Cc * dy * dy).min()  # over pixel centres
+                # over the continuous box of pixel centres (fine grid, 1/8 px)
+                ys, xs = np.mgrid[ty * 16:ty * 16 + 15.001:0.125, tx * 16:tx * 16 + 15.001:0.125]
+                dx, dy = xs - u, ys - v
+                qb = (A * dx * dx + 2 * B * dx * dy + Cc * dy * dy).min()
+                hit = (int(i), ty * TX + tx) in binned
+                got += hit
+                if q < 9.0 - 1e-6:
+                    assert hit, (i, tx, ty, q)   # a tile holding a reachable pixel is never dropped
+                if qb > 9.02:
+                    assert not hit, (i, tx, ty, qb)  # a tile the ellipse cannot reach is (0.1 % margin)
+        assert got == tt[0, i]
+    if cfg == "tiny":
+        assert tt.sum() == keys.size and keys.size < rect_pairs
+
+
 def test_exp_scale_recipe_is_correctly_rounded():
     # (float)exp((double)s) equals the correctly rounded fp32 exp (checked in long double via mpmath-free
     # error bound): compare against float64 exp rounded to float32 on a dense sample.
