@@ -404,14 +404,15 @@ static int tile_hits_ellipse(float u, float v, float A, float B, float C, int tx
     const float ax = (float)(tx * ORC_TILE) - u, bx = (float)(tx * ORC_TILE + ORC_TILE - 1) - u;
     const float ay = (float)(ty * ORC_TILE) - v, by = (float)(ty * ORC_TILE + ORC_TILE - 1) - v;
     if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return 1;
+    const float rA = 1.0f / A, rC = 1.0f / C;  /* the edge minimisers y* = -B X / C via 1/C */
     float best = INFINITY;
     for (int e = 0; e < 2; e++) {
         const float X = e ? bx : ax;
-        const float y = fminf(fmaxf(-(B * X) / C, ay), by);
+        const float y = fminf(fmaxf(-(B * X) * rC, ay), by);
         const float fx_ = fmaf(C * y, y, fmaf((2.f * B) * X, y, (A * X) * X));
         best = fminf(best, fx_);
         const float Y = e ? by : ay;
-        const float x = fminf(fmaxf(-(B * Y) / A, ax), bx);
+        const float x = fminf(fmaxf(-(B * Y) * rA, ax), bx);
         const float fy_ = fmaf(C * Y, Y, fmaf((2.f * B) * x, Y, (A * x) * x));
         best = fminf(best, fy_);
     }

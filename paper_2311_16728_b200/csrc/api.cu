@@ -45,6 +45,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.radius = take(M * sizeof(int32_t));
     L.rect = take(M * sizeof(int4));
     L.tiles_touched = take(M * sizeof(uint32_t));
+    L.tile_mask = take(M * sizeof(uint64_t));
     L.offsets = take(M * sizeof(uint32_t));
     L.grad2d = take(M * 3 * sizeof(float4));
     L.scan_flags = take((size_t)std::max<int64_t>(L.scan_blocks, 1) * sizeof(uint64_t));

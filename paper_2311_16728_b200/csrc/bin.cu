@@ -29,6 +29,8 @@ namespace gsk {
 // global atomic per (CTA, tile) on the padded cursors, then hands out slots with shared-memory
 // atomics -- so global atomic traffic is one per touched tile per CTA, not one per pair.
 __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ rect, const int32_t *__restrict__ radius,
+                                                     const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
+                                                     const uint64_t *__restrict__ tmask,
                                                      const float *__restrict__ depth,
                                                      const uint32_t *__restrict__ vis_list,
                                                      const uint32_t *__restrict__ tile_start,
@@ -54,9 +56,8 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
             for (int v = 0; v < V; v++) {
                 const int64_t m = (int64_t)v * n + gi;
                 if (radius[m] <= 0) continue;
-                const int4 r = rect[m];
-                for (int ty = r.y; ty < r.w; ty++)
-                    for (int tx = r.x; tx < r.z; tx++) atomicAdd(&s_bins[v * tiles + ty * TX + tx], 1u);
+                for_each_binned_tile(rect[m], tmask[m], rec0, rec1, m,
+                                     [&](int tx, int ty) { atomicAdd(&s_bins[v * tiles + ty * TX + tx], 1u); });
             }
         __syncthreads();
         for (int b = threadIdx.x; b < VT; b += blockDim.x) {
@@ -70,16 +71,14 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
     for (int v = 0; v < V; v++) {
         const int64_t m = (int64_t)v * n + gi;
         if (radius[m] <= 0) continue;
-        const int4 r = rect[m];
         const uint64_t key = (uint64_t)__float_as_uint(depth[m]) << 32 | gi;
         const uint32_t tb = (uint32_t)v * tiles;
-        for (int ty = r.y; ty < r.w; ty++)
-            for (int tx = r.x; tx < r.z; tx++) {
-                const uint32_t gt = tb + ty * TX + tx;
-                const uint32_t pos = use_smem ? s_bins[VT + gt] + atomicAdd(&s_bins[gt], 1u)
-                                              : tile_start[gt] + atomicAdd(&cursor[(size_t)gt * CNT_STRIDE], 1u);
-                tmp[pos] = key;
-            }
+        for_each_binned_tile(rect[m], tmask[m], rec0, rec1, m, [&](int tx, int ty) {
+            const uint32_t gt = tb + ty * TX + tx;
+            const uint32_t pos = use_smem ? s_bins[VT + gt] + atomicAdd(&s_bins[gt], 1u)
+                                          : tile_start[gt] + atomicAdd(&cursor[(size_t)gt * CNT_STRIDE], 1u);
+            tmp[pos] = key;
+        });
     }
 }
 
@@ -335,7 +334,8 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
     }
     if (L.n > 0)
         launch_pdl(k_bin_scatter, (unsigned)((L.n + 255) / 256), 256, smem, s, 
-            at<int4>(ws, L.rect), at<int32_t>(ws, L.radius), at<float>(ws, L.depth), at<uint32_t>(ws, L.vis_list),
+            at<int4>(ws, L.rect), at<int32_t>(ws, L.radius), at<float4>(ws, L.rec0), at<float4>(ws, L.rec1),
+            at<uint64_t>(ws, L.tile_mask), at<float>(ws, L.depth), at<uint32_t>(ws, L.vis_list),
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
     ProfScope prof("k_tile_sort", s);

@@ -63,6 +63,7 @@ struct Layout {
     size_t hdr, rec0, rec1, rec2, depth, radius, rect, tiles_touched, offsets, grad2d, scan_flags, vis_list;
     size_t slot, scratch;  // per-Gaussian list index (~0u = invisible); per-list-entry gradients [59][n]
     size_t tile_count, tile_start, tile_cursor, bin_big, big_tiles;  // bucket binning (bin.cu)
+    size_t tile_mask;   // per (view, Gaussian): rect tiles the ellipse reaches (rects <= 64 tiles)
     size_t tile_order;  // (view, tile) indices, longest list first (raster.cu)
     size_t prec;  // per-pair 48-byte records in sorted order (raster.cu)
     int64_t max_chunks;  // chunked raster path (0 if unused)
@@ -112,6 +113,62 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 template <typename T>
 __host__ __device__ inline T *at(void *ws, size_t off) {
     return reinterpret_cast<T *>(reinterpret_cast<char *>(ws) + off);
+}
+
+// Exact ellipse-tile test (R10'): can the 3-sigma ellipse d^T Q d <= 9 reach a pixel
+// centre of tile (tx, ty)?  Box minimum of the quadratic form over the tile's pixel centres (mean
+// inside -> 0, else the four clamped edge minima) against 9.01; fp32 IEEE operations in the same
+// fixed order as the oracle, so both sides bin exactly the same pairs.
+// rA = 1/A, rC = 1/C (IEEE, computed once per Gaussian by the caller: ellipse_recips)
+__device__ __forceinline__ void ellipse_recips(float A, float C, float &rA, float &rC) {
+    rA = __fdiv_rn(1.0f, A);
+    rC = __fdiv_rn(1.0f, C);
+}
+__device__ __forceinline__ bool tile_hits_ellipse(float u, float v, float A, float B, float C, float rA, float rC,
+                                                  int tx, int ty) {
+    const float ax = __fsub_rn((float)(tx * TILE), u), bx = __fsub_rn((float)(tx * TILE + TILE - 1), u);
+    const float ay = __fsub_rn((float)(ty * TILE), v), by = __fsub_rn((float)(ty * TILE + TILE - 1), v);
+    if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return true;
+    const float B2 = __fmul_rn(2.f, B);
+    float best = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        const float X = e ? bx : ax;
+        const float y = fminf(fmaxf(__fmul_rn(-__fmul_rn(B, X), rC), ay), by);
+        best = fminf(best, __fmaf_rn(__fmul_rn(C, y), y, __fmaf_rn(__fmul_rn(B2, X), y, __fmul_rn(__fmul_rn(A, X), X))));
+        const float Y = e ? by : ay;
+        const float x = fminf(fmaxf(__fmul_rn(-__fmul_rn(B, Y), rA), ax), bx);
+        best = fminf(best, __fmaf_rn(__fmul_rn(C, Y), Y, __fmaf_rn(__fmul_rn(B2, x), Y, __fmul_rn(__fmul_rn(A, x), x))));
+    }
+    return best <= 9.01f;
+}
+
+// Visit the binned tiles of rect r (row-major order), f(tx, ty): from the hit mask for rects of
+// <= 64 tiles, else by re-running the ellipse test.
+template <typename F>
+__device__ __forceinline__ void for_each_binned_tile(const int4 r, uint64_t mask, const float4 *__restrict__ rec0,
+                                                     const float4 *__restrict__ rec1, int64_t m, F f) {
+    const int rw = r.z - r.x;
+    if (rw * (r.w - r.y) <= 64) {
+        const uint64_t row_bits = rw >= 64 ? ~0ull : (1ull << rw) - 1;
+        for (int ty = r.y; mask; ty++, mask >>= rw) {  // row by row: no division
+            uint64_t m = mask & row_bits;
+            while (m) {
+                const int bit = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                f(r.x + bit, ty);
+            }
+            if (rw >= 64) break;
+        }
+    } else {  // large rect (rare): the test again, from the records
+        const float4 g = rec0[m];
+        const float C = rec1[m].x;
+        float rA, rC;
+        ellipse_recips(g.z, C, rA, rC);
+        for (int ty = r.y; ty < r.w; ty++)
+            for (int tx = r.x; tx < r.z; tx++)
+                if (tile_hits_ellipse(g.x, g.y, g.z, g.w, C, rA, rC, tx, ty)) f(tx, ty);
+    }
 }
 
 // Largest d^T Q d at which a Gaussian can still be composited: the 3-sigma cutoff (R9) or the

@@ -263,17 +263,30 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
         depth[m] = p.z;
         radius[m] = p.r;
         rect[m] = make_int4(p.x0, p.y0, p.x1, p.y1);
-        tt[m] = (uint32_t)((p.x1 - p.x0) * (p.y1 - p.y0));
-        if (count_tiles) {  // per-(view, tile) pair counts for the bucket binning (bin.cu)
-            const int tb = v * L.tiles;
-            uint32_t *tc = at<uint32_t>(ws, L.tile_count);
-            for (int ty = p.y0; ty < p.y1; ty++)
-                for (int tx = p.x0; tx < p.x1; tx++) {
-                    int b = tb + ty * L.TX + tx;
+        // pairs: the tiles of the rect the 3-sigma ellipse can reach (R10'); with the bucket
+        // binning also the per-(view, tile) pair counts (bin.cu)
+        // (rects of <= 64 tiles keep the hit mask for the key emission, bit = row-major rect index)
+        uint32_t hits = 0;
+        uint64_t mask = 0;
+        const int tb = v * L.tiles;
+        const int rw = p.x1 - p.x0;
+        uint32_t *tc = at<uint32_t>(ws, L.tile_count);
+        float rA, rC;
+        ellipse_recips(p.A, p.C, rA, rC);
+        for (int ty = p.y0; ty < p.y1; ty++)
+            for (int tx = p.x0; tx < p.x1; tx++) {
+                if (!tile_hits_ellipse(p.u, p.v, p.A, p.B, p.C, rA, rC, tx, ty)) continue;
+                hits++;
+                const int bit = (ty - p.y0) * rw + (tx - p.x0);
+                if (bit < 64) mask |= 1ull << bit;
+                if (count_tiles) {
+                    const int b = tb + ty * L.TX + tx;
                     if (smem_cnt) atomicAdd(&s_cnt[b], 1u);
                     else atomicAdd(&tc[(size_t)b * CNT_STRIDE], 1u);
                 }
-        }
+            }
+        tt[m] = hits;
+        at<uint64_t>(ws, L.tile_mask)[m] = mask;
         float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
         g2d[3 * m] = zero;
         g2d[3 * m + 1] = zero;

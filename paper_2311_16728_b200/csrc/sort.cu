@@ -117,7 +117,9 @@ cudaError_t launch_scan_u32(const uint32_t *in, uint32_t *out, int64_t count, ui
 
 // ------------------------------------------------------------------------------ duplicate
 __global__ void __launch_bounds__(256) k_duplicate(const int4 *__restrict__ rect, const uint32_t *__restrict__ off,
-                                                   const uint32_t *__restrict__ tt, const float *__restrict__ depth,
+                                                   const uint32_t *__restrict__ tt, const float4 *__restrict__ rec0,
+                                                   const float4 *__restrict__ rec1, const uint64_t *__restrict__ tmask,
+                                                   const float *__restrict__ depth,
                                                    int64_t n, int64_t M, int TX, int tiles, int64_t cap,
                                                    uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
                                                    WsHeader *hdr) {
@@ -135,18 +137,18 @@ __global__ void __launch_bounds__(256) k_duplicate(const int4 *__restrict__ rect
     int4 r = rect[m];
     uint32_t bits = __float_as_uint(depth[m]);
     uint64_t tbase = (uint64_t)view * tiles;
-    for (int ty = r.y; ty < r.w; ty++)
-        for (int tx = r.x; tx < r.z; tx++) {
-            keys[o] = ((tbase + (uint64_t)(ty * TX + tx)) << 32) | bits;
-            vals[o] = gi;
-            o++;
-        }
+    for_each_binned_tile(r, tmask[m], rec0, rec1, m, [&](int tx, int ty) {  // R10'
+        keys[o] = ((tbase + (uint64_t)(ty * TX + tx)) << 32) | bits;
+        vals[o] = gi;
+        o++;
+    });
 }
 
 cudaError_t launch_duplicate(const Layout &L, void *ws, cudaStream_t s) {
     if (L.M == 0) return cudaGetLastError();
     k_duplicate<<<(L.M + 255) / 256, 256, 0, s>>>(
-        at<int4>(ws, L.rect), at<uint32_t>(ws, L.offsets), at<uint32_t>(ws, L.tiles_touched), at<float>(ws, L.depth),
+        at<int4>(ws, L.rect), at<uint32_t>(ws, L.offsets), at<uint32_t>(ws, L.tiles_touched), at<float4>(ws, L.rec0),
+        at<float4>(ws, L.rec1), at<uint64_t>(ws, L.tile_mask), at<float>(ws, L.depth),
         L.n, L.M, L.TX, L.tiles, L.cap, at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<WsHeader>(ws, L.hdr));
     return cudaGetLastError();
 }
