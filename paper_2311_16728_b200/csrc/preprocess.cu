@@ -359,7 +359,12 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     float *S = at<float>(ws, L.scratch);  // [row][n], column t
     // loads whose values are needed only late, issued up front (the kernel is latency-bound)
     const float gnorm_old = gnorm ? gnorm[i] : 0.f;
-    const int32_t rad0 = radius[i];  // view 0 (the common single-view case)
+    // rendered views 0..63 (bit v: radius > 0), one pass of independent loads; views >= 64 test
+    // the radius again
+    uint64_t vm = 0;
+#pragma unroll 8
+    for (int v = 0; v < min(V, 64); v++) vm |= (uint64_t)(radius[(int64_t)v * n + i] > 0) << v;
+#define RENDERED(v, m) ((v) < 64 ? ((vm >> (v)) & 1ull) != 0 : radius[m] > 0)
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
                           P[9 * ld + i]);
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     // ---- geometry: conic -> Sigma2 -> (Sigma3, J) -> (q, s), mean2d -> P
     for (int v = 0; v < V; v++) {
         int64_t m = (int64_t)v * n + i;
-        if ((v == 0 ? rad0 : radius[m]) <= 0) continue;
+        if (!RENDERED(v, m)) continue;
         const gs_camera &cam = cams.c[v];
         Proj p = project_recipe(cam, px, py, pz, cv, L.TX, L.TY);
         float4 ga = g2d[3 * m], gb = g2d[3 * m + 1];
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         }
         for (int v = 0; v < V; v++) {
             int64_t m = (int64_t)v * n + i;
-            if ((v == 0 ? rad0 : radius[m]) <= 0) continue;
+            if (!RENDERED(v, m)) continue;
             const float *gcol4 = reinterpret_cast<const float *>(g2d + 3 * m);
             float gcol = gcol4[6 + ch];  // record [.. | C, sigma, r, g | b ..]
             float Cc[3];
@@ -493,8 +498,9 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     // consumed: reset the 2D records so a repeated backward on the same forward starts from 0
     for (int v = 0; v < V; v++) {
         int64_t m = (int64_t)v * n + i;
-        if (radius[m] > 0) g2d[3 * m] = g2d[3 * m + 1] = g2d[3 * m + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (RENDERED(v, m)) g2d[3 * m] = g2d[3 * m + 1] = g2d[3 * m + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#undef RENDERED
     // quaternion: dL/dq_hat from dL/dRq, then through the normalisation
     float w_ = cv.qn[0], qx = cv.qn[1], qy = cv.qn[2], qz = cv.qn[3];
     const float *g = gR;
