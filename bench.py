@@ -394,8 +394,16 @@ def run_ours(args):
     # prefetches nothing)
     gts_pinned = [eng.gt0.cpu().pin_memory() for _ in range(2)]
     out_pinned = torch.empty((iters_per_step, len(cams)), dtype=torch.float32).pin_memory()
-    def run_e2e(k, last):
-        eng.step_host(gts_pinned[k % 2], out_pinned, None if last else gts_pinned[(k + 1) % 2])
+    e2e_graph = world == 1 and not args.no_graph
+    if e2e_graph:  # single GPU: the same API as two CUDA graphs (MappingEngine.capture_pipelined)
+        outs = [out_pinned, torch.empty_like(out_pinned).pin_memory()]
+        eng.capture_pipelined(gts_pinned, outs)
+
+        def run_e2e(k, last):
+            eng.step_pipelined()
+    else:
+        def run_e2e(k, last):
+            eng.step_host(gts_pinned[k % 2], out_pinned, None if last else gts_pinned[(k + 1) % 2])
     for k in range(2):
         run_e2e(k, k == 1)
     torch.cuda.synchronize()
@@ -487,7 +495,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "iters/s",
                     "h2d_bytes_per_step": int(gts_pinned[0].numel() * 4),
-                    "d2h_bytes_per_step": int(out_pinned.numel() * 4)},
+                    "d2h_bytes_per_step": int(out_pinned.numel() * 4),
+                    "api": ("MappingEngine.step_pipelined (two CUDA graphs; next step's targets copied "
+                            "H2D while this step computes)") if e2e_graph else
+                           "MappingEngine.step_host (eager launches, prefetch on a copy stream)"},
             "gpu_launches": launches,
             "clocks": clocks,
             "render_fps": 1000.0 / render_ms * len(cams) * world,

@@ -15,7 +15,8 @@ import threading
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgs.so")
+# GS_LIB_PATH: an alternative build of the same sources (tools/build_variant.py A/B experiments)
+LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(PKG, "libgs.so")
 
 GS_OK, GS_ERR_INVALID_ARG, GS_ERR_SHAPE, GS_ERR_CAPACITY, GS_ERR_STALE_STATE, GS_ERR_CUDA, \
     GS_ERR_NOT_SUPPORTED = range(7)

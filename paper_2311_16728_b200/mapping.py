@@ -356,6 +356,61 @@ class MappingEngine:
     def replay(self):
         self.graph.replay()
 
+    def capture_pipelined(self, gts_pinned: list, out_pinned: list):
+        """The end-to-end step (`step_host` with prefetch) as two CUDA graphs, single GPU.
+
+        gts_pinned / out_pinned: two pinned host buffers each ([V, 3, H, W] targets, [levels, V]
+        losses).  Graph i computes a step from device target buffer i -- A0, the Eq. 5 pass, the
+        D2H of the losses into out_pinned[i] -- while a forked copy stream brings gts_pinned[1 - i]
+        (the NEXT step's targets) into device buffer 1 - i.  `step_pipelined()` replays graph
+        k % 2 for call k; the caller fills gts_pinned[(k + 1) % 2] before call k.  Use either this
+        pair or `capture()`/`replay()` on an engine, not both."""
+        if self.distributed():
+            raise RuntimeError("graph capture is for the single-GPU fused path")
+        self.adam.use_device_step()
+        bufs = [self.gt0, torch.empty_like(self.gt0)]
+        copy = torch.cuda.Stream(device=self.gt0.device)
+
+        def body(i):
+            self.gt0 = bufs[i]
+            cs = torch.cuda.current_stream()
+            copy.wait_stream(cs)  # the buffer's last reader (the previous step) is queued before
+            with torch.cuda.stream(copy):
+                bufs[1 - i].copy_(gts_pinned[1 - i], non_blocking=True)
+            self.build_pyramids(overlap=True)
+            out_pinned[i].copy_(torch.stack(self.step()), non_blocking=True)
+            cs.wait_stream(copy)
+
+        side = torch.cuda.Stream(device=self.gt0.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up (real steps) on a side stream
+            bufs[0].copy_(gts_pinned[0], non_blocking=True)
+            body(0)
+            body(1)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graphs = []
+        for i in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                body(i)
+            graphs.append(g)
+        self.gt0 = bufs[0]
+        self._pipe = dict(graphs=graphs, bufs=bufs, gts=gts_pinned, out=out_pinned, k=0)
+        return graphs
+
+    def step_pipelined(self) -> torch.Tensor:
+        """Call k of the pipelined end-to-end step (see capture_pipelined): returns the pinned
+        losses buffer it fills (valid after the stream synchronises).  Call 0 also copies its own
+        targets (gts_pinned[0]); later calls' targets were prefetched by the previous call."""
+        pp = self._pipe
+        i = pp["k"] % 2
+        if pp["k"] == 0:
+            pp["bufs"][0].copy_(pp["gts"][0], non_blocking=True)
+        pp["graphs"][i].replay()
+        pp["k"] += 1
+        return pp["out"][i]
+
     def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor,
                   next_gts_pinned: torch.Tensor | None = None):
         """End-to-end public API: new keyframe targets from pinned host memory (H2D), A0,

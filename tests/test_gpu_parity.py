@@ -507,6 +507,39 @@ def test_step_host_prefetch_matches_plain():
     assert not torch.allclose(la[0], la[1])  # the targets really changed between steps
 
 
+def test_step_pipelined_matches_step_host():
+    """The two-graph pipelined end-to-end step (capture_pipelined / step_pipelined) runs the same
+    steps as eager step_host on the same target sequence: its two warm-up steps (targets 0, 1)
+    and then calls k = 0..3 (targets k % 2)."""
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, _ = _renderer(scene, cams)
+    gt_a = r.forward(params, cams)[0].clone()
+    gt_b = torch.from_numpy(noise_image(48, 64, 9)[None]).cuda()
+    start = perturb(scene, 5)
+    host = [gt_a.cpu().pin_memory(), gt_b.cpu().pin_memory()]
+    a = MappingEngine(start, cams, gt_a, n_levels=1)
+    la = []
+    for k in range(6):
+        out = torch.empty((2, 1)).pin_memory()
+        a.step_host(host[k % 2], out)
+        torch.cuda.synchronize()
+        la.append(out.clone())
+    c = MappingEngine(start, cams, gt_a, n_levels=1)
+    outs = [torch.empty((2, 1)).pin_memory() for _ in range(2)]
+    c.capture_pipelined(host, outs)
+    lc = []
+    for k in range(4):
+        o = c.step_pipelined()
+        torch.cuda.synchronize()
+        assert o.data_ptr() == outs[k % 2].data_ptr()
+        lc.append(o.clone())
+    for x, y in zip(la[2:], lc):
+        torch.testing.assert_close(x, y, rtol=1e-3, atol=1e-6)
+    assert not torch.allclose(lc[0], lc[1])  # the targets alternate between calls
+    assert int(c.adam.t_dev.item()) == 6 * 2
+
+
 # ------------------------------------------------------------------------------ mapping loop
 def test_mapping_engine_reduces_loss():
     """A few Eq. 5 passes on the tiny config reduce the photometric loss (SPEC.md:460 trend)."""

@@ -1,11 +1,12 @@
 """Warp-stall samples per CUDA source line (cuda,sass correlation) of one kernel in an ncu report.
-usage: python tools/ncu_hot_cuda.py <report> [N]"""
+usage: python tools/ncu_hot_cuda.py <report> [N [ncu filter args]]"""
 import csv, io, subprocess, sys
 from collections import defaultdict
 
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+EXTRA = sys.argv[3:]  # e.g. -k regex:name --launch-skip 1 -c 1
+out = subprocess.run(["ncu", "-i", rep, *EXTRA, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 agg = defaultdict(int)
 src_text = {}
