@@ -28,7 +28,9 @@ namespace gsk {
 // memory, a CTA first counts its pairs per tile there, reserves each tile's sub-range with one
 // global atomic per (CTA, tile) on the padded cursors, then hands out slots with shared-memory
 // atomics -- so global atomic traffic is one per touched tile per CTA, not one per pair.
-__global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ rect, const int32_t *__restrict__ radius,
+constexpr int BIN_THREADS = 256;  // threads (visible Gaussians) per k_bin_scatter CTA
+
+__global__ void __launch_bounds__(BIN_THREADS) k_bin_scatter(const int4 *__restrict__ rect, const int32_t *__restrict__ radius,
                                                      const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
                                                      const uint64_t *__restrict__ tmask,
                                                      const float *__restrict__ depth,
@@ -49,16 +51,31 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = t < hdr->vis_count;
     const uint32_t gi = live ? vis_list[t] : 0u;
+    // every lane stays to the end: rects of > 64 tiles are binned by the whole warp
+    // (warp_big_rects), the others by their own lane from the hit mask
+    auto big_args = [&](int64_t m, bool big, float4 &g, float &C) {
+        g = big ? rec0[m] : make_float4(0.f, 0.f, 0.f, 0.f);
+        C = big ? rec1[m].x : 0.f;
+    };
     if (use_smem) {
         for (int b = threadIdx.x; b < VT; b += blockDim.x) s_bins[b] = 0;
         __syncthreads();
-        if (live)
-            for (int v = 0; v < V; v++) {
-                const int64_t m = (int64_t)v * n + gi;
-                if (radius[m] <= 0) continue;
-                for_each_binned_tile(rect[m], tmask[m], rec0, rec1, m,
+        for (int v = 0; v < V; v++) {
+            const int64_t m = (int64_t)v * n + gi;
+            const bool vis = live && radius[m] > 0;
+            const int4 r = vis ? rect[m] : make_int4(0, 0, 0, 0);
+            const bool big = (r.z - r.x) * (r.w - r.y) > 64;
+            if (vis && !big)
+                for_each_binned_tile(r, tmask[m], rec0, rec1, m,
                                      [&](int tx, int ty) { atomicAdd(&s_bins[v * tiles + ty * TX + tx], 1u); });
-            }
+            float4 g;
+            float C;
+            big_args(m, big, g, C);
+            warp_big_rects(
+                big, r, g.x, g.y, g.z, g.w, C, 0ull,
+                [&](uint64_t, int tx, int ty) { atomicAdd(&s_bins[v * tiles + ty * TX + tx], 1u); },
+                [](int, uint32_t) {});
+        }
         __syncthreads();
         for (int b = threadIdx.x; b < VT; b += blockDim.x) {
             uint32_t c = s_bins[b];
@@ -67,18 +84,24 @@ __global__ void __launch_bounds__(256) k_bin_scatter(const int4 *__restrict__ re
         }
         __syncthreads();
     }
-    if (!live) return;
     for (int v = 0; v < V; v++) {
         const int64_t m = (int64_t)v * n + gi;
-        if (radius[m] <= 0) continue;
-        const uint64_t key = (uint64_t)__float_as_uint(depth[m]) << 32 | gi;
+        const bool vis = live && radius[m] > 0;
+        const int4 r = vis ? rect[m] : make_int4(0, 0, 0, 0);
+        const bool big = (r.z - r.x) * (r.w - r.y) > 64;
+        const uint64_t key = vis ? (uint64_t)__float_as_uint(depth[m]) << 32 | gi : 0ull;
         const uint32_t tb = (uint32_t)v * tiles;
-        for_each_binned_tile(rect[m], tmask[m], rec0, rec1, m, [&](int tx, int ty) {
+        auto emit = [&](uint64_t k, int tx, int ty) {
             const uint32_t gt = tb + ty * TX + tx;
             const uint32_t pos = use_smem ? s_bins[VT + gt] + atomicAdd(&s_bins[gt], 1u)
                                           : tile_start[gt] + atomicAdd(&cursor[(size_t)gt * CNT_STRIDE], 1u);
-            tmp[pos] = key;
-        });
+            tmp[pos] = k;
+        };
+        if (vis && !big) for_each_binned_tile(r, tmask[m], rec0, rec1, m, [&](int tx, int ty) { emit(key, tx, ty); });
+        float4 g;
+        float C;
+        big_args(m, big, g, C);
+        warp_big_rects(big, r, g.x, g.y, g.z, g.w, C, key, emit, [](int, uint32_t) {});
     }
 }
 
@@ -333,7 +356,7 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
         attr = true;
     }
     if (L.n > 0)
-        launch_pdl(k_bin_scatter, (unsigned)((L.n + 255) / 256), 256, smem, s, 
+        launch_pdl(k_bin_scatter, (unsigned)((L.n + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, smem, s, 
             at<int4>(ws, L.rect), at<int32_t>(ws, L.radius), at<float4>(ws, L.rec0), at<float4>(ws, L.rec1),
             at<uint64_t>(ws, L.tile_mask), at<float>(ws, L.depth), at<uint32_t>(ws, L.vis_list),
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,

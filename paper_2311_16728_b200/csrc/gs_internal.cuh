@@ -144,7 +144,8 @@ __device__ __forceinline__ bool tile_hits_ellipse(float u, float v, float A, flo
 }
 
 // Visit the binned tiles of rect r (row-major order), f(tx, ty): from the hit mask for rects of
-// <= 64 tiles, else by re-running the ellipse test.
+// <= 64 tiles, else by re-running the ellipse test (the bucket binning hands those rects to
+// warp_big_rects instead; the radix path's k_duplicate still walks them here).
 template <typename F>
 __device__ __forceinline__ void for_each_binned_tile(const int4 r, uint64_t mask, const float4 *__restrict__ rec0,
                                                      const float4 *__restrict__ rec1, int64_t m, F f) {
@@ -168,6 +169,45 @@ __device__ __forceinline__ void for_each_binned_tile(const int4 r, uint64_t mask
         for (int ty = r.y; ty < r.w; ty++)
             for (int tx = r.x; tx < r.z; tx++)
                 if (tile_hits_ellipse(g.x, g.y, g.z, g.w, C, rA, rC, tx, ty)) f(tx, ty);
+    }
+}
+
+// Rects of more than 64 tiles (no hit mask; a few large footprints near the camera, up to
+// ~1000 tiles) are binned by the whole warp instead of their own thread, which would otherwise
+// walk them serially and hold its CTA (and the kernel's tail) for the entire rect.  For every
+// lane with `big` set, in lane order, the 32 lanes test tiles k = lane, lane + 32, ... of its
+// rect (row-major index k) with the same exact test and call f(owner's payload, tx, ty) per hit;
+// done(owner_lane, hits) is then called on every lane with the rect's total hit count.
+// All 32 lanes must call it (converged).  Visit order differs from the row-major one: callers
+// only count or fill buckets whose order the tile sorts fix.
+template <typename F, typename G>
+__device__ __forceinline__ void warp_big_rects(bool big, int4 r, float u, float v, float A, float B, float C,
+                                               uint64_t payload, F f, G done) {
+    unsigned bm = __ballot_sync(0xffffffffu, big);
+    const int lane = threadIdx.x & 31;
+    while (bm) {
+        const int src = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int x0 = __shfl_sync(0xffffffffu, r.x, src), y0 = __shfl_sync(0xffffffffu, r.y, src);
+        const int rw = __shfl_sync(0xffffffffu, r.z, src) - x0;
+        const int area = rw * (__shfl_sync(0xffffffffu, r.w, src) - y0);
+        const float uu = __shfl_sync(0xffffffffu, u, src), vv = __shfl_sync(0xffffffffu, v, src);
+        const float AA = __shfl_sync(0xffffffffu, A, src), BB = __shfl_sync(0xffffffffu, B, src);
+        const float CC = __shfl_sync(0xffffffffu, C, src);
+        const uint64_t pl = __shfl_sync(0xffffffffu, payload, src);
+        float rA, rC;
+        ellipse_recips(AA, CC, rA, rC);
+        uint32_t hits = 0;
+        for (int k = lane; k < area; k += 32) {
+            const int ty = y0 + k / rw, tx = x0 + k % rw;
+            if (tile_hits_ellipse(uu, vv, AA, BB, CC, rA, rC, tx, ty)) {
+                hits++;
+                f(pl, tx, ty);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+        done(src, hits);
     }
 }
 
