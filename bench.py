@@ -475,7 +475,9 @@ def run_ours(args):
             "config": {"workload": args.config, "n_gaussians": n, "sh_degree": D, "width": W, "height": H,
                        "gp_levels": cfg["levels"] + 1, "views_per_gpu": len(cams), "global_batch": total_views,
                        "iters_per_step": iters_per_step, "parallelism": f"dp{world}",
-                       "l2": f"working set {4 * K * ld * 4 / 1e6:.0f} MB (params+grads+Adam m,v) > 126 MB L2; no flush"},
+                       "l2": f"working set {4 * K * ld * 4 / 1e6:.0f} MB (params+grads+Adam m,v) > 126 MB L2; no flush",
+                       "layout": "Gaussians in Morton order (MappingEngine spatial_order, once at setup; the "
+                                 "input recipe shuffles them)"},
             "roofline": {"bound": "alu", "kernel": "k_raster_bwd (A8)", "achieved": bwd_achieved,
                          "peak": fp32_peak, "unit": "TFLOP/s", "frac": bwd_achieved / fp32_peak,
                          "traffic": (traffic or {}).get("k_raster_bwd"),

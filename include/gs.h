@@ -245,6 +245,25 @@ gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, i
 
 const char *gs_status_str(gs_status s);
 
+/* ---- Map layout (not a step of the method): spatial order.
+   Eq. 3 does not depend on where a Gaussian sits in memory -- its index only
+   breaks ties between equal depths (SPEC.md:348 (3)) -- but the memory behaviour of the
+   per-Gaussian kernels (A1, A9, A11, bin scatter) and of the raster backward's atomics does.
+   gs_spatial_order writes perm[k] (device uint32[n]) = index of the Gaussian placed at position
+   k: ascending 30-bit Morton code of its mean (x in bits 0, 3, ..., y in 1, 4, ..., z in 2, 5,
+   ...), each axis cell = min(1023, (int)((x - lo) * (1024 / (hi - lo)))) in fp32 IEEE operations
+   over the means' bounding box [lo, hi] (cell 0 for a flat axis); equal codes keep index order.
+   temp: device bytes >= gs_spatial_order_temp_size.  GS_ERR_NOT_SUPPORTED for n >= 2^30.
+   gs_permute_columns: dst[r * ld + k] = src[r * ld + perm[k]] for r < rows, k < n (src and dst
+   distinct device buffers; the parameter layout has rows = gs_param_rows(D), a per-Gaussian
+   array rows = 1).  Applying the same perm to params, Adam m and v keeps the optimiser state
+   with its Gaussians. */
+gs_status gs_spatial_order_temp_size(int64_t n, size_t *bytes);
+gs_status gs_spatial_order(const gs_params *params, uint32_t *perm, void *temp, size_t temp_bytes,
+                           gs_stream_t stream);
+gs_status gs_permute_columns(const float *src, float *dst, int64_t ld, int32_t rows, int64_t n, const uint32_t *perm,
+                             gs_stream_t stream);
+
 /* ---- test / benchmark entry points ------------------------------------------------------ */
 /* Stable LSD radix sort of n (key, value) pairs on key bits [0, key_bits) (8-bit digits,
    one decoupled-look-back pass per digit).  Sorted in place in keys/vals; keys_alt/vals_alt

@@ -28,7 +28,8 @@ EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
            "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
            "gs_densify_plan", "gs_densify_apply", "gs_densify_tags", "gs_geometry_densify",
-           "gs_query_status", "gs_status_str", "gs_sort_temp_size", "gs_debug_sort_pairs",
+           "gs_query_status", "gs_status_str", "gs_spatial_order_temp_size", "gs_spatial_order",
+           "gs_permute_columns", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
 
@@ -280,6 +281,23 @@ def gs_query_status(ws: torch.Tensor, stream=None):
     p = C.c_int64()
     s = lib().gs_query_status(_ptr(ws), C.c_size_t(ws.numel()), _stream(stream), C.byref(f), C.byref(p))
     return s, f.value, p.value
+
+
+def gs_spatial_order_temp_size(n) -> int:
+    b = C.c_size_t()
+    _check(lib().gs_spatial_order_temp_size(C.c_int64(n), C.byref(b)), "gs_spatial_order_temp_size")
+    return b.value
+
+
+def gs_spatial_order(params: GsParams, perm: torch.Tensor, temp: torch.Tensor, stream=None):
+    _check(lib().gs_spatial_order(C.byref(params), _ptr(perm), _ptr(temp), C.c_size_t(temp.numel()),
+                                  _stream(stream)), "gs_spatial_order")
+
+
+def gs_permute_columns(src: torch.Tensor, dst: torch.Tensor, ld: int, rows: int, n: int, perm: torch.Tensor,
+                       stream=None):
+    _check(lib().gs_permute_columns(_ptr(src), _ptr(dst), C.c_int64(ld), C.c_int32(rows), C.c_int64(n), _ptr(perm),
+                                    _stream(stream)), "gs_permute_columns")
 
 
 def gs_sort_temp_size(n, key_bits) -> int:

@@ -254,3 +254,25 @@ def geometry_densify(cam, uv: torch.Tensor, active: torch.Tensor, kp_depth, dept
                           L.params_struct(out, nk, sh_degree), src, count)
     c = int(count.item())
     return out, c, src[:c]
+
+
+def spatial_order(params: torch.Tensor, n: int, sh_degree: int) -> torch.Tensor:
+    """Map layout (gs_spatial_order): int32 [n] device perm, perm[k] = index of the Gaussian
+    that goes to position k (ascending Morton code of its mean)."""
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=params.device)
+    temp = torch.empty(L.gs_spatial_order_temp_size(n), dtype=torch.uint8, device=params.device)
+    L.gs_spatial_order(L.params_struct(params, n, sh_degree), perm, temp)
+    return perm[:n]
+
+
+def permute_columns(t: torch.Tensor, perm: torch.Tensor, n: int) -> torch.Tensor:
+    """New tensor with column k = column perm[k] of t for k < n (gs_permute_columns); t is
+    [rows, ld] (parameter layout, Adam moments) or [>= n] (per-Gaussian array, 4-byte dtype)."""
+    out = t.clone() if t.shape[-1] > n else torch.empty_like(t)  # columns >= n (padding) stay as they were
+    rows = 1 if t.dim() == 1 else t.shape[0]
+    ld = t.shape[-1]
+    if t.element_size() != 4:
+        raise ValueError("4-byte element type required")
+    L.gs_permute_columns(t.view(torch.float32) if t.dtype != torch.float32 else t,
+                         out.view(torch.float32) if out.dtype != torch.float32 else out, ld, rows, n, perm)
+    return out

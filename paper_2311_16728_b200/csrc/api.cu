@@ -479,6 +479,32 @@ const char *gs_status_str(gs_status s) {
     return "unknown status";
 }
 
+gs_status gs_spatial_order_temp_size(int64_t n, size_t *bytes) {
+    if (!bytes || n < 0) return GS_ERR_INVALID_ARG;
+    if (n >= ((int64_t)1 << 30)) return GS_ERR_NOT_SUPPORTED;
+    *bytes = spatial_order_temp_bytes(n);
+    return GS_OK;
+}
+
+gs_status gs_spatial_order(const gs_params *params, uint32_t *perm, void *temp, size_t temp_bytes,
+                           gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    size_t need = 0;
+    if ((st = gs_spatial_order_temp_size(params->n, &need))) return st;
+    if (!perm || !temp) return GS_ERR_INVALID_ARG;
+    if (temp_bytes < need) return GS_ERR_SHAPE;
+    if (params->n == 0) return GS_OK;
+    return cuda_status(launch_spatial_order(params->data, params->ld, params->n, perm, temp, (cudaStream_t)stream));
+}
+
+gs_status gs_permute_columns(const float *src, float *dst, int64_t ld, int32_t rows, int64_t n, const uint32_t *perm,
+                             gs_stream_t stream) {
+    if (n < 0 || rows < 0 || ld < n) return GS_ERR_INVALID_ARG;
+    if (n > 0 && rows > 0 && (!src || !dst || !perm || src == dst)) return GS_ERR_INVALID_ARG;
+    return cuda_status(launch_permute_columns(src, dst, ld, rows, n, perm, (cudaStream_t)stream));
+}
+
 gs_status gs_sort_temp_size(int64_t n, int32_t key_bits, size_t *bytes) {
     if (!bytes || n < 0 || key_bits <= 0 || key_bits > 64) return GS_ERR_INVALID_ARG;
     if (n >= ((int64_t)1 << 30)) return GS_ERR_NOT_SUPPORTED;

@@ -253,6 +253,10 @@ int binning_mode();
 cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_duplicate(const Layout &L, void *ws, cudaStream_t s);
 // generic pair sort on the primary buffers of a workspace (or debug buffers)
+size_t spatial_order_temp_bytes(int64_t n);  // order.cu
+cudaError_t launch_spatial_order(const float *P, int64_t ld, int64_t n, uint32_t *perm, void *temp, cudaStream_t s);
+cudaError_t launch_permute_columns(const float *src, float *dst, int64_t ld, int rows, int64_t n,
+                                   const uint32_t *perm, cudaStream_t s);
 cudaError_t launch_sort(uint64_t *k0, uint32_t *v0, uint64_t *k1, uint32_t *v1, const uint32_t *count,
                         int64_t cap, int key_bits, WsHeader *hdr, uint32_t *lookback, int64_t sort_blocks,
                         cudaStream_t s);

@@ -14,7 +14,8 @@ from synth import densify_samples, scaled_camera
 
 from . import _lib as L
 from .core import (Adam, AdamConfig, DensifyConfig, PhotometricLoss, Renderer, densify, gaussian_pyramid,
-                   geometry_densify, level_shapes, pack_params)
+                   geometry_densify, level_shapes, pack_params, permute_columns)
+from .core import spatial_order as core_spatial_order
 
 
 def gp_level(iteration: int, n_levels: int, iters_per_level: int) -> int:
@@ -120,12 +121,23 @@ class MappingEngine:
 
     def __init__(self, scene, cams, gts, n_levels: int = 2, lam: float = 0.2, adam: AdamConfig | None = None,
                  device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0),
-                 shard_optimizer: bool = True, densify_cfg: DensifyConfig | None = None):
+                 shard_optimizer: bool = True, densify_cfg: DensifyConfig | None = None,
+                 spatial_order: bool = True):
         self.device = device
         self.n = scene.means.shape[0]
         self.D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
         self.group = group
         packed = pack_params(scene, device)
+        # map layout (order.cu): Gaussians in Morton order of their means, so that the ones that
+        # land on the same tiles are neighbours in memory.  order[k] = index in `scene` of the
+        # Gaussian at position k (None once densification has changed the map).  Every rank
+        # computes the same permutation from the same parameters.
+        self.spatial_order = spatial_order
+        self.order = None
+        if spatial_order and self.n > 0:
+            perm = core_spatial_order(packed, self.n, self.D)
+            packed = permute_columns(packed, perm, self.n)
+            self.order = perm.to(torch.int64)
         self.sharded = None
         if shard_optimizer and self.distributed():
             # reduce-scatter -> row-sharded Adam -> all-gather (parameters / gradients live in
@@ -269,8 +281,13 @@ class MappingEngine:
         cfg = self.densify_cfg.struct(W, H)
         p, m, v, counts, tags = densify(self.params, self.n, self.D, self.adam.m, self.adam.v, self.grad2d_norm,
                                         self.vis_count, self.max_radius, z, cfg, tags=self.temporary)
-        self.temporary = tags
         self.n = counts[3]
+        if self.spatial_order and self.n > 0:  # clones and split children went to the end: re-order
+            perm = core_spatial_order(p, self.n, self.D)
+            p, m, v = (permute_columns(x, perm, self.n) for x in (p, m, v))
+            tags = permute_columns(tags.to(torch.int32), perm, self.n).to(torch.uint8)
+        self.order = None
+        self.temporary = tags
         self.params = p
         self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, self.n
         self.grads = torch.zeros_like(p)
@@ -315,6 +332,13 @@ class MappingEngine:
         self.grad2d_norm, self.vis_count, self.max_radius = (grow(self.grad2d_norm, 0), grow(self.vis_count, 0),
                                                              grow(self.max_radius, 0))
         self.n = n1
+        if self.spatial_order:  # the new primitives went to the end: re-order
+            perm = core_spatial_order(p, n1, self.D)
+            p, m, v = (permute_columns(x, perm, n1) for x in (p, m, v))
+            self.temporary = permute_columns(self.temporary.to(torch.int32), perm, n1).to(torch.uint8)
+            self.grad2d_norm, self.vis_count = (permute_columns(x, perm, n1) for x in (self.grad2d_norm, self.vis_count))
+            self.max_radius = permute_columns(self.max_radius, perm, n1)
+        self.order = None
         self.params = p
         self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, n1
         self.grads = torch.zeros_like(p)
