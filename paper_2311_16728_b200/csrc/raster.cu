@@ -346,37 +346,38 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                             chunk_bwd);
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Warp sum of eight values with a transposing butterfly: at offsets 16, 8, 4 every lane keeps
-// half of its values and receives the partner's other half (4 + 2 + 1 shuffles), then two
-// plain xor steps finish the sum.  Lane l ends with the total of value index
-// ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); 9 shuffles instead of 40.
-__device__ __forceinline__ float warp_sum8_transposed(float a[8], int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+// Warp sums of nine values: the eight of a[] with a transposing butterfly (at offsets 16, 8, 4
+// every lane keeps half of its values and receives the partner's other half) while the ninth
+// (b) is summed plainly alongside; at offset 2 the pair (r, b) is itself transposed and offset 1
+// finishes both: 4 + 1 + 2 + 1 + 1 + 1 + 1 + 1 = 12 shuffles instead of 9 + 5.  Lanes with (lane & 3) == 2 end with the total of value index
+// ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); lanes with (lane & 2) == 0 with the
+// total of b.
+__device__ __forceinline__ float warp_sum9_transposed(float a[8], float b, int lane) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
     float h[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-        float send = b4 ? a[k] : a[k + 4];
-        float keep = b4 ? a[k + 4] : a[k];
+        const float send = b4 ? a[k] : a[k + 4];
+        const float keep = b4 ? a[k + 4] : a[k];
         h[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
+    b += __shfl_xor_sync(0xffffffffu, b, 16);
     float q[2];
 #pragma unroll
     for (int k = 0; k < 2; k++) {
-        float send = b3 ? h[k] : h[k + 2];
-        float keep = b3 ? h[k + 2] : h[k];
+        const float send = b3 ? h[k] : h[k + 2];
+        const float keep = b3 ? h[k + 2] : h[k];
         q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-    float send = b2 ? q[0] : q[1];
+    b += __shfl_xor_sync(0xffffffffu, b, 8);
+    const float send = b2 ? q[0] : q[1];
     float r = (b2 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
-    r += __shfl_xor_sync(0xffffffffu, r, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    return r;
+    b += __shfl_xor_sync(0xffffffffu, b, 4);
+    // (r, b) transposed at offset 2: bit-1 lanes keep r, the others b
+    const float s2 = b1 ? b : r;
+    float x = (b1 ? r : b) + __shfl_xor_sync(0xffffffffu, s2, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
 }
 
 // ================================================================ chunked backward (few tiles)
@@ -478,7 +479,7 @@ struct Pix2 {
 // FEW: at most this many contributing lanes -> per-lane atomics instead of the warp reduction
 template <int FEW>
 __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint32_t position, float fx,
-                                           float2 fy2, int lane, int64_t vbase, float4 *g2d) {
+                                           float2 fy2, int lane, int red_off, float *g2dv) {
     const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
     // power per pixel in the recipe's op order (bit-identical to pixel_power)
     const float dx = SUB(fx, g0.x);
@@ -516,7 +517,7 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
     float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
                       qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
     const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
-    float *dst = reinterpret_cast<float *>(g2d + 3 * (vbase + gi));
+    float *dst = g2dv + 12 * gi;  // the view's 48-byte records (g2dv = g2d + 3 view n)
     if (FEW > 0 && __popc(__ballot_sync(0xffffffffu, vA || vB)) <= FEW) {
         // few contributing lanes (an entry touching the block's edge): their own atomics are
         // cheaper than the warp reduction
@@ -527,10 +528,13 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
         }
         return;
     }
-    const float mine = warp_sum8_transposed(vals8, lane);
-    const float bsum = warp_sum(db.x + db.y);
-    if ((lane & 3) == 0) atomicAdd(dst + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1), mine);
-    if (lane == 1) atomicAdd(dst + 8, bsum);
+    const float mine = warp_sum9_transposed(vals8, db.x + db.y, lane);
+    if ((lane & 3) == 2 || lane == 0) atomicAdd(dst + red_off, mine);
+}
+
+// per-lane slot of warp_sum9_transposed's result: value index for (lane & 3) == 2, 8 (b) for lane 0
+__device__ __forceinline__ int sum9_slot(int lane) {
+    return (lane & 3) == 2 ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1) : 8;
 }
 
 __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ ranges,
@@ -563,7 +567,8 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
     const uint2 range = ranges[(int64_t)view * tiles + tile];
     const float fx = (float)px;
     const float2 fy2 = make_float2((float)pyA, (float)pyB);
-    const int64_t vbase = (int64_t)view * n;
+    float *g2dv = reinterpret_cast<float *>(g2d + 3 * (int64_t)view * n);
+    const int red_off = sum9_slot(lane);
     const int64_t HW = (int64_t)H * W;
     const int64_t pixA = (int64_t)pyA * W + px, pixB = (int64_t)pyB * W + px;
     Pix2 P;
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         __syncwarp();
         for (int t = 0; t < nsel; t++) {
             const int j = wl[warp][t];
-            bwd2_entry<2>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, vbase, g2d);
+            bwd2_entry<2>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, red_off, g2dv);
         }
     }
 }
@@ -732,10 +737,11 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
     __syncwarp();
     const float fx = (float)px;
     const float2 fy2 = make_float2((float)pyA, (float)pyB);
-    const int64_t vbase = (int64_t)view * n;
+    float *g2dv = reinterpret_cast<float *>(g2d + 3 * (int64_t)view * n);
+    const int red_off = sum9_slot(lane);
     for (int t = 0; t < nsel; t++) {
         const int j = wl[warp][t];
-        bwd2_entry<FEW_CHUNK>(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, vbase, g2d);
+        bwd2_entry<FEW_CHUNK>(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, red_off, g2dv);
     }
 }
 
