@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     __shared__ __align__(128) RasterSmem S;
     constexpr int SEG = CHUNKED ? CHUNK : BATCH;  // list segment = unit of chunk recording
     constexpr int NSEG = BATCH / SEG;
-    __shared__ __align__(16) uint8_t wl[WARPS][BATCH];  // segment s's selection at [s * SEG, ...)
+    constexpr int FG = 8;                       // list entries evaluated together in phase 2
+    constexpr int SEGP = SEG + FG;              // segment stride: FG padding entries after each list
+    __shared__ __align__(16) int wl[WARPS][NSEG * SEGP];  // segment s's selection at [s * SEGP, ...)
     __shared__ int segn[WARPS][NSEG];
     // tiles in longest-list-first order (shorter lists end the kernel: less tail); without an
     // order blockIdx decides
@@ -278,9 +280,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
             int j = k + lane;
             bool hit = j < cnt && !block_misses(r[3 * j], r[3 * j + 1], r[3 * j + 2].w, wx0, wy0);
             unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) wl[warp][seg * SEG + nsel + __popc(b & lt)] = (uint8_t)j;
+            if (hit) wl[warp][seg * SEGP + nsel + __popc(b & lt)] = j;
             nsel += __popc(b);
-            if (lane == 0) segn[warp][seg] = nsel;
+            if (k + 32 >= cnt || (k + 32) % SEG == 0) {  // segment complete: its count, and FG
+                if (lane == 0) segn[warp][seg] = nsel;   // padding entries (record 0 of the batch:
+                if (lane < FG) wl[warp][seg * SEGP + nsel + lane] = 0;  // finite data) after it
+            }
         }
         __syncwarp();
         const int nseg = (cnt + SEG - 1) / SEG;
@@ -289,21 +294,21 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
             if (__all_sync(0xffffffffu, done)) break;
             float d0 = 0.f, d1 = 0.f, d2 = 0.f;  // colour composited in this segment
             const int ns = segn[warp][sg];
-            const uint8_t *wls = &wl[warp][sg * SEG];
+            const int *wls = &wl[warp][sg * SEGP];
             // phase 2 (sequential per pixel): composite the warp's list front to back, FG entries
             // at a time: their alphas (record loads, power, SFU exp) are independent and computed
             // first, then the compositing recurrence (T, C) runs over them branch-free -- the
             // latency of the independent part overlaps across the group
-            constexpr int FG = 8;
             for (int t = 0; t < ns; t += FG) {
                 if (__all_sync(0xffffffffu, done)) break;
-                const uint2 jw = *reinterpret_cast<const uint2 *>(&wls[t]);
+                const int4 ja = *reinterpret_cast<const int4 *>(&wls[t]);
+                const int4 jb = *reinterpret_cast<const int4 *>(&wls[t + 4]);
+                const int jj[FG] = {ja.x, ja.y, ja.z, ja.w, jb.x, jb.y, jb.z, jb.w};
                 float al[FG], cr[FG], cg[FG], cb[FG];
                 bool ok[FG];
 #pragma unroll
                 for (int k = 0; k < FG; k++) {
-                    // slots past the list end hold stale indices: use entry t's (finite data)
-                    const int j = t + k < ns ? ((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff : (jw.x & 0xff);
+                    const int j = jj[k];  // past the list end: the padding (record 0)
                     const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
                     float dx, dy;
                     const float p = pixel_power(fx, fy, g0, g1.x, dx, dy);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                     d2 += cb[k] * w;
                     T = take ? test_T : T;
                     composited += take ? 1u : 0u;
-                    if (take) last = (uint32_t)(b0 + (((k < 4 ? jw.x : jw.y) >> (8 * (k & 3))) & 0xff) + 1);
+                    if (take) last = (uint32_t)(b0 + jj[k] + 1);
                 }
             }
             c0 += d0;
