@@ -193,8 +193,10 @@ class Adam:
         self.t_dev = torch.zeros(1, dtype=torch.int64, device=params.device)
 
     def use_device_step(self):
-        """Switch the fused backward+Adam to the device-resident step counter (keeps the count)."""
-        self.t_dev.fill_(self.t)
+        """Switch the fused backward+Adam to the device-resident step counter (keeps the count;
+        a no-op once switched)."""
+        if not self.device_step:
+            self.t_dev.fill_(self.t)
         self.device_step = True
 
     def step(self, grads: torch.Tensor, zero_grads: bool = True, g_begin: int = 0, g_end: int | None = None):
