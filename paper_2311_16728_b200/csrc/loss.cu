@@ -7,7 +7,8 @@
 // then a vertical 11-tap pass over the five moment maps (x, y, x^2, y^2, xy).  The gradient
 // is the windowed-correlation form: dSSIM/dx_p = (w * A)_p + 2 x_p (w * B)_p + y_p (w * C)_p
 // with A = dS/dmu_x, B = dS/dE[x^2], C = dS/dE[xy] per pixel, so a second kernel applies
-// the same separable window to the three partial maps.  Loss sums are reduced per CTA; the
+// the same separable window to the three partial maps.  Both passes accumulate two maps at a
+// time with Blackwell's packed fp32x2 FFMA2 (x and y, x^2 and y^2; A and B).  Loss sums are reduced per CTA; the
 // first CTA of each view in the gradient kernel (or a one-CTA-per-view kernel when no gradient
 // is requested) sums that view's partials in a fixed order (deterministic) and writes the loss.
 #include <cmath>
@@ -87,7 +88,10 @@ __global__ void __launch_bounds__(NT) k_ssim_fwd(const float *__restrict__ X, co
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ float sxy[2][SH][SWP];
-    __shared__ float hm[5][SH][TW + 1];
+    // horizontal-pass results: (x, y) and (x^2, y^2) as float2 pairs, xy alone -- the passes run
+    // on packed fp32x2 FFMA2 (per-element fused multiply-add, the same rounding as the scalar FFMA)
+    __shared__ float2 hm2[2][SH][TW + 1];
+    __shared__ float hm1[SH][TW + 1];
     float (*sx)[SWP] = sxy[0];
     float (*sy)[SWP] = sxy[1];
     __shared__ float red[2][NT / 32];
@@ -100,50 +104,71 @@ __global__ void __launch_bounds__(NT) k_ssim_fwd(const float *__restrict__ X, co
     // horizontal pass: SH rows x TW columns of the five moment maps (x, y, x^2, y^2, xy)
     for (int it = tid; it < SH * (TW / HC); it += NT) {
         const int r = it / (TW / HC), c0 = (it % (TW / HC)) * HC;
-        float a[HC] = {}, b[HC] = {}, aa[HC] = {}, bb[HC] = {}, ab[HC] = {};
+        float2 m1[HC], m2[HC];  // (x, y), (x^2, y^2)
+        float mxy[HC];
+#pragma unroll
+        for (int o = 0; o < HC; o++) {
+            m1[o] = m2[o] = make_float2(0.f, 0.f);
+            mxy[o] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < 10 + HC; j++) {
-            const float xv = sx[r][c0 + j], yv = sy[r][c0 + j];
-            const float xx = xv * xv, yy = yv * yv, xy = xv * yv;
+            const float2 v = make_float2(sx[r][c0 + j], sy[r][c0 + j]);
+            const float2 vv = __fmul2_rn(v, v);
+            const float xy = v.x * v.y;
 #pragma unroll
             for (int o = 0; o < HC; o++) {
                 const int t = j - o;  // tap index of input j for output o
                 if (t >= 0 && t < 11) {
                     const float w = win.g[t];
-                    a[o] += w * xv;
-                    b[o] += w * yv;
-                    aa[o] += w * xx;
-                    bb[o] += w * yy;
-                    ab[o] += w * xy;
+                    const float2 w2 = make_float2(w, w);
+                    m1[o] = __ffma2_rn(w2, v, m1[o]);
+                    m2[o] = __ffma2_rn(w2, vv, m2[o]);
+                    mxy[o] = __fmaf_rn(w, xy, mxy[o]);
                 }
             }
         }
 #pragma unroll
         for (int o = 0; o < HC; o++) {
-            hm[0][r][c0 + o] = a[o];
-            hm[1][r][c0 + o] = b[o];
-            hm[2][r][c0 + o] = aa[o];
-            hm[3][r][c0 + o] = bb[o];
-            hm[4][r][c0 + o] = ab[o];
+            hm2[0][r][c0 + o] = m1[o];
+            hm2[1][r][c0 + o] = m2[o];
+            hm1[r][c0 + o] = mxy[o];
         }
     }
     __syncthreads();
     // vertical pass: column c, rows r0 .. r0 + VR - 1
     const int c = tid % TW, r0 = (tid / TW) * VR;
-    float mom[5][VR] = {};
+    float2 v1[VR], v2[VR];
+    float vxy[VR];
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        v1[o] = v2[o] = make_float2(0.f, 0.f);
+        vxy[o] = 0.f;
+    }
 #pragma unroll
     for (int j = 0; j < 10 + VR; j++) {
-        float v[5];
-#pragma unroll
-        for (int m = 0; m < 5; m++) v[m] = hm[m][r0 + j][c];
+        const float2 p1 = hm2[0][r0 + j][c], p2 = hm2[1][r0 + j][c];
+        const float pxy = hm1[r0 + j][c];
 #pragma unroll
         for (int o = 0; o < VR; o++) {
             const int t = j - o;
             if (t >= 0 && t < 11) {
-#pragma unroll
-                for (int m = 0; m < 5; m++) mom[m][o] += win.g[t] * v[m];
+                const float w = win.g[t];
+                const float2 w2 = make_float2(w, w);
+                v1[o] = __ffma2_rn(w2, p1, v1[o]);
+                v2[o] = __ffma2_rn(w2, p2, v2[o]);
+                vxy[o] = __fmaf_rn(w, pxy, vxy[o]);
             }
         }
+    }
+    float mom[5][VR];
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        mom[0][o] = v1[o].x;
+        mom[1][o] = v1[o].y;
+        mom[2][o] = v2[o].x;
+        mom[3][o] = v2[o].y;
+        mom[4][o] = vxy[o];
     }
     float l1 = 0.f, S_sum = 0.f;
     const int gx = blockIdx.x * TW + c;
@@ -237,7 +262,8 @@ __global__ void __launch_bounds__(NT) k_ssim_bwd(const float *__restrict__ X, co
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ float s[3][SH][SWP];
-    __shared__ float hm[3][SH][TW + 1];
+    __shared__ float2 hm2[SH][TW + 1];  // (A, B) pairs for packed FFMA2; C alone
+    __shared__ float hm1[SH][TW + 1];
     const int plane = blockIdx.z;
     const int64_t HW = (int64_t)H * W;
     const int tid = threadIdx.x;
@@ -258,45 +284,64 @@ __global__ void __launch_bounds__(NT) k_ssim_bwd(const float *__restrict__ X, co
     __syncthreads();
     for (int it = tid; it < SH * (TW / HC); it += NT) {
         const int r = it / (TW / HC), c0 = (it % (TW / HC)) * HC;
-        float acc[3][HC] = {};
+        float2 ab[HC];
+        float cc[HC];
+#pragma unroll
+        for (int o = 0; o < HC; o++) {
+            ab[o] = make_float2(0.f, 0.f);
+            cc[o] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < 10 + HC; j++) {
-            float v[3];
-#pragma unroll
-            for (int m = 0; m < 3; m++) v[m] = s[m][r][c0 + j];
+            const float2 v = make_float2(s[0][r][c0 + j], s[1][r][c0 + j]);
+            const float vc = s[2][r][c0 + j];
 #pragma unroll
             for (int o = 0; o < HC; o++) {
                 const int t = j - o;
                 if (t >= 0 && t < 11) {
-#pragma unroll
-                    for (int m = 0; m < 3; m++) acc[m][o] += win.g[t] * v[m];
+                    const float w = win.g[t];
+                    ab[o] = __ffma2_rn(make_float2(w, w), v, ab[o]);
+                    cc[o] = __fmaf_rn(w, vc, cc[o]);
                 }
             }
         }
 #pragma unroll
         for (int o = 0; o < HC; o++) {
-#pragma unroll
-            for (int m = 0; m < 3; m++) hm[m][r][c0 + o] = acc[m][o];
+            hm2[r][c0 + o] = ab[o];
+            hm1[r][c0 + o] = cc[o];
         }
     }
     __syncthreads();
     // the first CTA of each view also reduces that view's loss partials (written by k_ssim_fwd)
     if (blockIdx.x == 0 && blockIdx.y == 0 && plane % 3 == 0)
         finalize_view(part, plane / 3, gridDim.x * gridDim.y, lambda, invN, loss);
-    float acc[3][VR] = {};
+    float2 vab[VR];
+    float vc[VR];
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        vab[o] = make_float2(0.f, 0.f);
+        vc[o] = 0.f;
+    }
 #pragma unroll
     for (int j = 0; j < 10 + VR; j++) {
-        float v[3];
-#pragma unroll
-        for (int m = 0; m < 3; m++) v[m] = hm[m][r0 + j][c];
+        const float2 p = hm2[r0 + j][c];
+        const float pc = hm1[r0 + j][c];
 #pragma unroll
         for (int o = 0; o < VR; o++) {
             const int t = j - o;
             if (t >= 0 && t < 11) {
-#pragma unroll
-                for (int m = 0; m < 3; m++) acc[m][o] += win.g[t] * v[m];
+                const float w = win.g[t];
+                vab[o] = __ffma2_rn(make_float2(w, w), p, vab[o]);
+                vc[o] = __fmaf_rn(w, pc, vc[o]);
             }
         }
+    }
+    float acc[3][VR];
+#pragma unroll
+    for (int o = 0; o < VR; o++) {
+        acc[0][o] = vab[o].x;
+        acc[1][o] = vab[o].y;
+        acc[2][o] = vc[o];
     }
     if (gx >= W) return;
 #pragma unroll
