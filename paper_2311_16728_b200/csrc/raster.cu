@@ -41,6 +41,7 @@ constexpr float T_STOP = 1e-4f;
 constexpr float POWER_CUT = -4.5f;
 constexpr int BATCH = 256;  // records per staged batch (list indices fit in a byte)
 constexpr int FEW_CHUNK = 5;  // chunked backward: per-lane atomics for entries with <= 5 contributing lanes
+constexpr int FEW_TILE = 6;   // tile backward: the same for <= 6 lanes (measured: 2, 4, 6, 8, 12)
 
 // power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order
 __device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float C, float &dx, float &dy) {
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ r
         __syncwarp();
         for (int t = 0; t < nsel; t++) {
             const int j = wl[warp][t];
-            bwd2_entry<2>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, red_off, g2dv);
+            bwd2_entry<FEW_TILE>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, red_off, g2dv);
         }
     }
 }
