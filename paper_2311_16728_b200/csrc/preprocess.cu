@@ -206,16 +206,45 @@ __device__ __forceinline__ void cam_centre(const gs_camera &cam, float C[3]) {
     for (int k = 0; k < 3; k++) C[k] = -(cam.R[k] * cam.t[0] + cam.R[3 + k] * cam.t[1] + cam.R[6 + k] * cam.t[2]);
 }
 
+// SH colour of a Gaussian at (px, py, pz) seen from cam: c = max(0, sum_l SH_l Y_l(dir) + 0.5),
+// dir = normalize(P - C_cam) (R6); shc = its 3 NC coefficients, [l][channel]
 template <int D>
+__device__ __forceinline__ void sh_colour(const gs_camera &cam, float px, float py, float pz, const float *shc,
+                                          float rgb[3]) {
+    constexpr int NC = (D + 1) * (D + 1);
+    float Cc[3];
+    cam_centre(cam, Cc);
+    float dx = px - Cc[0], dy = py - Cc[1], dz = pz - Cc[2];
+    float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+    float Y[16];
+    sh_basis<D>(dx * inv, dy * inv, dz * inv, Y);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+        float acc = 0.5f;
+#pragma unroll
+        for (int l = 0; l < NC; l++) acc += shc[3 * l + ch] * Y[l];
+        rgb[ch] = fmaxf(acc, 0.0f);
+    }
+}
+
+template <int D, bool SPLIT>
 __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int64_t n, int64_t ld,
                                                const CamBatch &cams, int V, const Layout &L, char *ws,
                                                bool count_tiles, bool smem_cnt, uint32_t *s_cnt, int64_t i) {
     constexpr int NC = (D + 1) * (D + 1);
-    // every load of the Gaussian is issued before the projection chain (the kernel is bound by
-    // memory latency; culled lanes' SH sectors are fetched for the warp's visible lanes anyway)
-    float shc[3 * NC];
+    // SPLIT (one or two views): two phases, the geometry of every view first (rows 0..10), then
+    // -- only for a Gaussian visible in some view -- its 3 NC SH coefficients and the colour of
+    // its visible views, so the SH registers are never live together with the projection's
+    // (79 instead of 123 registers at D = 3: more warps in flight for this latency-bound kernel).
+    // Otherwise one phase with every load issued before the projection chain: with many views
+    // the records outgrow L2 and the split's two half-record writes per (view, Gaussian) cost
+    // more than the occupancy gains (A1).
+    uint64_t vis_views = 0;
+    float shc[SPLIT ? 1 : 3 * NC];
+    if constexpr (!SPLIT) {
 #pragma unroll
-    for (int k = 0; k < 3 * NC; k++) shc[k] = P[(11 + k) * ld + i];
+        for (int k = 0; k < 3 * NC; k++) shc[k] = P[(11 + k) * ld + i];
+    }
     float px = P[i], py = P[ld + i], pz = P[2 * ld + i];
     Cov3 cv = cov3_recipe(P[3 * ld + i], P[4 * ld + i], P[5 * ld + i], P[6 * ld + i], P[7 * ld + i], P[8 * ld + i],
                           P[9 * ld + i]);
@@ -240,26 +269,21 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
             continue;
         }
         any_vis = true;
-        // SH colour, dir = normalize(P - C_cam) (R6)
-        float Cc[3];
-        cam_centre(cam, Cc);
-        float dx = px - Cc[0], dy = py - Cc[1], dz = pz - Cc[2];
-        float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-        float Y[16];
-        sh_basis<D>(dx * inv, dy * inv, dz * inv, Y);
-        float rgb[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ch++) {
-            float acc = 0.5f;
-#pragma unroll
-            for (int l = 0; l < NC; l++) acc += shc[3 * l + ch] * Y[l];
-            rgb[ch] = fmaxf(acc, 0.0f);
-        }
+        vis_views |= 1ull << v;
         rec0[m] = make_float4(p.u, p.v, p.A, p.B);
-        rec1[m] = make_float4(p.C, sigma, rgb[0], rgb[1]);
         // padded exact 3-sigma extents of the ellipse d^T Q d <= 9 (Q^-1 = Sigma2' = [[a, b], [b, c]]):
         // used by the raster kernels for a conservative warp-level skip test
-        rec2[m] = make_float4(rgb[2], 3.0f * sqrtf(p.a) * 1.0001f + 1e-3f, 3.0f * sqrtf(p.c) * 1.0001f + 1e-3f, 0.f);
+        const float ea = 3.0f * sqrtf(p.a) * 1.0001f + 1e-3f, ec = 3.0f * sqrtf(p.c) * 1.0001f + 1e-3f;
+        if constexpr (SPLIT) {  // rec1.zw, rec2.x: the colour, phase 2
+            reinterpret_cast<float2 *>(rec1 + m)[0] = make_float2(p.C, sigma);
+            reinterpret_cast<float *>(rec2 + m)[1] = ea;
+            reinterpret_cast<float2 *>(rec2 + m)[1] = make_float2(ec, 0.f);
+        } else {
+            float rgb[3];
+            sh_colour<D>(cam, px, py, pz, shc, rgb);
+            rec1[m] = make_float4(p.C, sigma, rgb[0], rgb[1]);
+            rec2[m] = make_float4(rgb[2], ea, ec, 0.f);
+        }
         depth[m] = p.z;
         radius[m] = p.r;
         rect[m] = make_int4(p.x0, p.y0, p.x1, p.y1);
@@ -292,6 +316,21 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
         g2d[3 * m + 1] = zero;
         g2d[3 * m + 2] = zero;
     }
+    // phase 2 (SPLIT): the SH colour of the visible views
+    if (SPLIT && vis_views) {
+        float sh2[3 * NC];
+#pragma unroll
+        for (int k = 0; k < 3 * NC; k++) sh2[k] = P[(11 + k) * ld + i];
+        do {
+            const int v = __ffsll((long long)vis_views) - 1;
+            vis_views &= vis_views - 1;
+            const int64_t m = (int64_t)v * n + i;
+            float rgb[3];
+            sh_colour<D>(cams.c[v], px, py, pz, sh2, rgb);
+            reinterpret_cast<float2 *>(rec1 + m)[1] = make_float2(rgb[0], rgb[1]);
+            reinterpret_cast<float *>(rec2 + m)[0] = rgb[2];
+        } while (vis_views);
+    }
     // compacted list of Gaussians visible in some view (warp-aggregated append) so that the
     // backward chain runs on full warps of visible Gaussians only
     unsigned active = __activemask();
@@ -311,7 +350,7 @@ __device__ __forceinline__ void preprocess_one(const float *__restrict__ P, int6
     at<uint32_t>(ws, L.slot)[i] = slot;
 }
 
-template <int D>
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P, int64_t n, int64_t ld,
                                                     const CamBatch cams, int V, Layout L, char *ws,
                                                     bool count_tiles) {
@@ -325,7 +364,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float *__restrict__ P,
         __syncthreads();
     }
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) preprocess_one<D>(P, n, ld, cams, V, L, ws, count_tiles, smem_cnt, s_cnt, i);
+    if (i < n) preprocess_one<D, SPLIT>(P, n, ld, cams, V, L, ws, count_tiles, smem_cnt, s_cnt, i);
     if (smem_cnt) {  // one global add per (CTA, tile) into the padded counters
         __syncthreads();
         uint32_t *tc = at<uint32_t>(ws, L.tile_count);
@@ -527,16 +566,29 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     if (gnorm) gnorm[i] = gnorm_old + norm_acc;
 }
 
+// the two-phase A1 (geometry, then SH colour) up to this many views per call (measured: TUM
+// +2.6 %, EuRoC even, the 64-view stress step -1.6 %)
+constexpr int SPLIT_MAX_VIEWS = 2;
+
+template <int D>
+static void launch_pre(bool split, int64_t blocks, cudaStream_t s, const gs_params &p, const CamBatch &cams, int V,
+                       const Layout &L, void *ws, bool count_tiles) {
+    if (split)
+        launch_pdl(k_preprocess<D, true>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles);
+    else
+        launch_pdl(k_preprocess<D, false>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles);
+}
+
 cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
                               bool count_tiles, cudaStream_t s) {
     int64_t blocks = (p.n + 255) / 256;
     if (blocks == 0) return cudaGetLastError();
     ProfScope prof("k_preprocess", s);
     switch (p.sh_degree) {
-        case 0: launch_pdl(k_preprocess<0>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        case 1: launch_pdl(k_preprocess<1>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        case 2: launch_pdl(k_preprocess<2>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
-        default: launch_pdl(k_preprocess<3>, blocks, 256, 0, s, p.data, p.n, p.ld, cams, V, L, (char *)ws, count_tiles); break;
+        case 0: launch_pre<0>(V <= SPLIT_MAX_VIEWS, blocks, s, p, cams, V, L, ws, count_tiles); break;
+        case 1: launch_pre<1>(V <= SPLIT_MAX_VIEWS, blocks, s, p, cams, V, L, ws, count_tiles); break;
+        case 2: launch_pre<2>(V <= SPLIT_MAX_VIEWS, blocks, s, p, cams, V, L, ws, count_tiles); break;
+        default: launch_pre<3>(V <= SPLIT_MAX_VIEWS, blocks, s, p, cams, V, L, ws, count_tiles); break;
     }
     return cudaGetLastError();
 }
