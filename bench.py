@@ -404,11 +404,13 @@ def run_ours(args):
     else:
         def run_e2e(k, last):
             eng.step_host(gts_pinned[k % 2], out_pinned, None if last else gts_pinned[(k + 1) % 2])
-    # warm-up: W steps, and on for at least 0.3 s -- the graph captures above leave the GPU idle
-    # long enough for its clocks to drop, and a short warm-up then times the ramp (measured:
-    # 0.67 -> 0.617 ms per TUM step over the first ~100 ms, tools/e2e_var.py)
+    # warm-up: W steps, and on one GPU on for at least 0.3 s -- the graph captures above leave
+    # the GPU idle long enough for its clocks to drop, and a short warm-up then times the ramp
+    # (measured: 0.67 -> 0.617 ms per TUM step over the first ~100 ms, tools/e2e_var.py).  Under
+    # torchrun every rank runs the same fixed count (each step holds collectives).
     t_w, k = time.perf_counter(), 0
-    while k < max(args.warmup, 3) or time.perf_counter() - t_w < 0.3:
+    n_w = max(args.warmup, 3) + (0 if world == 1 else 16)
+    while k < n_w or (world == 1 and time.perf_counter() - t_w < 0.3):
         run_e2e(k, False)
         k += 1
         if k % 8 == 0:
