@@ -351,18 +351,33 @@ def run_ours(args):
     ms_max = float(ms_t.item())
     eng.check()
 
-    # ---- render FPS: A1-A6 at level 0 for this rank's views
-    for _ in range(3):
-        eng.render(0)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # ---- render FPS: A1-A6 at level 0 for this rank's views, eager launches and (one GPU) the
+    # replay of a CUDA graph of the same calls (the eager number carries the host's per-call cost)
+    def frame_ms(fn, nr, graph):
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                fn()
+            torch.cuda.current_stream().wait_stream(side)
+            with torch.cuda.graph(g):
+                fn()
+            fn = g.replay
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(nr):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / nr
+
     nr = 50
-    a.record(stream)
-    for _ in range(nr):
-        eng.render(0)
-    b.record(stream)
-    torch.cuda.synchronize()
-    render_ms = a.elapsed_time(b) / nr
+    render_ms_eager = frame_ms(lambda: eng.render(0), nr, False)
+    render_ms = frame_ms(lambda: eng.render(0), nr, world == 1) if world == 1 else render_ms_eager
 
     # ---- context for BASELINE.md's only comparable paper number (Table 1 render FPS on Replica
     # 1200x680, 911-1084 FPS on an RTX 4090 with ~130-140K trained Gaussians): A1-A6 of one
@@ -373,17 +388,13 @@ def run_ours(args):
         rcam = make_cameras("replica", 1)
         rr = Renderer(rscene.n, 3, 1, rcam[0].width, rcam[0].height, 1 << 23)
         rp = pack_params(rscene)
-        for _ in range(3):
-            rr.forward(rp, rcam)
+        rr.forward(rp, rcam)
         torch.cuda.synchronize()
         st, flags, pairs = rr.ws.status()
-        a.record(stream)
-        for _ in range(nr):
-            rr.forward(rp, rcam)
-        b.record(stream)
-        torch.cuda.synchronize()
+        replica_eager_ms = frame_ms(lambda: rr.forward(rp, rcam), nr, False)
+        replica_ms = frame_ms(lambda: rr.forward(rp, rcam), nr, True)
         replica = {"workload": "replica 1200x680, 500000 Gaussians, SH 3, 1 view", "pairs": int(pairs),
-                   "render_fps": 1000.0 * nr / a.elapsed_time(b),
+                   "render_fps": 1000.0 / replica_ms, "render_fps_eager": 1000.0 / replica_eager_ms,
                    "paper_render_fps_rtx4090": [911.262, 1084.017],
                    "paper_note": "PAPER.md:416-417,444-445 (mono, RGB-D; trained maps of 31-35 MB): context only"}
         del rr, rp
@@ -519,6 +530,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "render_fps": 1000.0 / render_ms * len(cams) * world,
+            "render_fps_eager": 1000.0 / render_ms_eager * len(cams) * world,
             "render_replica": replica,
             "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
             "timing": {"headline": "CUDA graph replay per step" if use_graph else "eager launches",
