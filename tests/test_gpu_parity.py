@@ -199,7 +199,7 @@ def test_forward_parity_tiny_full_image():
     assert (ref["ncomp"] > 0).mean() > 0.3
 
 
-@pytest.mark.parametrize("cfg,views,level", [("tum", 1, 0), ("tum", 1, 2), ("euroc", 4, 1), ("replica", 1, 0)])
+@pytest.mark.parametrize("cfg,views,level", [("tum", 1, 0), ("tum", 1, 2), ("euroc", 4, 1), ("euroc", 2, 0), ("replica", 1, 0)])
 def test_forward_parity_full_size_sampled(cfg, views, level):
     scene = make_scene(cfg)
     cams = [scaled_camera(c, level) for c in make_cameras(cfg, views)]
