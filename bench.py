@@ -109,7 +109,8 @@ def oracle_sample_step(cfg_name: str, rank_view: int = 0, n_pix: int = 4096, see
     and the fp64 Adam step over every parameter.  Returns (seconds extrapolated to the full
     step, seconds actually spent, description)."""
     import oracle.oracle as orc
-    from synth import config, make_cameras, make_scene, perturb, scaled_camera
+    from synth import config, make_cameras, make_scene, perturb
+    scaled_camera = orc.level_camera
     cfg = config(cfg_name)
     scene = perturb(make_scene(cfg), 99)
     cam0 = make_cameras(cfg, rank_view + 1)[rank_view]
@@ -278,6 +279,7 @@ def run_ours(args):
                     sh.t += 1
                     sh._adam_rows()
                     all_gather_rows(sh.padded_params, sh.R)
+                    sh.padded_grads.zero_()
                 else:
                     reduce_gradients(eng.grads)
                     e[5].record(); eng.adam.step(eng.grads, zero_grads=True)
@@ -445,6 +447,9 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+    if e2e_graph:
+        eng.pipeline_check()  # raises if a timed step overflowed its pair capacity (rendered nothing)
+    eng.check()
 
     # ---- rooflines.  Dominant kernel: the raster backward (A8), FP32-ALU bound: algorithmic
     # FLOPs = evaluated pairs x 13 + composited pairs x 45 against 148 SMs x 128 FP32

@@ -243,6 +243,18 @@ gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, floa
    GS_ERR_CAPACITY if bit 0 is set. */
 gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs);
 
+/* Enqueues on stream a copy of the workspace status into dst[0..1] (device or pinned host
+   int32): dst[0] = flags (bit 0 = pair capacity overflow of the last gs_preprocess: that call's
+   outputs are invalid), dst[1] = its pair count.  Does not synchronise, so it can sit inside a
+   captured CUDA graph (the end-to-end step reads it back with its losses).
+   GS_ERR_INVALID_ARG for a NULL pointer or a buffer smaller than a workspace header. */
+gs_status gs_status_async(const void *ws, size_t ws_bytes, int32_t *dst, gs_stream_t stream);
+
+/* Forgets the forward-state token of ws (SPEC.md:355-359 StaleRenderState check): call before
+   freeing a workspace, so that a new workspace allocated at the same address cannot pass the
+   check with the old one's token.  GS_ERR_INVALID_ARG for NULL. */
+gs_status gs_workspace_release(const void *ws);
+
 const char *gs_status_str(gs_status s);
 
 /* ---- Map layout (not a step of the method): spatial order.

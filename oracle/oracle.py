@@ -85,6 +85,27 @@ def _scene_args(scene):
     return arrs, [C.c_int64(scene.means.shape[0]), C.c_int(D)] + [_p(a) for a in arrs]
 
 
+def level_camera(cam, level: int):
+    """The camera of Gaussian-pyramid level l, as the oracle reads the paper: Eq. 5 renders
+    I_r^l at the level's own resolution (R19), a pinhole camera scaled by
+    2^-l (pixel centres at integers, R12: u_l = fx/2^l x/z + cx/2^l), size ceil-halved per level
+    (SPEC.md:402), tan clamp of R15 (1.3 (W/2)/fx) recomputed at the level's size.  Values are
+    fp32 like gs_camera."""
+    import dataclasses
+    import math
+    if level == 0:
+        return cam
+    H, W = cam.height, cam.width
+    for _ in range(level):
+        H, W = (H + 1) // 2, (W + 1) // 2
+    s = 0.5 ** level
+    fx, fy = np.float32(cam.fx * s).item(), np.float32(cam.fy * s).item()
+    lim_x = cam.lim_x if math.isinf(cam.lim_x) else np.float32(1.3 * (0.5 * W) / fx).item()
+    lim_y = cam.lim_y if math.isinf(cam.lim_y) else np.float32(1.3 * (0.5 * H) / fy).item()
+    return dataclasses.replace(cam, fx=fx, fy=fy, cx=np.float32(cam.cx * s).item(),
+                               cy=np.float32(cam.cy * s).item(), width=W, height=H, lim_x=lim_x, lim_y=lim_y)
+
+
 def project(scene, cam, mode="recipe") -> dict:
     arrs, sargs = _scene_args(scene)
     n = scene.means.shape[0]

@@ -28,7 +28,7 @@ EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
            "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
            "gs_densify_plan", "gs_densify_apply", "gs_densify_tags", "gs_geometry_densify",
-           "gs_query_status", "gs_status_str", "gs_spatial_order_temp_size", "gs_spatial_order",
+           "gs_query_status", "gs_status_async", "gs_workspace_release", "gs_status_str", "gs_spatial_order_temp_size", "gs_spatial_order",
            "gs_permute_columns", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
@@ -281,6 +281,20 @@ def gs_query_status(ws: torch.Tensor, stream=None):
     p = C.c_int64()
     s = lib().gs_query_status(_ptr(ws), C.c_size_t(ws.numel()), _stream(stream), C.byref(f), C.byref(p))
     return s, f.value, p.value
+
+
+def gs_status_async(ws: torch.Tensor, dst: torch.Tensor, stream=None):
+    """Enqueue {flags, pairs} of the workspace into dst (int32[2], device or pinned host)."""
+    if dst.dtype != torch.int32 or dst.numel() < 2 or not dst.is_contiguous():
+        raise ValueError("dst must be a contiguous int32 tensor of >= 2 elements")
+    if not dst.is_cuda and not dst.is_pinned():
+        raise ValueError("dst must be device or pinned host memory")
+    _check(lib().gs_status_async(_ptr(ws), C.c_size_t(ws.numel()), C.c_void_p(dst.data_ptr()), _stream(stream)),
+           "gs_status_async")
+
+
+def gs_workspace_release(ws: torch.Tensor):
+    _check(lib().gs_workspace_release(C.c_void_p(ws.data_ptr())), "gs_workspace_release")
 
 
 def gs_spatial_order_temp_size(n) -> int:

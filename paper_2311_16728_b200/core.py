@@ -83,6 +83,15 @@ class Workspace:
         """(status, flags, pairs) -- synchronises the current stream."""
         return L.gs_query_status(self.buf)
 
+    def __del__(self):
+        # the library's forward-state token is keyed by the buffer address, which the caching
+        # allocator may hand to the next workspace: forget it with the buffer
+        try:
+            if getattr(self, "buf", None) is not None:
+                L.gs_workspace_release(self.buf)
+        except Exception:
+            pass
+
 
 class Renderer:
     """A1-A6 forward and A8-A9 backward over one workspace."""

@@ -466,6 +466,20 @@ gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, i
     return (h.flags & 1u) ? GS_ERR_CAPACITY : GS_OK;
 }
 
+gs_status gs_status_async(const void *ws, size_t ws_bytes, int32_t *dst, gs_stream_t stream) {
+    if (!ws || !dst || ws_bytes < sizeof(WsHeader)) return GS_ERR_INVALID_ARG;
+    // WsHeader starts with {flags, P}: one async 8-byte copy (a memcpy node when captured)
+    if (cudaMemcpyAsync(dst, ws, sizeof(uint32_t) * 2, cudaMemcpyDefault, (cudaStream_t)stream) != cudaSuccess)
+        return GS_ERR_CUDA;
+    return GS_OK;
+}
+
+gs_status gs_workspace_release(const void *ws) {
+    if (!ws) return GS_ERR_INVALID_ARG;
+    g_tokens.erase(ws);
+    return GS_OK;
+}
+
 const char *gs_status_str(gs_status s) {
     switch (s) {
         case GS_OK: return "ok";

@@ -10,12 +10,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from synth import densify_samples, scaled_camera
-
 from . import _lib as L
 from .core import (Adam, AdamConfig, DensifyConfig, PhotometricLoss, Renderer, densify, gaussian_pyramid,
                    geometry_densify, level_shapes, pack_params, permute_columns)
 from .core import spatial_order as core_spatial_order
+from .levels import densify_samples, level_camera
 
 
 def gp_level(iteration: int, n_levels: int, iters_per_level: int) -> int:
@@ -79,7 +78,11 @@ class ShardedAdam:
     rows, Adam on this rank's rows only (gs_adam_step_rows; m and v exist for those rows only,
     1/world of the optimiser state), all-gather of the updated parameter rows.  Same NVLink volume
     as the all-reduce, 1/world of the Adam bytes.  `params` / `grads` are the first K rows of
-    padded [world R][ld] buffers (`padded_params`, `padded_grads`)."""
+    padded [world R][ld] buffers (`padded_params`, `padded_grads`).
+
+    The backward ADDS into `grads` (gs.h gs_render_backward), so after a step the whole padded
+    gradient buffer is zeroed: the reduce-scatter leaves partial or summed gradients in the rows
+    other ranks own, and re-adding them next iteration would apply stale gradient."""
 
     def __init__(self, padded_params: torch.Tensor, padded_grads: torch.Tensor, n: int, sh_degree: int,
                  cfg: AdamConfig | None = None, group=None):
@@ -88,21 +91,44 @@ class ShardedAdam:
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.K = param_rows(sh_degree)
         self.R, self.r0, self.r1 = row_shard(self.K, self.rank, self.world)
-        assert padded_params.shape[0] == self.world * self.R and padded_grads.shape == padded_params.shape
-        self.padded_params, self.padded_grads = padded_params, padded_grads
-        self.params, self.grads = padded_params[:self.K], padded_grads[:self.K]
         self.n, self.D = n, sh_degree
         self.cfg = cfg or AdamConfig()
         self.hp = self.cfg.struct()
-        ld = padded_params.shape[1]
-        self.m = torch.zeros((max(self.r1 - self.r0, 1), ld), dtype=torch.float32, device=padded_params.device)
-        self.v = torch.zeros_like(self.m)
         self.t = 0
+        self.rebind(padded_params, padded_grads, n)
+
+    def rebind(self, padded_params: torch.Tensor, padded_grads: torch.Tensor, n: int,
+               m_full: torch.Tensor | None = None, v_full: torch.Tensor | None = None):
+        """New parameter / gradient buffers (after densification); m_full / v_full: the full
+        [>= K][ld] moments of the new map (every rank passes the same), of which this rank keeps
+        its rows; None = zero moments."""
+        assert padded_params.shape[0] == self.world * self.R and padded_grads.shape == padded_params.shape
+        self.padded_params, self.padded_grads = padded_params, padded_grads
+        self.params, self.grads = padded_params[:self.K], padded_grads[:self.K]
+        self.n = n
+        ld = padded_params.shape[1]
+        # R rows (not r1 - r0): every rank's moment chunk has the same size for full_state()'s gather
+        self.m = torch.zeros((self.R, ld), dtype=torch.float32, device=padded_params.device)
+        self.v = torch.zeros_like(self.m)
+        for mine, full in ((self.m, m_full), (self.v, v_full)):
+            if full is not None and self.r1 > self.r0:
+                mine[:self.r1 - self.r0] = full[self.r0:self.r1]
+
+    def full_state(self) -> tuple:
+        """All-gather of the moment rows: (m, v) as [world R][ld] tensors, rows [0, K) valid --
+        what densification needs to move the optimiser state with its Gaussians."""
+        out = []
+        for mine in (self.m, self.v):
+            full = torch.zeros((self.world * self.R, mine.shape[1]), dtype=mine.dtype, device=mine.device)
+            full[self.rank * self.R:(self.rank + 1) * self.R] = mine
+            all_gather_rows(full, self.R, self.group)
+            out.append(full)
+        return tuple(out)
 
     def _adam_rows(self):
         from . import _lib as L
         ps = L.params_struct(self.params, self.n, self.D)
-        L.gs_adam_step_rows(ps, self.grads, self.m, self.v, self.hp, self.t, self.r0, self.r1, True)
+        L.gs_adam_step_rows(ps, self.grads, self.m, self.v, self.hp, self.t, self.r0, self.r1, False)
 
     def step(self):
         reduce_scatter_rows(self.padded_grads, self.R, self.group)   # A10
@@ -110,6 +136,7 @@ class ShardedAdam:
         if self.r1 > self.r0:
             self._adam_rows()                                          # A11 on this rank's rows
         all_gather_rows(self.padded_params, self.R, self.group)       # replicas identical again
+        self.padded_grads.zero_()                                      # no row may carry into the next +=
 
 
 class MappingEngine:
@@ -139,13 +166,13 @@ class MappingEngine:
             packed = permute_columns(packed, perm, self.n)
             self.order = perm.to(torch.int64)
         self.sharded = None
-        if shard_optimizer and self.distributed():
+        self._pipe = None
+        self._status = None
+        self.graph = None
+        if shard_optimizer and dist.is_available() and dist.is_initialized():
             # reduce-scatter -> row-sharded Adam -> all-gather (parameters / gradients live in
             # the first K rows of buffers padded to world x R rows)
-            world = dist.get_world_size(group)
-            R, _, _ = row_shard(packed.shape[0], 0, world)
-            pp = torch.zeros((world * R, packed.shape[1]), dtype=torch.float32, device=device)
-            pp[:packed.shape[0]] = packed
+            pp = self._padded(packed)
             self.sharded = ShardedAdam(pp, torch.zeros_like(pp), self.n, self.D, adam, group)
             self.params, self.grads = self.sharded.params, self.sharded.grads
         else:
@@ -168,7 +195,7 @@ class MappingEngine:
         self.group = group
         H, W = self.cams0[0].height, self.cams0[0].width
         self.shapes = level_shapes(H, W, n_levels)
-        self.cams = [[scaled_camera(c, l) for c in self.cams0] for l in range(n_levels + 1)]
+        self.cams = [[level_camera(c, l) for c in self.cams0] for l in range(n_levels + 1)]
         self.gt0 = torch.empty((self.V, 3, H, W), dtype=torch.float32, device=device)
         self.set_keyframes(gts)
         self.losses = [PhotometricLoss(self.V, h, w, lam, device) for (h, w) in self.shapes]
@@ -240,12 +267,14 @@ class MappingEngine:
         r = self.renderers[level]
         cams = self.cams[level]
         rgb, _ = r.forward(self.params, cams, self.bg)                       # A1-A6
+        if self._status is not None:  # overflow flag + pair count, read back with the losses
+            L.gs_status_async(r.ws.buf, self._status[level])
         if self.densify_cfg is not None:                                     # f1 statistics
             L.gs_densify_stats(L.params_struct(self.params, self.n, self.D), cams, r.ws.buf, self.vis_count,
                                self.max_radius)
         loss, dL = self.losses[level](rgb, self._pyramid(level))             # A7
         if fused is None:
-            fused = not self.distributed()
+            fused = self.sharded is None and not self.distributed()
         if fused:
             r.backward_adam(self.params, cams, dL, self.adam, self.grad2d_norm, self.bg)  # A8-A9 + A11
         else:
@@ -261,6 +290,41 @@ class MappingEngine:
         """One pass of the Eq. 5 schedule: iterations at levels n, n-1, ..., 0."""
         return [self.iteration(l) for l in range(self.n_levels, -1, -1)]
 
+    # ------------------------------------------------------------------ map replacement
+    def _padded(self, p: torch.Tensor) -> torch.Tensor:
+        """[K][ld] -> [world R][ld] (rows K.. zero), the sharded optimiser's buffer shape."""
+        world = dist.get_world_size(self.group)
+        R, _, _ = row_shard(p.shape[0], 0, world)
+        pp = torch.zeros((world * R, p.shape[1]), dtype=torch.float32, device=p.device)
+        pp[:p.shape[0]] = p
+        return pp
+
+    def _moments(self) -> tuple:
+        """The full [K][ld] Adam moments of the current map (all-gathered when row-sharded)."""
+        if self.sharded is not None:
+            m, v = self.sharded.full_state()
+            K = self.params.shape[0]
+            return m[:K], v[:K]
+        return self.adam.m, self.adam.v
+
+    def _install(self, p: torch.Tensor, m: torch.Tensor, v: torch.Tensor, n: int):
+        """Replace the map by p (moments m, v; [K][ld'], n Gaussians): optimiser state, gradient
+        buffers and per-level workspaces follow; captured graphs refer to the old buffers and are
+        dropped."""
+        self.n = n
+        if self.sharded is not None:
+            pp = self._padded(p)
+            self.sharded.rebind(pp, torch.zeros_like(pp), n, m, v)
+            self.params, self.grads = self.sharded.params, self.sharded.grads
+        else:
+            self.params = p
+            self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, n
+            self.grads = torch.zeros_like(p)
+        self.renderers = [None] * (self.n_levels + 1)
+        self.graph = None   # a captured step refers to the old buffers
+        self._pipe = None
+        self.calibrate()
+
     # ------------------------------------------------------------------ densify and prune (f1)
     def densify_and_prune(self, seed: int) -> tuple:
         """SPEC.md:463-471 with the statistics gathered since the last call (needs densify_cfg):
@@ -270,8 +334,6 @@ class MappingEngine:
         max) so every rank takes the same decisions with the same samples."""
         if self.densify_cfg is None:
             raise RuntimeError("densify_and_prune needs MappingEngine(densify_cfg=...)")
-        if self.sharded is not None:
-            raise NotImplementedError("densify with the row-sharded optimiser (use shard_optimizer=False)")
         if self.distributed():
             dist.all_reduce(self.grad2d_norm, group=self.group)
             dist.all_reduce(self.vis_count, group=self.group)
@@ -279,25 +341,21 @@ class MappingEngine:
         z = torch.from_numpy(densify_samples(self.n, seed)).to(self.params.device)
         H, W = self.shapes[0]
         cfg = self.densify_cfg.struct(W, H)
-        p, m, v, counts, tags = densify(self.params, self.n, self.D, self.adam.m, self.adam.v, self.grad2d_norm,
+        m0, v0 = self._moments()
+        p, m, v, counts, tags = densify(self.params, self.n, self.D, m0, v0, self.grad2d_norm,
                                         self.vis_count, self.max_radius, z, cfg, tags=self.temporary)
-        self.n = counts[3]
-        if self.spatial_order and self.n > 0:  # clones and split children went to the end: re-order
-            perm = core_spatial_order(p, self.n, self.D)
-            p, m, v = (permute_columns(x, perm, self.n) for x in (p, m, v))
-            tags = permute_columns(tags.to(torch.int32), perm, self.n).to(torch.uint8)
+        n = counts[3]
+        if self.spatial_order and n > 0:  # clones and split children went to the end: re-order
+            perm = core_spatial_order(p, n, self.D)
+            p, m, v = (permute_columns(x, perm, n) for x in (p, m, v))
+            tags = permute_columns(tags.to(torch.int32), perm, n).to(torch.uint8)
         self.order = None
         self.temporary = tags
-        self.params = p
-        self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, self.n
-        self.grads = torch.zeros_like(p)
         dev = p.device
-        self.grad2d_norm = torch.zeros(max(self.n, 1), dtype=torch.float32, device=dev)
-        self.vis_count = torch.zeros(max(self.n, 1), dtype=torch.float32, device=dev)
-        self.max_radius = torch.zeros(max(self.n, 1), dtype=torch.int32, device=dev)
-        self.renderers = [None] * (self.n_levels + 1)
-        self.graph = None  # a captured step refers to the old buffers
-        self.calibrate()
+        self.grad2d_norm = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+        self.vis_count = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+        self.max_radius = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+        self._install(p, m, v, n)
         return counts[:3]
 
     # ------------------------------------------------------------------ geometry densification (f2)
@@ -307,8 +365,6 @@ class MappingEngine:
         (level-0 camera), appended to the map with zero Adam moments; the workspaces are re-sized.
         uv [n, 2], active [n] (0/1), kp_depth [n] (mono), depth_map [H, W] (RGB-D, mode 1),
         image [3, H, W]; numpy or device tensors.  Returns the number of primitives added."""
-        if self.sharded is not None:
-            raise NotImplementedError("geometry densification with the row-sharded optimiser")
         dev = self.params.device
         t = lambda a, dt: None if a is None else torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a,  # noqa: E731
                                                                  dtype=dt).to(dev).contiguous()
@@ -320,18 +376,18 @@ class MappingEngine:
         n0, n1 = self.n, self.n + cnt
         K = self.params.shape[0]
         ld = L.param_ld(n1)
+        m0, v0 = self._moments()
         p = torch.zeros((K, ld), dtype=torch.float32, device=dev)
         p[:, :n0] = self.params[:, :n0]
         p[:, n0:n1] = newp[:, :cnt]
         m = torch.zeros_like(p)
         v = torch.zeros_like(p)
-        m[:, :n0] = self.adam.m[:, :n0]
-        v[:, :n0] = self.adam.v[:, :n0]
+        m[:, :n0] = m0[:, :n0]
+        v[:, :n0] = v0[:, :n0]
         grow = lambda a, fill: torch.cat([a[:n0], torch.full((cnt,), fill, dtype=a.dtype, device=dev)])  # noqa: E731
         self.temporary = grow(self.temporary, 1)
         self.grad2d_norm, self.vis_count, self.max_radius = (grow(self.grad2d_norm, 0), grow(self.vis_count, 0),
                                                              grow(self.max_radius, 0))
-        self.n = n1
         if self.spatial_order:  # the new primitives went to the end: re-order
             perm = core_spatial_order(p, n1, self.D)
             p, m, v = (permute_columns(x, perm, n1) for x in (p, m, v))
@@ -339,12 +395,7 @@ class MappingEngine:
             self.grad2d_norm, self.vis_count = (permute_columns(x, perm, n1) for x in (self.grad2d_norm, self.vis_count))
             self.max_radius = permute_columns(self.max_radius, perm, n1)
         self.order = None
-        self.params = p
-        self.adam.params, self.adam.m, self.adam.v, self.adam.n = p, m, v, n1
-        self.grads = torch.zeros_like(p)
-        self.renderers = [None] * (self.n_levels + 1)
-        self.graph = None
-        self.calibrate()
+        self._install(p, m, v, n1)
         return cnt
 
     # ------------------------------------------------------------------ CUDA graphs
@@ -353,7 +404,7 @@ class MappingEngine:
         the targets and the D2H copy of the losses) -- into a CUDA graph; `replay()` then runs it
         with a single launch.  Single GPU only (the fused backward+Adam with a device-resident
         step counter; the DP path has an NCCL collective between backward and Adam)."""
-        if self.distributed():
+        if self.distributed() or self.sharded is not None:
             raise RuntimeError("graph capture is for the single-GPU fused path")
         self.adam.use_device_step()
         side = torch.cuda.Stream()
@@ -392,32 +443,58 @@ class MappingEngine:
         for the copies.  Use either this pair or `capture()`/`replay()` on an engine, not both.
         (Measured on B200, TUM config: 0.625 ms/step vs 0.664 ms with the copies inside two
         graphs and 0.607 ms for the device-only replay, tools/e2e_probe.py.)"""
-        if self.distributed():
+        if self.distributed() or self.sharded is not None:
             raise RuntimeError("graph capture is for the single-GPU fused path")
         self.adam.use_device_step()
         bufs = [self.gt0, torch.empty_like(self.gt0)]
+        dev = bufs[0].device
+        self._status = torch.zeros((self.n_levels + 1, 2), dtype=torch.int32, device=dev)
         graphs, losses = [], []
-        for i in range(2):  # capture() also runs one real (warm-up) step on targets i
-            self.gt0 = bufs[i]
-            bufs[i].copy_(gts_pinned[i], non_blocking=True)
-            graphs.append(self.capture())
-            losses.append(self.graph_losses)
+        try:
+            for i in range(2):  # capture() also runs one real (warm-up) step on targets i
+                self.gt0 = bufs[i]
+                bufs[i].copy_(gts_pinned[i], non_blocking=True)
+                graphs.append(self.capture())
+                losses.append(self.graph_losses)
+        finally:
+            status = self._status
+            self._status = None
         self.gt0 = bufs[0]
         self.graph = None
-        dev = bufs[0].device
         self._pipe = dict(graphs=graphs, losses=losses, bufs=bufs, gts=gts_pinned, out=out_pinned, k=0,
-                          copy=torch.cuda.Stream(device=dev),
+                          copy=torch.cuda.Stream(device=dev), status=status,
+                          status_host=[torch.zeros_like(status, device="cpu").pin_memory() for _ in range(2)],
                           ev_in=[torch.cuda.Event() for _ in range(2)],
-                          ev_done=[torch.cuda.Event() for _ in range(2)])
+                          ev_done=[torch.cuda.Event() for _ in range(2)],
+                          ev_out=[torch.cuda.Event() for _ in range(2)], pending=[False, False])
         return graphs
+
+    def _pipe_check(self, i: int):
+        """Raise if step slot i's read-back status (host wait on its copy) shows a capacity
+        overflow: that step rendered nothing on the overflowing level (gs.h gs_status_async)."""
+        pp = self._pipe
+        if not pp["pending"][i]:
+            return
+        pp["ev_out"][i].synchronize()
+        pp["pending"][i] = False
+        st = pp["status_host"][i]
+        if int(st[:, 0].bitwise_and(1).any()):
+            lv = [l for l in range(st.shape[0]) if int(st[l, 0]) & 1]
+            raise RuntimeError(f"pair capacity exceeded at GP level(s) {lv} (pairs {st[:, 1].tolist()}); "
+                               "re-calibrate (MappingEngine.calibrate) and re-capture")
 
     def step_pipelined(self) -> torch.Tensor:
         """Call k of the pipelined end-to-end step (see capture_pipelined): returns the pinned
         losses buffer it fills (valid after pipeline_join() and a synchronise).  Call 0 also copies
-        its own targets (gts_pinned[0]); later calls' targets were prefetched by the previous call."""
+        its own targets (gts_pinned[0]); later calls' targets were prefetched by the previous call.
+        Call k first checks the status read back by call k - 2 (which used the same pinned
+        buffers) and raises on a pair-capacity overflow."""
         pp = self._pipe
+        if pp is None:
+            raise RuntimeError("step_pipelined needs capture_pipelined() (again, after the map was replaced)")
         k = pp["k"]
         i = k % 2
+        self._pipe_check(i)
         cs, cp = torch.cuda.current_stream(), pp["copy"]
         if k == 0:
             pp["bufs"][i].copy_(pp["gts"][i], non_blocking=True)
@@ -431,14 +508,22 @@ class MappingEngine:
         pp["graphs"][i].replay()
         pp["ev_done"][i].record(cs)
         cp.wait_event(pp["ev_done"][i])
-        with torch.cuda.stream(cp):                # this step's losses, off the compute stream
+        with torch.cuda.stream(cp):                # this step's losses and status, off the compute stream
             pp["out"][i].copy_(pp["losses"][i], non_blocking=True)
+            pp["status_host"][i].copy_(pp["status"], non_blocking=True)
+            pp["ev_out"][i].record(cp)
+        pp["pending"][i] = True
         pp["k"] = k + 1
         return pp["out"][i]
 
     def pipeline_join(self):
         """The current stream waits for the pipelined step's copies (losses read back, prefetch)."""
         torch.cuda.current_stream().wait_stream(self._pipe["copy"])
+
+    def pipeline_check(self):
+        """Host wait for the outstanding read-backs; raises on a pair-capacity overflow."""
+        for i in range(2):
+            self._pipe_check(i)
 
     def step_host(self, gts_pinned: torch.Tensor, out_pinned: torch.Tensor,
                   next_gts_pinned: torch.Tensor | None = None):

@@ -296,20 +296,6 @@ def level_shape(height: int, width: int, level: int) -> tuple[int, int]:
     return height, width
 
 
-def scaled_camera(cam: Camera, level: int) -> Camera:
-    """Camera for GP level l: fx, fy, cx, cy scaled by 2^-l, size ceil-halved.
-    Input preparation for a level; the tan clamp is recomputed for the new size."""
-    if level == 0:
-        return cam
-    s = 0.5 ** level
-    H, W = level_shape(cam.height, cam.width, level)
-    fx, fy = np.float32(cam.fx * s).item(), np.float32(cam.fy * s).item()
-    lim_x = cam.lim_x if math.isinf(cam.lim_x) else np.float32(1.3 * (0.5 * W) / fx).item()
-    lim_y = cam.lim_y if math.isinf(cam.lim_y) else np.float32(1.3 * (0.5 * H) / fy).item()
-    return replace(cam, fx=fx, fy=fy, cx=np.float32(cam.cx * s).item(), cy=np.float32(cam.cy * s).item(),
-                   width=W, height=H, lim_x=lim_x, lim_y=lim_y)
-
-
 def noise_image(height: int, width: int, seed: int, channels: int = 3) -> np.ndarray:
     """A smooth, seeded RGB image in [0.05, 0.95] (sum of random plane waves + fine noise)."""
     rng = np.random.default_rng(np.random.PCG64(seed))

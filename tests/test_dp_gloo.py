@@ -110,6 +110,15 @@ def _oracle_adam_rows(P, G, M, V, r0, r1, step):
         G[r] = 0.0
 
 
+STEPS = 3
+
+
+def _step_grad(g: torch.Tensor, step: int) -> torch.Tensor:
+    """A different per-rank gradient every step (the engine's backward output changes as the map
+    moves), so a stale row from an earlier step cannot cancel out."""
+    return g * (1.0 + 0.5 * step)
+
+
 def _sharded_worker(rank, world, port, out_dir):
     from paper_2311_16728_b200.mapping import ShardedAdam, row_shard
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -126,13 +135,28 @@ def _sharded_worker(rank, world, port, out_dir):
         pp[:K] = torch.from_numpy(p0)
         pg = torch.zeros_like(pp)
         opt = ShardedAdam(pp, pg, n, 0)
-        opt.m = torch.zeros((opt.r1 - opt.r0, n), dtype=torch.float64)
+        opt.m = torch.zeros((opt.R, n), dtype=torch.float64)
         opt.v = torch.zeros_like(opt.m)
-        opt._adam_rows = lambda: _oracle_adam_rows(opt.params, opt.grads, opt.m, opt.v, opt.r0, opt.r1, opt.t)
-        for _ in range(2):  # two steps with the same per-rank gradients
-            pg[:K] = g
+        # gs_adam_step_rows semantics, zero_grads=False as ShardedAdam calls it: only this rank's
+        # rows of params / moments change, the gradient rows are left as they are
+        opt._adam_rows = lambda: _oracle_adam_rows(opt.params, opt.grads.clone(), opt.m, opt.v, opt.r0, opt.r1, opt.t)
+        # replicated path in the same process: all-reduce of the full gradient, Adam on every row
+        P = torch.from_numpy(p0.copy())
+        Pg = torch.zeros_like(P)
+        M, V = torch.zeros_like(P), torch.zeros_like(P)
+        traj_s, traj_r = [], []
+        for step in range(STEPS):
+            gs = _step_grad(g, step)
+            pg[:K] += gs           # the engine's backward ADDS into the gradient buffer (gs.h)
             opt.step()
-        np.save(os.path.join(out_dir, f"sp{rank}.npy"), opt.params.numpy())
+            Pg += gs
+            dist.all_reduce(Pg)
+            _oracle_adam_rows(P, Pg, M, V, 0, K, step + 1)   # zeroes Pg (zero_grads=True)
+            traj_s.append(opt.params.numpy().copy())
+            traj_r.append(P.numpy().copy())
+            assert float(pg.abs().max()) == 0.0  # nothing left over for the next +=
+        np.save(os.path.join(out_dir, f"sp{rank}.npy"), np.stack(traj_s))
+        np.save(os.path.join(out_dir, f"rp{rank}.npy"), np.stack(traj_r))
         np.save(os.path.join(out_dir, f"rows{rank}.npy"), np.array([opt.r0, opt.r1]))
     finally:
         dist.destroy_process_group()
@@ -150,23 +174,99 @@ def test_row_shard_partition():
 
 
 def test_gloo_world2_sharded_adam_equals_replicated(tmp_path):
-    """reduce-scatter -> row-sharded Adam -> all-gather gives every rank the parameters of the
-    replicated all-reduce + full Adam path, bit for bit (the update is elementwise)."""
+    """reduce-scatter -> row-sharded Adam -> all-gather, with the engine's += gradient pattern over
+    3 steps, gives every rank the parameters of the replicated all-reduce + full Adam path bit for
+    bit at every step (the update is elementwise), and both equal the batched oracle."""
     world = 2
     mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
     s0, s1 = np.load(tmp_path / "sp0.npy"), np.load(tmp_path / "sp1.npy")
-    assert np.array_equal(s0, s1)
+    rp0 = np.load(tmp_path / "rp0.npy")
+    assert np.array_equal(s0, s1)            # replicas identical
+    assert np.array_equal(s0, rp0)           # sharded == replicated, every step, bitwise
     r0, r1 = np.load(tmp_path / "rows0.npy"), np.load(tmp_path / "rows1.npy")
     assert r0[0] == 0 and r0[1] == r1[0] and r1[1] == 14
-    # replicated reference: batched gradient (sum over all views), full Adam on every row
+    # batched reference: one process, gradient summed over all views (R22), full Adam on every row
     scene, cams, G = _views()
     K, n = 14, scene.means.shape[0]
     g = torch.from_numpy(_flat_grad(scene, cams, G).reshape(K, n).copy())
     P = torch.from_numpy(np.concatenate([scene.means.T, scene.quats.T, scene.log_scales.T,
                                          scene.opacity_logits[None], scene.sh.reshape(n, -1).T]).astype(np.float64))
     M, V = torch.zeros_like(P), torch.zeros_like(P)
-    for step in (1, 2):
-        Gr = g.clone()
-        _oracle_adam_rows(P, Gr, M, V, 0, K, step)
-    np.testing.assert_allclose(s0, P.numpy(), rtol=1e-12, atol=1e-15)
+    for step in range(STEPS):
+        _oracle_adam_rows(P, _step_grad(g, step).clone(), M, V, 0, K, step + 1)
+        np.testing.assert_allclose(s0[step], P.numpy(), rtol=1e-12, atol=1e-15)
+
+
+def _stale_worker(rank, world, port, out_dir):
+    """The pre-fix ShardedAdam (only this rank's gradient rows zeroed after the step): the
+    regression the fixed step must not show."""
+    from paper_2311_16728_b200.mapping import ShardedAdam
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, n = 14, 8
+        pp = torch.zeros((K, n), dtype=torch.float64)
+        pg = torch.zeros_like(pp)
+        opt = ShardedAdam(pp, pg, n, 0)
+
+        def sgd_rows():  # SGD with lr 1 on this rank's rows
+            opt.params[opt.r0:opt.r1] -= opt.grads[opt.r0:opt.r1]
+        opt._adam_rows = sgd_rows
+        for _ in range(3):
+            pg[:K] += 1.0 + rank  # per-rank gradient (sum over ranks = 3)
+            opt.step()
+        np.save(os.path.join(out_dir, f"stale{rank}.npy"), opt.params.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_step_leaves_no_stale_gradient(tmp_path):
+    """3 SGD steps of the summed gradient 3 move every row to exactly -9 (a stale row re-added
+    in later steps gives -18 and more)."""
+    mp.start_processes(_stale_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"stale{r}.npy"), np.full((14, 8), -9.0))
+
+
+def _state_worker(rank, world, port, out_dir):
+    from paper_2311_16728_b200.mapping import ShardedAdam
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, n = 14, 5
+        R = 7
+        pp = torch.zeros((world * R, n), dtype=torch.float64)
+        opt = ShardedAdam(pp, torch.zeros_like(pp), n, 0)
+        opt.m = torch.zeros((opt.R, n), dtype=torch.float64)
+        opt.v = torch.zeros_like(opt.m)
+        rows = torch.arange(opt.r0, opt.r1, dtype=torch.float64)[:, None]
+        opt.m[:opt.r1 - opt.r0] = rows * 10 + torch.arange(n)
+        opt.v[:opt.r1 - opt.r0] = -(rows * 10 + torch.arange(n))
+        m, v = opt.full_state()
+        np.save(os.path.join(out_dir, f"m{rank}.npy"), m.numpy())
+        # densification: a new map of n' = 3 Gaussians with full moments; each rank keeps its rows
+        m_new = torch.arange(world * R * 3, dtype=torch.float64).view(world * R, 3)
+        pp2 = torch.zeros((world * R, 3), dtype=torch.float64)
+        opt.rebind(pp2, torch.zeros_like(pp2), 3, m_new, -m_new)
+        np.save(os.path.join(out_dir, f"mine{rank}.npy"), opt.m.numpy())
+        np.save(os.path.join(out_dir, f"v{rank}.npy"), v.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_state_gather_and_rebind(tmp_path):
+    """Densification under the row-sharded optimiser: full_state() all-gathers every rank's
+    moment rows into the full layout; rebind() keeps exactly this rank's rows of the new map's
+    moments (rows [r0, r1), zero padding after)."""
+    mp.start_processes(_state_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    want = np.arange(14)[:, None] * 10.0 + np.arange(5)
+    for r in range(2):
+        m = np.load(tmp_path / f"m{r}.npy")
+        assert np.array_equal(m[:14], want)
+        assert np.array_equal(np.load(tmp_path / f"v{r}.npy")[:14], -want)
+        mine = np.load(tmp_path / f"mine{r}.npy")
+        full = np.arange(14 * 3, dtype=np.float64).reshape(14, 3)
+        assert np.array_equal(mine, full[7 * r:7 * (r + 1)])

@@ -176,3 +176,61 @@ def test_mapping_engine_geometry_densify():
     assert np.isfinite(losses).all()
     nc, ns, npr = eng.densify_and_prune(seed=1)
     assert eng.temporary.shape[0] >= eng.n
+
+
+def test_mapping_engine_densify_with_row_sharded_optimizer(tmp_path):
+    """Densify and prune with shard_optimizer=True (NCCL process group of one rank, so the
+    reduce-scatter / all-gather are real NCCL calls): the new map and its Adam moments equal what
+    core.densify makes of the engine's state before the call (moments all-gathered from the
+    shards), bit for bit; the engine keeps stepping afterwards."""
+    import torch.distributed as dist
+    from paper_2311_16728_b200.core import permute_columns
+    from paper_2311_16728_b200.core import spatial_order as sorder
+    from paper_2311_16728_b200.levels import densify_samples as dsamples
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        scene = make_scene("tiny")
+        cams = make_cameras("tiny", 1)
+        r = Renderer(scene.n, 0, 1, cams[0].width, cams[0].height, 1 << 16)
+        gt = r.forward(pack_params(scene), cams)[0].clone()
+        cfg = DensifyConfig(grad_threshold=1e-3, scene_extent=1.0)
+        eng = MappingEngine(perturb(scene, 4), cams, gt, n_levels=1, densify_cfg=cfg)
+        assert eng.sharded is not None and eng.adam is None
+        for _ in range(6):
+            eng.build_pyramids()
+            eng.step()
+        n = eng.n
+        m, v = eng._moments()
+        assert float(m[:, :n].abs().sum()) > 0  # the sharded Adam has stepped
+        z = torch.from_numpy(dsamples(n, 3)).cuda()
+        p_e, m_e, v_e, counts, _ = densify(eng.params.clone(), n, 0, m.clone(), v.clone(), eng.grad2d_norm.clone(),
+                                           eng.vis_count.clone(), eng.max_radius.clone(), z,
+                                           cfg.struct(cams[0].width, cams[0].height), tags=eng.temporary.clone())
+        nn = counts[3]
+        perm = sorder(p_e, nn, 0)
+        p_e, m_e, v_e = (permute_columns(x, perm, nn) for x in (p_e, m_e, v_e))
+        nc, ns, npr = eng.densify_and_prune(seed=3)
+        assert (nc, ns, npr) == counts[:3] and nc + ns > 0 and eng.n == nn
+        m2, v2 = eng._moments()
+        assert torch.equal(eng.params[:, :nn], p_e[:, :nn])
+        assert torch.equal(m2[:, :nn], m_e[:, :nn]) and torch.equal(v2[:, :nn], v_e[:, :nn])
+        assert float(eng.grads.abs().max()) == 0.0
+        for _ in range(3):
+            eng.build_pyramids()
+            losses = [x.item() for x in eng.step()]
+        assert np.isfinite(losses).all()
+        # geometry densification under the sharded optimiser: moments of the old map carried over
+        from synth import make_keypoints
+        uv, active, kd, depth, img = make_keypoints(cams[0], 120, 2)
+        n0 = eng.n
+        m0, _ = eng._moments()
+        mass = float(m0[:, :n0].abs().sum())
+        added = eng.add_keyframe_features(0, uv, active, kd, depth, img, mode=1)
+        assert added > 0 and eng.n == n0 + added
+        m1, _ = eng._moments()
+        assert abs(float(m1[:, :eng.n].abs().sum()) - mass) <= 1e-6 * mass  # same values, new order
+        eng.build_pyramids()
+        assert np.isfinite([x.item() for x in eng.step()]).all()
+    finally:
+        dist.destroy_process_group()

@@ -22,7 +22,9 @@ from paper_2311_16728_b200 import _lib as L
 from paper_2311_16728_b200.core import (Adam, AdamConfig, PhotometricLoss, Renderer, gaussian_pyramid, pack_params,
                                         unpack)
 from paper_2311_16728_b200.mapping import MappingEngine
-from synth import make_cameras, make_scene, noise_image, perturb, scaled_camera
+from synth import make_cameras, make_scene, noise_image, perturb
+
+scaled_camera = orc.level_camera
 
 pytestmark = pytest.mark.gpu
 

@@ -8,7 +8,8 @@ import pytest
 
 from paper_2311_16728_b200.core import level_shapes, pack_params, param_rows, unpack
 from paper_2311_16728_b200.mapping import gp_level
-from synth import make_cameras, make_scene, scaled_camera
+from paper_2311_16728_b200.levels import level_camera, level_size
+from synth import make_cameras, make_scene
 
 
 def test_gp_level_schedule():
@@ -25,11 +26,25 @@ def test_gp_level_schedule():
 def test_level_shapes_and_cameras():
     assert level_shapes(480, 640, 2) == [(480, 640), (240, 320), (120, 160)]
     assert level_shapes(33, 47, 2) == [(33, 47), (17, 24), (9, 12)]
+    assert level_size(33, 47, 2) == (9, 12) and level_size(680, 1200, 2) == (170, 300)
     cam = make_cameras("tum", 1)[0]
-    c2 = scaled_camera(cam, 2)
+    c2 = level_camera(cam, 2)
+    # closed form (R12): f/4 and c/4 are exact in fp32; lim = 1.3 (W/2)/fx at the level size
     assert (c2.width, c2.height) == (160, 120)
-    assert c2.fx == pytest.approx(cam.fx / 4) and c2.cx == pytest.approx(cam.cx / 4)
-    assert scaled_camera(cam, 0) is cam
+    assert c2.fx == cam.fx / 4 and c2.cx == cam.cx / 4 and c2.cy == cam.cy / 4
+    assert c2.lim_x == float(np.float32(1.3 * 80 / (cam.fx / 4)))
+    assert level_camera(cam, 0) is cam
+
+
+def test_product_level_camera_equals_oracle_reading():
+    """The engine's own level cameras (paper_2311_16728_b200.levels) and the oracle side's
+    (oracle.level_camera, what the parity tests feed both sides) are written separately; they
+    must agree field for field on every config and level."""
+    import oracle.oracle as orc
+    for cfg in ("tiny", "tum", "replica", "euroc"):
+        for cam in make_cameras(cfg, 3):
+            for lv in range(4):
+                assert level_camera(cam, lv) == orc.level_camera(cam, lv), (cfg, lv)
 
 
 def test_pack_unpack_roundtrip():
