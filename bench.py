@@ -42,6 +42,25 @@ BWD_FLOP_PER_COMP = 45
 BWD_FLOP_PER_PAIR = BWD_FLOP_PER_EVAL + BWD_FLOP_PER_COMP
 
 
+# Forward (A6) FLOPs (SURVEY §8(d) ALU model): every list entry up to the pixel's stop is
+# evaluated -- dx, dy, the quadratic form and the cutoff, sigma e^power, the alpha clamp and skip
+# (12); a composited entry adds the colour update 3 x fma and the transmittance update (9).
+FWD_FLOP_PER_EVAL = 12
+FWD_FLOP_PER_COMP = 9
+
+
+def survey_step_bytes(K: int, n: int, b: int, lv: dict, world: int, eng) -> float:
+    """SURVEY §8(d) algorithmic bytes of one iteration (one GP level) per GPU with b local views,
+    the measured visible count V and pair count P per view: A1 4KN + b(8N + 40V), A2 b 8N,
+    A3 b(20V + 12P), A4 b 24P, A5 b(8P + 8 tiles), A6 b(40P + 20 Npx), A7 b 36 Npx,
+    A8 b(40P + 20 Npx + 36V), A9 8KN + b 36V, A11 28KN (28KN/G row-sharded)."""
+    V, P, px, tiles = lv["V"], lv["P"], lv["px"], lv["tiles"]
+    a11 = 28 * K * n / (world if getattr(eng, "sharded", None) is not None else 1)
+    return (4 * K * n + b * (8 * n + 40 * V) + b * 8 * n + b * (20 * V + 12 * P) + b * 24 * P
+            + b * (8 * P + 8 * tiles) + b * (40 * P + 20 * px) + b * 36 * px + b * (40 * P + 20 * px + 36 * V)
+            + 8 * K * n + b * 36 * V + a11)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -102,51 +121,93 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+# ----------------------------------------------------------------------------- workload
+def workload_config(name: str, world: int) -> dict:
+    """The `config` object of the JSON line (both arms print the same one)."""
+    from synth import config
+    cfg = config(name)
+    K = 11 + 3 * (cfg["sh_degree"] + 1) ** 2
+    ld = (cfg["n"] + 63) // 64 * 64
+    views = 1 if cfg["views"] == 1 else cfg["views"]
+    per_gpu = 1 if cfg["views"] == 1 else len(range(0, views, world))
+    total = world if cfg["views"] == 1 else views
+    return {"workload": name, "n_gaussians": cfg["n"], "sh_degree": cfg["sh_degree"], "width": cfg["width"],
+            "height": cfg["height"], "gp_levels": cfg["levels"] + 1, "views_per_gpu": per_gpu,
+            "global_batch": total, "iters_per_step": cfg["levels"] + 1, "parallelism": f"dp{world}",
+            "l2": f"working set {4 * K * ld * 4 / 1e6:.0f} MB (params+grads+Adam m,v) > 126 MB L2; no flush",
+            "layout": "Gaussians in Morton order (MappingEngine spatial_order, once at setup; the input recipe "
+                      "shuffles them)"}
+
+
 # ----------------------------------------------------------------------------- oracle (CPU)
-def oracle_sample_step(cfg_name: str, rank_view: int = 0, n_pix: int = 4096, seed: int = 0):
-    """The CPU oracle on a bounded sample of one step of the workload: for each GP level,
-    render + backward on n_pix random pixels (dL masked to them), Eq. 4 on the full level image,
-    and the fp64 Adam step over every parameter.  Returns (seconds extrapolated to the full
-    step, seconds actually spent, description)."""
+_ORACLE_SCENES = {}
+
+
+def oracle_fraction_step(cfg_name: str, level0_pixels: int, seed: int = 0, rank_view: int = 0):
+    """The CPU oracle on a fraction f = level0_pixels / (H W) of one step of the workload, every
+    stage at the same fraction: for each GP level n..0, render + backward on f H_l W_l random
+    pixels (dL masked to them), Eq. 4 on an f-high band of rows, and the fp64 Adam step of an f
+    share of the Gaussians.  Returns (seconds, iteration-equivalents done = (n+1) f, description):
+    throughput = iteration-equivalents / seconds, all of it measured (no extrapolation)."""
     import oracle.oracle as orc
     from synth import config, make_cameras, make_scene, perturb
-    scaled_camera = orc.level_camera
     cfg = config(cfg_name)
-    scene = perturb(make_scene(cfg), 99)
-    cam0 = make_cameras(cfg, rank_view + 1)[rank_view]
+    if cfg_name not in _ORACLE_SCENES:  # input construction, not oracle work
+        _ORACLE_SCENES[cfg_name] = (perturb(make_scene(cfg), 99), make_cameras(cfg, rank_view + 1)[rank_view])
+    scene, cam0 = _ORACLE_SCENES[cfg_name]
     n_levels = cfg["levels"]
+    f = min(1.0, level0_pixels / (cam0.width * cam0.height))
     rng = np.random.default_rng(seed)
-    spent = 0.0
-    extrap = 0.0
-    K = scene.sh.shape[1]
     n = scene.n
+    ng = max(1, int(round(f * n)))
+    spent = 0.0
     for level in range(n_levels, -1, -1):
-        cam = scaled_camera(cam0, level)
+        cam = orc.level_camera(cam0, level)
         H, W = cam.height, cam.width
-        k = min(n_pix, H * W)
+        k = max(1, int(round(f * H * W)))
         idx = rng.choice(H * W, size=k, replace=False)
         pix = np.stack([np.zeros(k, int), idx // W, idx % W], 1).astype(np.int32)
-        gt = rng.uniform(0.05, 0.95, size=(3, H, W))
+        band = max(1, int(round(f * H)))
+        gt = rng.uniform(0.05, 0.95, size=(3, band, W))
+        crop = rng.uniform(0.05, 0.95, size=(3, band, W))
+        G = rng.normal(size=(k, 3))
         t0 = time.perf_counter()
-        r = orc.render(scene, [cam], "recipe", pixels=pix)
-        t1 = time.perf_counter()
-        img = np.zeros((3, H, W))
-        img[:, pix[:, 1], pix[:, 2]] = r["rgb"].T
-        loss, _, dL = orc.loss(img, gt, 0.2)
-        t2 = time.perf_counter()
-        g = orc.backward(scene, [cam], dL[:, pix[:, 1], pix[:, 2]].T, "recipe", pixels=pix)
-        t3 = time.perf_counter()
+        orc.render(scene, [cam], "recipe", pixels=pix)
+        orc.loss(crop, gt, 0.2)
+        g = orc.backward(scene, [cam], G, "recipe", pixels=pix)
         for cls, lr in (("means", 1.6e-4), ("quats", 1e-3), ("log_scales", 5e-3), ("opacity_logits", 5e-2),
                         ("sh", 2.5e-3)):
-            arr = getattr(scene, cls)
-            orc.adam(arr.reshape(-1), g[cls].reshape(-1), np.zeros(arr.size), np.zeros(arr.size), lr=lr, step=1)
-        t4 = time.perf_counter()
-        scale = (H * W) / k
-        spent += t4 - t0
-        extrap += (t1 - t0) * scale + (t2 - t1) + (t3 - t2) * scale + (t4 - t3)
-    desc = (f"{cfg_name}: per GP level {n_levels}..0, render+backward on {n_pix} random pixels "
-            f"(extrapolated x H*W/{n_pix}), full-image Eq. 4 loss, fp64 Adam over all {n}x{11 + 3 * K} params")
-    return extrap, spent, desc
+            arr = getattr(scene, cls)[:ng].reshape(-1).astype(np.float64)
+            orc.adam(arr, g[cls][:ng].reshape(-1), np.zeros(arr.size), np.zeros(arr.size), lr=lr, step=1)
+        spent += time.perf_counter() - t0
+    desc = (f"{cfg_name}: fraction f = {f:.5f} of one step (levels {n_levels}..0: render + backward on f H W "
+            f"random pixels, Eq. 4 on an f-high row band, fp64 Adam on f of the {n} Gaussians); "
+            f"iteration-equivalents = {n_levels + 1} f per step, measured, not extrapolated")
+    return spent, (n_levels + 1) * f, desc
+
+
+def oracle_full_frame(cfg_name: str = "tiny", threads: int | None = None):
+    """The oracle over a whole frame (every pixel): render + Eq. 4 + backward + Adam of the tiny
+    config (configs[0]), with the given OpenMP thread count; seconds."""
+    import oracle.oracle as orc
+    from synth import make_cameras, make_scene, noise_image
+    scene = make_scene(cfg_name)
+    cam = make_cameras(cfg_name, 1)[0]
+    gt = noise_image(cam.height, cam.width, 1)
+    old = orc.threads()
+    if threads:
+        orc.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        r = orc.render(scene, [cam], "recipe")
+        _, _, dL = orc.loss(r["rgb"][0], gt, 0.2)
+        g = orc.backward(scene, [cam], dL[None], "recipe")
+        for cls in ("means", "quats", "log_scales", "opacity_logits", "sh"):
+            arr = getattr(scene, cls).reshape(-1).astype(np.float64)
+            orc.adam(arr, g[cls].reshape(-1), np.zeros(arr.size), np.zeros(arr.size), lr=1e-3, step=1)
+        return time.perf_counter() - t0, orc.threads()
+    finally:
+        orc.set_threads(old)
 
 
 def run_reference(args):
@@ -154,24 +215,22 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle.oracle as orc
-    from synth import config
-    cfg = config(args.config)
-    iters_per_step = cfg["levels"] + 1
-    for _ in range(args.warmup):
-        oracle_sample_step(args.config, n_pix=args.ref_pixels)
-    ext = []
+    for w in range(args.warmup):
+        oracle_fraction_step(args.config, args.ref_pixels, seed=1000 + w)
+    secs, work = 0.0, 0.0
     for s in range(args.steps):
-        e, _, desc = oracle_sample_step(args.config, n_pix=args.ref_pixels, seed=s)
-        ext.append(e)
-    sec = float(np.mean(ext))
-    value = iters_per_step / sec
+        t, wk, desc = oracle_fraction_step(args.config, args.ref_pixels, seed=s)
+        secs += t
+        work += wk
+    value = work / secs
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.config, world),
             "cpu_baseline": {"value": value, "unit": "iters/s", "cores": orc.threads(), "kind": "oracle",
                              "sample": desc},
-            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "iteration_equivalents_per_step": work / args.steps}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -295,23 +354,31 @@ def run_ours(args):
     # ---- algorithmic work of the raster kernels per level: composited (pixel, Gaussian) pairs
     # and evaluated pairs (list entries up to each pixel's last contributor, which the
     # back-to-front replay visits)
-    comp_pairs, eval_pairs = [], []
+    comp_pairs, eval_pairs, levels_meas = [], [], []
     for level in range(cfg["levels"], -1, -1):
         eng.render(level)
         torch.cuda.synchronize()
-        v = eng.renderers[level].ws.views()
+        rw = eng.renderers[level].ws
+        v = rw.views()
         comp_pairs.append(int(v["n_composited"].sum().item()))
         eval_pairs.append(int(v["n_contrib"].to(torch.int64).sum().item()))
+        _, _, P_l = rw.status()
+        levels_meas.append({"level": level, "V": int((v["radius"] > 0).sum().item()) / len(cams), "P": P_l / len(cams),
+                            "px": rw.W * rw.H, "tiles": rw.tiles_x * rw.tiles_y})
     pairs_per_step = sum(comp_pairs)
     flops_per_step = BWD_FLOP_PER_EVAL * sum(eval_pairs) + BWD_FLOP_PER_COMP * pairs_per_step
 
-    # ---- live kernel timing (eager launches): the dominant kernels are bracketed with CUDA
-    # events recorded by libgs.so on their launching stream (gs_profile_kernel)
+    # ---- live kernel timing (eager launches): each kernel family of the step is bracketed with
+    # CUDA events recorded by libgs.so on its launching stream (gs_profile_kernel), one family per
+    # pass of K eager steps; share = its summed launch time / the pass's step time
     live = {}
+    akern = "k_adam_fused" if world == 1 else "k_adam"
+    families = ["k_preprocess", "k_tile_scan", "k_bin_scatter", "k_tile_sort", "k_raster_fwd", "k_ssim",
+                "k_raster_bwd", "k_preprocess_bwd", akern]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    for kname in ("k_raster_bwd", "k_adam_fused" if world == 1 else "k_adam"):
+    for kname in families:
         L.gs_profile_kernel(kname)
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -323,7 +390,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         live[kname] = L.gs_profile_read() + (t0.elapsed_time(t1),)
     L.gs_profile_kernel(None)
-    eager_ms = min(v[2] for v in live.values())
+    eager_ms = statistics.median(v[2] for v in live.values())
+    shares = {k: v[0] / v[2] for k, v in live.items()}
 
     # ---- headline: K timed steps (one CUDA-graph replay per step on a single GPU; eager
     # launches under torchrun, where the NCCL all-reduce sits inside the iteration)
@@ -385,7 +453,7 @@ def run_ours(args):
     # 1200x680, 911-1084 FPS on an RTX 4090 with ~130-140K trained Gaussians): A1-A6 of one
     # Replica-like keyframe view (500K Gaussians, SH 3) on this GPU
     replica = None
-    if rank == 0 and world == 1 and not args.no_replica:
+    if rank == 0 and world == 1 and not args.no_replica and args.config != "replica":
         rscene = make_scene("replica")
         rcam = make_cameras("replica", 1)
         rr = Renderer(rscene.n, 3, 1, rcam[0].width, rcam[0].height, 1 << 23)
@@ -451,28 +519,36 @@ def run_ours(args):
         eng.pipeline_check()  # raises if a timed step overflowed its pair capacity (rendered nothing)
     eng.check()
 
-    # ---- rooflines.  Dominant kernel: the raster backward (A8), FP32-ALU bound: algorithmic
-    # FLOPs = evaluated pairs x 13 + composited pairs x 45 against 148 SMs x 128 FP32
-    # lanes x 2 x the SM clock sampled during the run.  Second: the fused Adam (A11), HBM bound.
+    # ---- rooflines.  Per kernel family: the raster kernels (A6, A8) are FP32-ALU bound
+    # (algorithmic FLOPs per evaluated / composited pair) against 148 SMs x 128 FP32
+    # lanes x 2 x the SM clock sampled during the run; the per-Gaussian kernels are HBM bound
+    # (SURVEY §8(d) algorithmic bytes with the measured V, P) against the measured copy peak.
+    # `roofline` is the family with the largest measured share of the step.
     K = 11 + 3 * (D + 1) ** 2
     ld = eng.params.shape[1]
     clocks = clk.summary()
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = sms * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
-    bwd_ms, bwd_launches, _ = live["k_raster_bwd"]
-    bwd_flops = flops_per_step * args.steps
-    bwd_achieved = bwd_flops / (bwd_ms * 1e-3) / 1e12
-    akern = "k_adam_fused" if world == 1 else "k_adam"
-    adam_ms, adam_launches, _ = live[akern]
+    peak, peak_src = load_peaks()
+    b = len(cams)
+    bytes_model = {  # algorithmic bytes per step (all levels), measured V and P
+        "k_preprocess": sum(4 * K * n + b * (8 * n + 40 * lv["V"]) for lv in levels_meas),
+        "k_tile_scan": sum(b * 8 * lv["tiles"] for lv in levels_meas),
+        "k_bin_scatter": sum(b * (20 * lv["V"] + 12 * lv["P"]) for lv in levels_meas),
+        "k_tile_sort": sum(b * (24 + 8) * lv["P"] for lv in levels_meas),
+        "k_ssim": sum(b * 36 * lv["px"] for lv in levels_meas),
+        "k_preprocess_bwd": sum(8 * K * n + b * 36 * lv["V"] for lv in levels_meas),
+    }
     if world == 1:
-        adam_bytes = K * n * 24 + 4 * n
+        adam_bytes = K * n * 24 + 4 * n  # fused: p, m, v read + written, a 4-byte slot per Gaussian
     elif eng.sharded is not None:  # this rank's rows only
         adam_bytes = (eng.sharded.r1 - eng.sharded.r0) * ld * 32
     else:
         adam_bytes = K * ld * 32
-    peak, peak_src = load_peaks()
-    adam_achieved = adam_bytes * adam_launches / (adam_ms * 1e-3) / 1e9
+    bytes_model[akern] = adam_bytes * len(levels_meas)
+    flops_model = {"k_raster_bwd": flops_per_step,
+                   "k_raster_fwd": FWD_FLOP_PER_EVAL * sum(eval_pairs) + FWD_FLOP_PER_COMP * pairs_per_step}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -480,6 +556,40 @@ def run_ours(args):
             traffic = json.load(open(tp)).get(args.config, {})
         except Exception:  # noqa: BLE001
             traffic = {}
+
+    def roof(kname):
+        ms_k, launches_k, wall = live[kname]
+        per_step = ms_k / args.steps
+        common = {"kernel": kname, "avg_launch_ms": ms_k / max(launches_k, 1), "launches_per_step":
+                  launches_k / args.steps, "share_of_step": ms_k / wall,
+                  "traffic": (traffic or {}).get(kname),
+                  "timing": "CUDA events around each launch on its stream, eager pass of K steps"}
+        if kname in flops_model:
+            ach = flops_model[kname] / (per_step * 1e-3) / 1e12
+            return {"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                    "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sampled)",
+                    "algorithmic_flops_per_launch": flops_model[kname] / max(launches_k / args.steps, 1), **common}
+        ach = bytes_model[kname] / (per_step * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_model[kname] /
+                max(launches_k / args.steps, 1), **common}
+
+    kernel_roofs = {k: roof(k) for k in families if (k in flops_model or k in bytes_model) and live[k][0] > 0}
+    dominant = max(kernel_roofs, key=lambda k: kernel_roofs[k]["share_of_step"])
+    roofline = dict(kernel_roofs[dominant])
+    roofline["chosen_by"] = "largest measured share of the step"
+    roofline["evaluated_pairs_per_level"] = eval_pairs
+    roofline["composited_pairs_per_level"] = comp_pairs
+    # step-level HBM fraction (the metric's third part): SURVEY §8(d) algorithmic bytes of every
+    # stage at every level with the measured V and P, over the measured step time
+    step_bytes = sum(survey_step_bytes(K, n, b, lv, world, eng) for lv in levels_meas)
+    ms_step = ms_max / args.steps
+    roofline_step = {"bound": "hbm", "algorithmic_bytes_per_step": step_bytes, "peak": peak, "unit": "GB/s",
+                     "achieved": step_bytes / (ms_step * 1e-3) / 1e9,
+                     "frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak,
+                     "levels": [{k: lv[k] for k in ("level", "V", "P", "px", "tiles")} for lv in levels_meas],
+                     "model": "SURVEY §8(d): A1 4KN+b(8N+40V), A2 b8N, A3 b(20V+12P), A4 b24P, A5 b(8P+8 tiles), "
+                              "A6 b(40P+20Npx), A7 b36Npx, A8 b(40P+20Npx+36V), A9 8KN+b36V, A11 28KN (/G sharded)"}
 
     total_views = len(cams) * world
     value = iters_per_step * total_views * args.steps / (ms_max * 1e-3)
@@ -491,40 +601,79 @@ def run_ours(args):
         launches_step += launches_per_iteration(bits, world == 1, chunked=t < CHUNK_MAX_TILES, view_tiles=t)
     launches = args.steps * launches_step
 
+    # ---- sorted keys/s (A4): the level-0 pairs of this step (keys (tile << 32 | depth bits),
+    # Gaussian ids), randomly permuted, through the onesweep LSD radix sort (gs_debug_sort_pairs);
+    # and the default bucket path's rate: pairs / (bin scatter + tile sorts) per level-0 launch
+    sorted_keys = None
+    if rank == 0:
+        rw = eng.renderers[0].ws
+        eng.render(0)
+        torch.cuda.synchronize()
+        v0 = rw.views()
+        P0 = int(levels_meas[-1]["P"] * len(cams))
+        bits = 32 + max(1, math.ceil(math.log2(max(rw.tiles_x * rw.tiles_y * len(cams), 2))))
+        perm = torch.randperm(P0, device=dev)
+        k_src, v_src = v0["keys"][:P0][perm].clone(), v0["vals"][:P0][perm].clone()
+        kk, vv = torch.empty_like(k_src), torch.empty_like(v_src)
+        k2, v2 = torch.empty_like(k_src), torch.empty_like(v_src)
+        temp = torch.empty(L.gs_sort_temp_size(P0, bits), dtype=torch.uint8, device=dev)
+        reps, tot = 20, 0.0
+        for r_ in range(reps + 3):
+            kk.copy_(k_src)
+            vv.copy_(v_src)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            L.gs_debug_sort_pairs(kk, vv, k2, v2, bits, temp)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            if r_ >= 3:
+                tot += a_.elapsed_time(b_)
+        # keys equal the bucket path's order; equal keys (same tile, equal fp32 depth) keep the
+        # permuted input order in the stable radix sort, so values are compared as per-key sets
+        ok = bool(torch.equal(kk, v0["keys"][:P0]) and
+                  torch.equal((kk * 0 + vv.to(torch.int64)).sum(), v0["vals"][:P0].to(torch.int64).sum()))
+        radix_ms = tot / reps
+        bucket_ms = None
+        if eng.renderers[0].ws.tiles_x * eng.renderers[0].ws.tiles_y * len(cams) >= CHUNK_MAX_TILES:
+            # level-0 share of the bucket kernels: launches are per level, level 0 is the last of each step
+            L.gs_profile_kernel("k_tile_sort")
+            eng.render(0)
+            tms = L.gs_profile_read()
+            L.gs_profile_kernel("k_bin_scatter")
+            eng.render(0)
+            bms = L.gs_profile_read()
+            L.gs_profile_kernel(None)
+            bucket_ms = tms[0] + bms[0]
+        sorted_keys = {"pairs": P0, "key_bits": bits, "radix_onesweep_keys_per_s": P0 / (radix_ms * 1e-3),
+                       "radix_ms": radix_ms, "radix_keys_equal_bucket_order": ok,
+                       "bucket_keys_per_s": (P0 / (bucket_ms * 1e-3)) if bucket_ms else None,
+                       "bucket_ms": bucket_ms,
+                       "note": "level-0 pairs of this step; radix = gs_debug_sort_pairs on a random permutation; "
+                               "bucket = bin scatter + per-tile bitonic sorts (the default A3+A4 path)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle.oracle as orc
-        ext, spent, desc = oracle_sample_step(args.config, n_pix=args.ref_pixels)
-        cpu = {"value": iters_per_step / ext, "unit": "iters/s", "cores": orc.threads(), "kind": "oracle",
-               "sample": desc + f"; {spent:.1f} s measured"}
+        secs, work, desc = oracle_fraction_step(args.config, args.ref_pixels)
+        full_1, _ = oracle_full_frame("tiny", threads=1)
+        full_n, nth = oracle_full_frame("tiny")
+        cpu = {"value": work / secs, "unit": "iters/s", "cores": orc.threads(), "kind": "oracle",
+               "sample": desc + f"; {secs:.1f} s measured",
+               "full_frame_tiny": {"seconds_1_thread": full_1, "seconds_all_threads": full_n, "threads": nth,
+                                   "what": "configs[0] (1000 Gaussians, 64x48): render + Eq. 4 + backward + Adam "
+                                           "over every pixel, one iteration"}}
     if rank == 0:
         H, W = cams[0].height, cams[0].width
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": args.config, "n_gaussians": n, "sh_degree": D, "width": W, "height": H,
-                       "gp_levels": cfg["levels"] + 1, "views_per_gpu": len(cams), "global_batch": total_views,
-                       "iters_per_step": iters_per_step, "parallelism": f"dp{world}",
-                       "l2": f"working set {4 * K * ld * 4 / 1e6:.0f} MB (params+grads+Adam m,v) > 126 MB L2; no flush",
-                       "layout": "Gaussians in Morton order (MappingEngine spatial_order, once at setup; the "
-                                 "input recipe shuffles them)"},
-            "roofline": {"bound": "alu", "kernel": "k_raster_bwd (A8)", "achieved": bwd_achieved,
-                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": bwd_achieved / fp32_peak,
-                         "traffic": (traffic or {}).get("k_raster_bwd"),
-                         "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sampled)",
-                         "algorithmic_flops_per_launch": flops_per_step / len(comp_pairs),
-                         "flop_per_evaluated_pair": BWD_FLOP_PER_EVAL,
-                         "flop_per_composited_pair_extra": BWD_FLOP_PER_COMP,
-                         "evaluated_pairs_per_level": eval_pairs, "composited_pairs_per_level": comp_pairs,
-                         "avg_launch_ms": bwd_ms / max(bwd_launches, 1),
-                         "share_of_step": bwd_ms / live["k_raster_bwd"][2],
-                         "timing": "CUDA events around each launch, eager pass of K steps"},
-            "roofline_hbm": {"bound": "hbm", "kernel": f"{akern} (A11)", "achieved": adam_achieved, "peak": peak,
-                             "unit": "GB/s", "frac": adam_achieved / peak, "traffic": (traffic or {}).get(akern),
-                             "peak_source": peak_src, "algorithmic_bytes_per_launch": adam_bytes,
-                             "avg_launch_ms": adam_ms / max(adam_launches, 1),
-                             "share_of_step": adam_ms / live[akern][2]},
+            "config": workload_config(args.config, world),
+            "roofline": roofline,
+            "roofline_step": roofline_step,
+            "roofline_hbm": kernel_roofs[akern],
+            "kernel_rooflines": kernel_roofs,
+            "sorted_keys_per_s": sorted_keys,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "iters/s",
                     "h2d_bytes_per_step": int(gts_pinned[0].numel() * 4),
@@ -553,11 +702,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="tum")
+    ap.add_argument("--config", default="replica",
+                    help="workload (synth CONFIGS); the headline is configs[2], the Replica-like keyframe")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-replica", action="store_true", help="skip the Replica render-FPS context line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-pixels", type=int, default=4096)
+    ap.add_argument("--ref-pixels", type=int, default=2048,
+                    help="oracle sample: level-0 pixels per step (the same fraction of every level and stage)")
     ap.add_argument("--launch-list", action="store_true", help="profile exactly one step (ncu range)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of graph replays")
     args = ap.parse_args()

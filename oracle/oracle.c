@@ -27,7 +27,8 @@
  *              loss and gradients are then evaluated in double from those values.
  *
  * Build: gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math (see oracle/oracle.py).
- * parity unpinned: nothing (every function has a pin in tests/test_oracle_*.py).
+ * parity unpinned: nothing -- every function has a pin in tests/test_oracle_*.py (the R15
+ * clamped-tangent and R7 alpha-clamp branches in test_oracle_clamps.py).
  */
 #include <math.h>
 #include <stdint.h>
@@ -118,6 +119,42 @@ static void sh_basis(int D, double x, double y, double z, double Y[16], double d
     dY[14][0] = c3e * 2 * x * z; dY[14][1] = -c3e * 2 * y * z; dY[14][2] = c3e * (xx - yy);
     Y[15] = -c3a * x * (xx - 3 * yy);
     dY[15][0] = -c3a * (3 * xx - 3 * yy); dY[15][1] = -c3a * (-6 * x * y);
+}
+
+/* The basis with every monomial taken in absolute value, at nonnegative (xa, ya, za): the
+   magnitude a finite-precision evaluation of Y_l / dY_l at a direction whose components are
+   at most (xa, ya, za) in size rounds (rounding allowance only, see orc_backward's mag). */
+static void sh_basis_abs(int D, double x, double y, double z, double Y[16], double dY[16][3]) {
+    const double pi = M_PI;
+    const double c0 = sqrt(1.0 / (4.0 * pi)), c1 = sqrt(3.0 / (4.0 * pi)), c2a = sqrt(15.0 / (4.0 * pi));
+    const double c2b = 0.25 * sqrt(5.0 / pi), c2c = 0.25 * sqrt(15.0 / pi), c3a = 0.25 * sqrt(35.0 / (2.0 * pi));
+    const double c3b = 0.5 * sqrt(105.0 / pi), c3c = 0.25 * sqrt(21.0 / (2.0 * pi)), c3d = 0.25 * sqrt(7.0 / pi);
+    const double c3e = 0.25 * sqrt(105.0 / pi);
+    memset(Y, 0, 16 * sizeof(double));
+    memset(dY, 0, 16 * 3 * sizeof(double));
+    Y[0] = c0;
+    if (D < 1) return;
+    Y[1] = c1 * y;  dY[1][1] = c1;
+    Y[2] = c1 * z;  dY[2][2] = c1;
+    Y[3] = c1 * x;  dY[3][0] = c1;
+    if (D < 2) return;
+    double xx = x * x, yy = y * y, zz = z * z;
+    Y[4] = c2a * x * y;               dY[4][0] = c2a * y;  dY[4][1] = c2a * x;
+    Y[5] = c2a * y * z;               dY[5][1] = c2a * z;  dY[5][2] = c2a * y;
+    Y[6] = c2b * (2 * zz + xx + yy);  dY[6][0] = 2 * c2b * x; dY[6][1] = 2 * c2b * y; dY[6][2] = 4 * c2b * z;
+    Y[7] = c2a * x * z;               dY[7][0] = c2a * z;  dY[7][2] = c2a * x;
+    Y[8] = c2c * (xx + yy);           dY[8][0] = 2 * c2c * x; dY[8][1] = 2 * c2c * y;
+    if (D < 3) return;
+    Y[9] = c3a * y * (3 * xx + yy);   dY[9][0] = c3a * 6 * x * y; dY[9][1] = c3a * (3 * xx + 3 * yy);
+    Y[10] = c3b * x * y * z;          dY[10][0] = c3b * y * z; dY[10][1] = c3b * x * z; dY[10][2] = c3b * x * y;
+    Y[11] = c3c * y * (4 * zz + xx + yy);
+    dY[11][0] = c3c * 2 * x * y; dY[11][1] = c3c * (4 * zz + xx + 3 * yy); dY[11][2] = c3c * 8 * y * z;
+    Y[12] = c3d * z * (2 * zz + 3 * xx + 3 * yy);
+    dY[12][0] = c3d * 6 * x * z; dY[12][1] = c3d * 6 * y * z; dY[12][2] = c3d * (6 * zz + 3 * xx + 3 * yy);
+    Y[13] = c3c * x * (4 * zz + xx + yy);
+    dY[13][0] = c3c * (4 * zz + 3 * xx + yy); dY[13][1] = c3c * 2 * x * y; dY[13][2] = c3c * 8 * x * z;
+    Y[14] = c3e * z * (xx + yy);      dY[14][0] = c3e * 2 * x * z; dY[14][1] = c3e * 2 * y * z; dY[14][2] = c3e * (xx + yy);
+    Y[15] = c3a * x * (xx + 3 * yy);  dY[15][0] = c3a * (3 * xx + 3 * yy); dY[15][1] = c3a * 6 * x * y;
 }
 
 /* exported for the orthonormality pin */
@@ -690,18 +727,127 @@ static void chain_to_3d(const orc_scene *s, int64_t i, const orc_camera *cam, co
 /* Backward of sum over views of <dL/dI_v, I_v> for listed pixels.  dL_drgb[npix][3].
    Outputs (zeroed here, fp64, per-class AoS): gm[n][3], gq[n][4], gs[n][3], go[n], gsh[n][K][3];
    grad2d_norm[n] = sum over views of ||dL/dmean2d_v|| if non-NULL.
-   flag_gauss[n] (optional): 1 if the Gaussian was evaluated at a band-flagged pixel. */
+   flag_gauss[n] (optional): 1 if the Gaussian was evaluated at a band-flagged pixel.
+   mag (optional, [n][3+4+3+1+3K] in that class order): the conditioning of each gradient
+   element -- for every 2-D quantity k (u, v, A, B, C, sigma, r, g, b) the sum over pixels of
+   the absolute values of the per-pixel terms that make up its gradient, S_k (each product split
+   into its addends: dL/dalpha from |g||c| + |g||acc|, dL/du from |A dx| + |B dy|, ...), carried
+   to the parameters by chain_to_3d_abs (the chain with |coefficients| and |intermediates|).  An
+   evaluation in precision eps (any summation order, any association of the chain) is within a
+   small multiple of eps * mag of the exact value; the GPU parity tests use it as their rounding
+   allowance.  Not the method: a bound on what rounding can do to it. */
+static void chain_to_3d_abs(const orc_scene *s, int64_t i, const orc_camera *cam, const double S[G_N],
+                            const int clamped[3], double *gm, double *gq, double *gs, double *go, double *gsh) {
+    /* chain_to_3d with every coefficient and every intermediate replaced by its absolute value
+       (sums of |products|; a subtraction becomes an addition): applied to the nonnegative S it
+       bounds, step by step, the magnitudes a finite-precision evaluation of the chain rounds. */
+    orc_fwd64 f;
+    if (!fwd64(s, i, cam, &f)) return;
+    double a = f.S2[0], b = f.S2[1], c = f.S2[2];
+    double det = a * c - b * b;
+    double Q[4] = {fabs(c / det), fabs(b / det), fabs(b / det), fabs(a / det)};
+    double G[4] = {S[G_A], 0.5 * S[G_B], 0.5 * S[G_B], S[G_C]};
+    double QG[4] = {Q[0] * G[0] + Q[1] * G[2], Q[0] * G[1] + Q[1] * G[3],
+                    Q[2] * G[0] + Q[3] * G[2], Q[2] * G[1] + Q[3] * G[3]};
+    double H[4] = {QG[0] * Q[0] + QG[1] * Q[2], QG[0] * Q[1] + QG[1] * Q[3],
+                   QG[2] * Q[0] + QG[3] * Q[2], QG[2] * Q[1] + QG[3] * Q[3]};
+    double T[6];
+    for (int k = 0; k < 6; k++) T[k] = fabs(f.T[k]);
+    double GS3[9];
+    for (int r = 0; r < 3; r++)
+        for (int cc = 0; cc < 3; cc++) {
+            double acc = 0;
+            for (int p = 0; p < 2; p++)
+                for (int q2 = 0; q2 < 2; q2++) acc += T[3 * p + r] * H[2 * p + q2] * T[3 * q2 + cc];
+            GS3[3 * r + cc] = acc;
+        }
+    double HT[6];
+    for (int p = 0; p < 2; p++)
+        for (int cc = 0; cc < 3; cc++) HT[3 * p + cc] = H[2 * p] * T[cc] + H[2 * p + 1] * T[3 + cc];
+    double GT[6];
+    for (int p = 0; p < 2; p++)
+        for (int cc = 0; cc < 3; cc++)
+            GT[3 * p + cc] = 2.0 * (HT[3 * p] * fabs(f.S3[cc]) + HT[3 * p + 1] * fabs(f.S3[3 + cc]) +
+                                    HT[3 * p + 2] * fabs(f.S3[6 + cc]));
+    double GJ[6];
+    for (int p = 0; p < 2; p++)
+        for (int k = 0; k < 3; k++)
+            GJ[3 * p + k] = GT[3 * p] * fabs(cam->R[3 * k]) + GT[3 * p + 1] * fabs(cam->R[3 * k + 1]) +
+                            GT[3 * p + 2] * fabs(cam->R[3 * k + 2]);
+    double fx = cam->fx, fy = cam->fy, z = f.z, x = fabs(f.pc[0]), y = fabs(f.pc[1]);
+    double gpc[3] = {0, 0, 0};
+    gpc[2] += GJ[0] * (fx / (z * z)) + GJ[4] * (fy / (z * z));
+    if (!f.clx) { gpc[0] += GJ[2] * (fx / (z * z)); gpc[2] += GJ[2] * (2.0 * fx * x / (z * z * z)); }
+    else gpc[2] += GJ[2] * (fx * fabs(f.txc) / (z * z));
+    if (!f.cly) { gpc[1] += GJ[5] * (fy / (z * z)); gpc[2] += GJ[5] * (2.0 * fy * y / (z * z * z)); }
+    else gpc[2] += GJ[5] * (fy * fabs(f.ty_c) / (z * z));
+    gpc[0] += S[G_U] * fx / z;
+    gpc[1] += S[G_V] * fy / z;
+    gpc[2] += S[G_U] * (fx * x / (z * z)) + S[G_V] * (fy * y / (z * z));
+    for (int k = 0; k < 3; k++)
+        gm[k] += fabs(cam->R[k]) * gpc[0] + fabs(cam->R[3 + k]) * gpc[1] + fabs(cam->R[6 + k]) * gpc[2];
+    double M[9];
+    for (int k = 0; k < 9; k++) M[k] = fabs(f.M[k]);
+    double GM[9];
+    for (int r = 0; r < 3; r++)
+        for (int cc = 0; cc < 3; cc++)
+            GM[3 * r + cc] = 2.0 * (GS3[3 * r] * M[cc] + GS3[3 * r + 1] * M[3 + cc] + GS3[3 * r + 2] * M[6 + cc]);
+    double GR[9];
+    for (int j = 0; j < 3; j++) {
+        double gsj = 0;
+        for (int r = 0; r < 3; r++) { gsj += GM[3 * r + j] * fabs(f.Rq[3 * r + j]); GR[3 * r + j] = GM[3 * r + j] * f.sc[j]; }
+        gs[j] += gsj * f.sc[j];
+    }
+    double w = fabs(f.qn[0]), qx = fabs(f.qn[1]), qy = fabs(f.qn[2]), qz = fabs(f.qn[3]);
+    double gqn[4];
+    gqn[0] = 2 * (qz * GR[1] + qy * GR[2] + qz * GR[3] + qx * GR[5] + qy * GR[6] + qx * GR[7]);
+    gqn[1] = 2 * (qy * GR[1] + qz * GR[2] + qy * GR[3] + 2 * qx * GR[4] + w * GR[5] + qz * GR[6] + w * GR[7] + 2 * qx * GR[8]);
+    gqn[2] = 2 * (2 * qy * GR[0] + qx * GR[1] + w * GR[2] + qx * GR[3] + qz * GR[5] + w * GR[6] + qz * GR[7] + 2 * qy * GR[8]);
+    gqn[3] = 2 * (2 * qz * GR[0] + w * GR[1] + qx * GR[2] + w * GR[3] + 2 * qz * GR[4] + qy * GR[5] + qx * GR[6] + qy * GR[7]);
+    double dotg = w * gqn[0] + qx * gqn[1] + qy * gqn[2] + qz * gqn[3];
+    for (int k = 0; k < 4; k++) gq[k] += (gqn[k] + fabs(f.qn[k]) * dotg) / f.qnorm;
+    double sg = sigmoid(s->opac[i]);
+    go[0] += sg * (1 - sg) * S[G_SIG];
+    double Cc[3];
+    for (int k = 0; k < 3; k++)
+        Cc[k] = -((double)cam->R[k] * cam->t[0] + (double)cam->R[3 + k] * cam->t[1] + (double)cam->R[6 + k] * cam->t[2]);
+    double d[3] = {s->means[3 * i] - Cc[0], s->means[3 * i + 1] - Cc[1], s->means[3 * i + 2] - Cc[2]};
+    double nd = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    double dir[3] = {d[0] / nd, d[1] / nd, d[2] / nd};
+    /* a direction component is the rounded difference P_k - C_k: its size for the allowance is
+       (|P_k| + |C_k|) / |d|, not |dir_k| (a component near 0 carries an absolute error) */
+    double da[3];
+    for (int k = 0; k < 3; k++) da[k] = (fabs((double)s->means[3 * i + k]) + fabs(Cc[k])) / nd;
+    double Y[16], dY[16][3];
+    sh_basis_abs(s->D, da[0], da[1], da[2], Y, dY);
+    int K = (s->D + 1) * (s->D + 1);
+    double gdir[3] = {0, 0, 0};
+    const double gc[3] = {S[G_R], S[G_G], S[G_BL]};
+    for (int ch = 0; ch < 3; ch++) {
+        if (clamped[ch]) continue;
+        for (int l = 0; l < K; l++) {
+            gsh[l * 3 + ch] += Y[l] * gc[ch];
+            double shv = fabs(s->sh[(i * K + l) * 3 + ch]);
+            for (int k = 0; k < 3; k++) gdir[k] += gc[ch] * shv * dY[l][k];
+        }
+    }
+    double dd = fabs(dir[0]) * gdir[0] + fabs(dir[1]) * gdir[1] + fabs(dir[2]) * gdir[2];
+    for (int k = 0; k < 3; k++) gm[k] += (gdir[k] + fabs(dir[k]) * dd) / nd;
+}
+
 void orc_backward(int mode, int64_t n, int D, const float *means, const float *quats, const float *log_scales,
                   const float *opac, const float *sh, int V, const orc_camera *cams, const double *bg,
                   int64_t npix, const int32_t *pix, const double *dL_drgb, double *gm, double *gq, double *gs,
-                  double *go, double *gsh, double *grad2d_norm, int32_t *flag_gauss) {
+                  double *go, double *gsh, double *grad2d_norm, int32_t *flag_gauss, double *mag) {
     orc_scene s = {n, D, means, quats, log_scales, opac, sh};
     int K = (D + 1) * (D + 1);
+    int P = 11 + 3 * K;
     memset(gm, 0, sizeof(double) * 3 * n); memset(gq, 0, sizeof(double) * 4 * n);
     memset(gs, 0, sizeof(double) * 3 * n); memset(go, 0, sizeof(double) * n);
     memset(gsh, 0, sizeof(double) * 3 * K * n);
     if (grad2d_norm) memset(grad2d_norm, 0, sizeof(double) * n);
     if (flag_gauss) memset(flag_gauss, 0, sizeof(int32_t) * n);
+    if (mag) memset(mag, 0, sizeof(double) * P * n);
     int nth = orc_get_threads();
     for (int v = 0; v < V; v++) {
         orc_proj *pr = project_all(mode, &s, cams + v);
@@ -711,10 +857,12 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
         for (int64_t i = 0; i < n; i++) slot[i] = -1;
         for (int64_t j = 0; j < m; j++) slot[order[j]] = j;
         double *g2 = (double *)calloc((size_t)nth * (m > 0 ? m : 1) * G_N, sizeof(double));
+        double *s2 = mag ? (double *)calloc((size_t)nth * (m > 0 ? m : 1) * G_N, sizeof(double)) : NULL;
 #pragma omp parallel num_threads(nth)
         {
             int tid = omp_get_thread_num();
             double *mine = g2 + (size_t)tid * (m > 0 ? m : 1) * G_N;
+            double *mine_s = s2 ? s2 + (size_t)tid * (m > 0 ? m : 1) * G_N : NULL;
             int cap = 4096;
             orc_contrib *list = (orc_contrib *)malloc(sizeof(orc_contrib) * cap);
 #pragma omp for schedule(dynamic, 16)
@@ -745,13 +893,18 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
                     const orc_contrib *e = list + c;
                     const orc_proj *g = pr + e->k;
                     double *G = mine + slot[e->k] * G_N;
-                    double dLda = 0;
+                    double dLda = 0, dLda_mag = 0;
                     for (int ch = 0; ch < 3; ch++) {
                         G[G_R + ch] += gpix[ch] * e->alpha * e->T;
                         dLda += gpix[ch] * (g->rgb[ch] - acc[ch]);
+                        dLda_mag += fabs(gpix[ch]) * (fabs(g->rgb[ch]) + fabs(acc[ch]));
                         acc[ch] = e->alpha * g->rgb[ch] + (1.0 - e->alpha) * acc[ch];
                     }
                     dLda *= e->T;
+                    dLda_mag *= e->T;
+                    double *S = mine_s ? mine_s + slot[e->k] * G_N : NULL;
+                    if (S)
+                        for (int ch = 0; ch < 3; ch++) S[G_R + ch] += fabs(gpix[ch] * e->alpha * e->T);
                     if (e->clamped) continue; /* alpha = 0.99 constant */
                     G[G_SIG] += e->ep * dLda;
                     double dLdp = e->alpha * dLda;
@@ -761,6 +914,15 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
                     G[G_A] += dLdp * (-0.5 * dx * dx);
                     G[G_B] += dLdp * (-dx * dy);
                     G[G_C] += dLdp * (-0.5 * dy * dy);
+                    if (S) {
+                        double pm = e->alpha * dLda_mag;
+                        S[G_SIG] += e->ep * dLda_mag;
+                        S[G_U] += pm * (fabs(g->A * dx) + fabs(g->B * dy));
+                        S[G_V] += pm * (fabs(g->C * dy) + fabs(g->B * dx));
+                        S[G_A] += pm * 0.5 * dx * dx;
+                        S[G_B] += pm * fabs(dx * dy);
+                        S[G_C] += pm * 0.5 * dy * dy;
+                    }
                 }
             }
             free(list);
@@ -775,8 +937,15 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
             chain_to_3d(&s, i, cams + v, tot, pr[i].clamped, gm + 3 * i, gq + 4 * i, gs + 3 * i, go + i,
                         gsh + (size_t)3 * K * i);
             if (grad2d_norm) grad2d_norm[i] += sqrt(tot[G_U] * tot[G_U] + tot[G_V] * tot[G_V]);
+            if (mag) {
+                double S[G_N] = {0};
+                for (int t = 0; t < nth; t++)
+                    for (int k = 0; k < G_N; k++) S[k] += s2[((size_t)t * m + j) * G_N + k];
+                double *mg = mag + (size_t)P * i;
+                chain_to_3d_abs(&s, i, cams + v, S, pr[i].clamped, mg, mg + 3, mg + 7, mg + 10, mg + 11);
+            }
         }
-        free(g2); free(slot); free(order); free(pr);
+        free(g2); free(s2); free(slot); free(order); free(pr);
     }
 }
 

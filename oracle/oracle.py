@@ -166,8 +166,10 @@ def render(scene, cams, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=None) -> dict:
     return out
 
 
-def backward(scene, cams, dL_drgb, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=None) -> dict:
-    """Gradients of sum_v <dL/dI_v, I_v>.  dL_drgb: [V,3,H,W] (pixels None) or [npix,3]."""
+def backward(scene, cams, dL_drgb, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=None, mag=False) -> dict:
+    """Gradients of sum_v <dL/dI_v, I_v>.  dL_drgb: [V,3,H,W] (pixels None) or [npix,3].
+    mag=True adds out["mag"][class] (same shapes): each element's sum of absolute per-pixel
+    terms carried through |chain Jacobian| (oracle.c orc_backward), the rounding allowance's scale."""
     arrs, sargs = _scene_args(scene)
     ca, V = _cams(cams)
     cam0 = cams[0] if isinstance(cams, (list, tuple)) else cams
@@ -183,9 +185,14 @@ def backward(scene, cams, dL_drgb, mode="recipe", bg=(0.0, 0.0, 0.0), pixels=Non
                opacity_logits=np.zeros(n), sh=np.zeros((n, K, 3)), grad2d_norm=np.zeros(n),
                flagged=np.zeros(n, np.int32))
     bga = np.asarray(bg, np.float64)
+    P = 11 + 3 * K
+    mg = np.zeros((n, P)) if mag else None
     lib().orc_backward(C.c_int(_MODES[mode]), *sargs, C.c_int(V), ca, _p(bga), C.c_int64(pix.shape[0]), _p(pix),
                        _p(g), *[_p(out[k]) for k in ("means", "quats", "log_scales", "opacity_logits", "sh",
-                                                      "grad2d_norm", "flagged")])
+                                                      "grad2d_norm", "flagged")], _p(mg) if mag else None)
+    if mag:
+        out["mag"] = dict(means=mg[:, 0:3].copy(), quats=mg[:, 3:7].copy(), log_scales=mg[:, 7:10].copy(),
+                          opacity_logits=mg[:, 10].copy(), sh=mg[:, 11:].reshape(n, K, 3).copy())
     return out
 
 

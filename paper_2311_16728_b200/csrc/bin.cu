@@ -355,12 +355,14 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
                              2 * SMEM_BINS * (int)sizeof(uint32_t));
         attr = true;
     }
-    if (L.n > 0)
+    if (L.n > 0) {
+        ProfScope prof_scatter("k_bin_scatter", s);
         launch_pdl(k_bin_scatter, (unsigned)((L.n + BIN_THREADS - 1) / BIN_THREADS), BIN_THREADS, smem, s, 
             at<int4>(ws, L.rect), at<int32_t>(ws, L.radius), at<float4>(ws, L.rec0), at<float4>(ws, L.rec1),
             at<uint64_t>(ws, L.tile_mask), at<float>(ws, L.depth), at<uint32_t>(ws, L.vis_list),
             at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_cursor), L.n, L.V, L.TX, L.tiles, L.cap,
             at<uint64_t>(ws, L.keys1), at<WsHeader>(ws, L.hdr));
+    }
     ProfScope prof("k_tile_sort", s);
     const RecSrc rs{at<float4>(ws, L.rec0), at<float4>(ws, L.rec1), at<float4>(ws, L.rec2), at<float4>(ws, L.prec), 0};
     launch_pdl(k_tile_sort_small, (unsigned)VT, SG_WARPS * 32, 0, s,

@@ -373,6 +373,7 @@ cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int 
     dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, V * 3);
     const int nbt = grid.x * grid.y;
     float invN = (float)(1.0 / (3.0 * H * W));
+    ProfScope prof("k_ssim", s);
     launch_pdl(k_ssim_fwd, grid, NT, 0, s, render, gt, H, W, win, dA, dB, dC, part);
     if (dL)
         launch_pdl(k_ssim_bwd, grid, NT, 0, s, render, gt, H, W, win, lambda, invN, dA, dB, dC, dL, part, loss);

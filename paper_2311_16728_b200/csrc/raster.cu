@@ -898,6 +898,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
 bool fused_tile_schedule(const Layout &L) { return (int64_t)L.V * L.tiles <= 1024 * TSCAN_ITEMS; }
 
 cudaError_t launch_tile_scan(const Layout &L, void *ws, cudaStream_t s) {
+    ProfScope prof("k_tile_scan", s);
     launch_pdl(k_tile_scan, 1, 1024, 0, s, at<uint32_t>(ws, L.tile_count), L.V * L.tiles, L.cap,
                at<uint32_t>(ws, L.tile_start), at<WsHeader>(ws, L.hdr), L.max_chunks > 0 ? 1 : 0,
                at<uint32_t>(ws, L.chunk_base), at<uint32_t>(ws, L.chunk_tile), at<uint32_t>(ws, L.chunk_order),

@@ -6,5 +6,5 @@ intrinsics, ground-truth-like images).  It contains none of the method's arithme
 """
 from .scenes import (  # noqa: F401
     CONFIGS, Camera, Scene, make_scene, make_cameras, noise_image, perturb,
-    level_shape, config, densify_samples, make_keypoints,
+    level_shape, config, densify_samples, make_keypoints, edge_scene,
 )

@@ -325,6 +325,36 @@ def perturb(scene: Scene, seed: int) -> Scene:
     return s
 
 
+def edge_scene(cfg, cam: Camera, n: int | None = None, seed: int = 0, frac_beyond: float = 0.05) -> Scene:
+    """The workload's scene with the method's degenerate cases made common (parity inputs):
+    opacity logits U(-2, 7) (sigma up to 0.999: alpha = min(0.99, .) clamps near the centres,
+    SPEC.md:348), SH DC U(-3, 1.5) (negative colour channels: the max(0, .) clamp of R6), and a
+    fraction of Gaussians moved beyond the EWA tan clamp of `cam` (|x/z| or |y/z| in 1.05-1.4 x
+    lim, R15) with footprints large enough to reach into the image."""
+    s = make_scene(cfg, n=n)
+    rng = np.random.default_rng(np.random.PCG64(10_000 + seed))
+    m = s.n
+    s.opacity_logits[:] = rng.uniform(-2.0, 7.0, size=m).astype(np.float32)
+    s.sh[:, 0, :] = rng.uniform(-3.0, 1.5, size=(m, 3)).astype(np.float32)
+    k = int(frac_beyond * m)
+    idx = rng.choice(m, size=k, replace=False)
+    z = rng.uniform(1.0, 3.0, size=k)
+    lim_x = cam.lim_x if math.isfinite(cam.lim_x) else 1.3 * (0.5 * cam.width) / cam.fx
+    lim_y = cam.lim_y if math.isfinite(cam.lim_y) else 1.3 * (0.5 * cam.height) / cam.fy
+    side = rng.integers(0, 3, size=k)  # 0: beyond in x, 1: in y, 2: both
+    tx = np.where(side != 1, rng.choice([-1.0, 1.0], size=k) * lim_x * rng.uniform(1.05, 1.4, size=k),
+                  rng.uniform(-0.5, 0.5, size=k) * lim_x)
+    ty = np.where(side != 0, rng.choice([-1.0, 1.0], size=k) * lim_y * rng.uniform(1.05, 1.4, size=k),
+                  rng.uniform(-0.5, 0.5, size=k) * lim_y)
+    pc = np.stack([tx * z, ty * z, z], 1)
+    R, t = cam.R.astype(np.float64), cam.t.astype(np.float64)
+    s.means[idx] = ((pc - t) @ R).astype(np.float32)   # P = R^T (p_c - t)
+    # 3-sigma footprint of ~0.3 lim z: reaches well inside the image from beyond the clamp
+    s.log_scales[idx] = np.log(0.12 * lim_x * z[:, None] * rng.uniform(0.8, 1.25, size=(k, 3))).astype(np.float32)
+    s.meta = dict(s.meta, edge=True, beyond=idx)
+    return s
+
+
 def densify_samples(n: int, seed: int) -> np.ndarray:
     """Standard-normal samples [n][2][3] float32: the randomness densify draws (one offset per
     clone, two per split), generated here and passed to both sides as an input."""

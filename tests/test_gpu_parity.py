@@ -326,14 +326,40 @@ def test_adam_parity(sgd):
 
 
 # ------------------------------------------------------------------------------ backward
-def _check_grads(got, ref, flagged):
+EPS32 = 2.0 ** -24
+MAG_FACTOR = 8.0   # fp32 sums / products, ex2.approx, T recovery
+
+
+def _check_grads(got, ref, flagged, tag=None):
+    """Per element |gpu - oracle| <= 1e-3 |g_ref| + 8 * 2^-24 * mag (SURVEY §8(c) contract item 5,
+    with the rounding allowance scaled by the oracle's sum of absolute per-pixel terms carried
+    through |chain Jacobian| -- orc_backward's `mag`), excluding Gaussians evaluated at
+    band-flagged pixels.  Records the worst ratio |delta| / (2^-24 mag) per class."""
     keep = flagged == 0
+    worst, fails = {}, []
     for c in CLASSES:
-        a, b = got[c][keep], ref[c][keep]
-        rms = math.sqrt(float((ref[c] ** 2).mean())) + 1e-30
-        tol = 1e-3 * np.maximum(np.abs(b), 5e-2 * rms)
-        bad = np.abs(a - b) > tol
-        assert bad.sum() == 0, (c, int(bad.sum()), float(np.abs(a - b)[bad].max()), rms)
+        a, b, mg = got[c][keep], ref[c][keep], ref["mag"][c][keep]
+        tol = 1e-3 * np.abs(b) + MAG_FACTOR * EPS32 * mg
+        d = np.abs(a - b)
+        bad = d > tol
+        excess = np.maximum(d - 1e-3 * np.abs(b), 0)
+        worst[c] = float((excess / np.maximum(EPS32 * mg, 1e-38)).max(initial=0))
+        if bad.sum():
+            fails.append((c, int(bad.sum()), float(d[bad].max()), float(mg[bad][np.argmax(d[bad])])))
+    _record(tag, dict(worst_excess_over_eps_mag=worst, excluded=int((~keep).sum()), gaussians=int(keep.size)))
+    assert not fails, fails
+
+
+def _record(tag, d):
+    """Parity statistics for DESIGN.md (gpurun_out/parity_stats.jsonl when run on the GPU box)."""
+    if tag is None:
+        return
+    import json
+    import os
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "parity_stats.jsonl"), "a") as f:
+        f.write(json.dumps(dict(test=tag, **d)) + "\n")
 
 
 def test_backward_parity_tiny():
@@ -347,15 +373,15 @@ def test_backward_parity_tiny():
     gn = torch.zeros(scene.means.shape[0], device="cuda")
     r.backward(params, cams, torch.from_numpy(G).cuda(), grads, gn)
     got = unpack(grads, scene.means.shape[0], D)
-    ref = orc.backward(scene, cams, G, "recipe")
-    _check_grads(got, ref, ref["flagged"])
+    ref = orc.backward(scene, cams, G, "recipe", mag=True)
+    _check_grads(got, ref, ref["flagged"], "backward_tiny")
     keep = ref["flagged"] == 0
     np.testing.assert_allclose(gn.cpu().numpy()[keep], ref["grad2d_norm"][keep], rtol=1e-3,
                                atol=1e-5 * ref["grad2d_norm"].max())
 
 
 @pytest.mark.parametrize("cfg,views,level,D", [("tum", 1, 0, 3), ("tum", 1, 2, 3), ("euroc", 3, 1, 3),
-                                                ("euroc", 6, 2, 3), ("euroc", 16, 2, 3)])
+                                                ("euroc", 6, 2, 3), ("euroc", 16, 2, 3), ("replica", 1, 0, 3)])
 def test_backward_parity_sampled(cfg, views, level, D):
     """dL/dI masked to 4096 sampled pixels on both sides (SURVEY §8(d) 'Parity runs'), up to 16
     views per call (the EuRoC keyframe batch of one GPU)."""
@@ -371,8 +397,8 @@ def test_backward_parity_sampled(cfg, views, level, D):
     grads = torch.zeros_like(params)
     r.backward(params, cams, torch.from_numpy(G).cuda(), grads)
     got = unpack(grads, scene.means.shape[0], D)
-    ref = orc.backward(scene, cams, gp, "recipe", pixels=pix)
-    _check_grads(got, ref, ref["flagged"])
+    ref = orc.backward(scene, cams, gp, "recipe", pixels=pix, mag=True)
+    _check_grads(got, ref, ref["flagged"], f"backward_{cfg}_v{views}_l{level}")
 
 
 def test_backward_accumulates_and_zero_upstream():
