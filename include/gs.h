@@ -243,6 +243,41 @@ gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, floa
    GS_ERR_CAPACITY if bit 0 is set. */
 gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, int32_t *flags, int64_t *pairs);
 
+/* ---- A10 + A11 fused over peer memory (SURVEY §8(e) extension f3; north_star: "Gaussian-
+   parameter gradients are summed ... over NVLink"; the optimiser step PAPER.md:568, R20).
+   Data parallelism over keyframe views: every rank's backward adds its views' gradient into its
+   own [K][ld] gradient buffer; the step's gradient is the sum over ranks (R22).  Rank g owns the
+   flat element range [e_begin, e_end) of the [K][ld] layout (gs_comm_shard: world ranges of
+   whole float4s, the last one shorter).
+
+   gs_reduce_adam_bcast: for every element of the rank's range, g = sum over ranks of
+   grad_peers[q][e] (with grad_mc / param_mc -- multicast addresses of NVLink SHARP groups -- one
+   multimem.ld_reduce; else peer loads summed in rank order 0..world-1), the Adam update of
+   gs_adam_step (same arithmetic, same bits; columns >= n left as they are) on m_shard / v_shard
+   (device, the range's moments, index e - e_begin), then the new value is stored into
+   param_peers[q][e] and 0 into grad_peers[q][e] for every rank q (multimem.st on the multicast
+   addresses, else one peer store per rank).  param_peers / grad_peers: host arrays of `world`
+   device pointers valid on this device (this rank's own buffers at index `rank`;
+   param_peers[rank] must equal params->data); the buffers are symmetric (same n, ld on every
+   rank) and owned by the caller.  step >= 1, or step_dev (device int64, read by the kernel:
+   the bias corrections of graph replays) with step ignored.
+   gs_peer_barrier: every rank's earlier work on its stream completes and becomes visible to all
+   ranks before any rank's later work starts: flag_peers = host array of `world` device
+   pointers to each rank's uint32[world] flag array (zeroed by the caller before the first call,
+   symmetric), epoch = this rank's device uint32 barrier count; step_dev (optional) is
+   incremented once the barrier passed.  A step is: backward -> gs_peer_barrier(step_dev) ->
+   gs_reduce_adam_bcast(step_dev) -> gs_peer_barrier(NULL).  Both calls only enqueue (graph
+   capturable).  GS_ERR_INVALID_ARG for a NULL pointer, world outside [1, 8] or rank outside
+   [0, world); GS_ERR_SHAPE for ld % 4 != 0.  Errors not detected: peers calling with different
+   shapes or barrier counts (the barrier then waits forever -- a caller contract). */
+gs_status gs_comm_shard(int64_t n, int32_t sh_degree, int32_t rank, int32_t world, int64_t *e_begin, int64_t *e_end);
+gs_status gs_peer_barrier(uint32_t *const *flag_peers, int32_t rank, int32_t world, uint32_t *epoch,
+                          int64_t *step_dev, gs_stream_t stream);
+gs_status gs_reduce_adam_bcast(const gs_params *params, float *const *param_peers, float *const *grad_peers,
+                               float *param_mc, float *grad_mc, float *m_shard, float *v_shard,
+                               const gs_adam_hparams *hp, int64_t step, const int64_t *step_dev, int32_t rank,
+                               int32_t world, gs_stream_t stream);
+
 /* Enqueues on stream a copy of the workspace status into dst[0..1] (device or pinned host
    int32): dst[0] = flags (bit 0 = pair capacity overflow of the last gs_preprocess: that call's
    outputs are invalid), dst[1] = its pair count.  Does not synchronise, so it can sit inside a

@@ -731,7 +731,9 @@ static void chain_to_3d(const orc_scene *s, int64_t i, const orc_camera *cam, co
    mag (optional, [n][3+4+3+1+3K] in that class order): the conditioning of each gradient
    element -- for every 2-D quantity k (u, v, A, B, C, sigma, r, g, b) the sum over pixels of
    the absolute values of the per-pixel terms that make up its gradient, S_k (each product split
-   into its addends: dL/dalpha from |g||c| + |g||acc|, dL/du from |A dx| + |B dy|, ...), carried
+   into its addends: dL/dalpha from |g||c| + |g||acc|, dL/du from |A dx| + |B dy|, ...; every
+   term weighted by its pixel's transmittance conditioning kappa = 1 + sum_j alpha_j/(1-alpha_j)
+   over the composited layers), carried
    to the parameters by chain_to_3d_abs (the chain with |coefficients| and |intermediates|).  An
    evaluation in precision eps (any summation order, any association of the chain) is within a
    small multiple of eps * mag of the exact value; the GPU parity tests use it as their rounding
@@ -889,6 +891,12 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
                     }
                 }
                 double acc[3] = {bg[0], bg[1], bg[2]};
+                /* transmittance conditioning of this pixel (rounding allowance only): a relative
+                   error delta in every alpha_j moves each T_k by up to sum_j alpha_j/(1-alpha_j)
+                   delta relative -- d log T / d alpha_j = -1/(1-alpha_j) */
+                double kappa = 1.0;
+                if (mine_s)
+                    for (int c = 0; c < nc; c++) kappa += list[c].alpha / (1.0 - list[c].alpha);
                 for (int c = nc - 1; c >= 0; c--) {
                     const orc_contrib *e = list + c;
                     const orc_proj *g = pr + e->k;
@@ -901,10 +909,10 @@ void orc_backward(int mode, int64_t n, int D, const float *means, const float *q
                         acc[ch] = e->alpha * g->rgb[ch] + (1.0 - e->alpha) * acc[ch];
                     }
                     dLda *= e->T;
-                    dLda_mag *= e->T;
+                    dLda_mag *= e->T * kappa;
                     double *S = mine_s ? mine_s + slot[e->k] * G_N : NULL;
                     if (S)
-                        for (int ch = 0; ch < 3; ch++) S[G_R + ch] += fabs(gpix[ch] * e->alpha * e->T);
+                        for (int ch = 0; ch < 3; ch++) S[G_R + ch] += fabs(gpix[ch] * e->alpha * e->T) * kappa;
                     if (e->clamped) continue; /* alpha = 0.99 constant */
                     G[G_SIG] += e->ep * dLda;
                     double dLdp = e->alpha * dLda;

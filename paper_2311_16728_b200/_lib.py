@@ -28,7 +28,8 @@ EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
            "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
            "gs_densify_plan", "gs_densify_apply", "gs_densify_tags", "gs_geometry_densify",
-           "gs_query_status", "gs_status_async", "gs_workspace_release", "gs_status_str", "gs_spatial_order_temp_size", "gs_spatial_order",
+           "gs_query_status", "gs_status_async", "gs_workspace_release", "gs_status_str",
+           "gs_comm_shard", "gs_peer_barrier", "gs_reduce_adam_bcast", "gs_spatial_order_temp_size", "gs_spatial_order",
            "gs_permute_columns", "gs_sort_temp_size", "gs_debug_sort_pairs",
            "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
@@ -232,6 +233,35 @@ def gs_adam_step_rows(params: GsParams, grads, m_rows, v_rows, hp: GsAdamHparams
     _check(lib().gs_adam_step_rows(C.byref(params), _ptr(grads), _ptr(m_rows), _ptr(v_rows), C.byref(hp),
                                    C.c_int64(step), C.c_int32(row_begin), C.c_int32(row_end),
                                    C.c_int32(int(zero_grads)), _stream(stream)), "gs_adam_step_rows")
+
+
+def gs_comm_shard(n: int, sh_degree: int, rank: int, world: int) -> tuple[int, int]:
+    e0, e1 = C.c_int64(), C.c_int64()
+    _check(lib().gs_comm_shard(C.c_int64(n), C.c_int32(sh_degree), C.c_int32(rank), C.c_int32(world),
+                               C.byref(e0), C.byref(e1)), "gs_comm_shard")
+    return e0.value, e1.value
+
+
+def _ptr_array(ptrs) -> C.Array:
+    return (C.c_void_p * len(ptrs))(*[C.c_void_p(int(p)) for p in ptrs])
+
+
+def gs_peer_barrier(flag_ptrs, rank: int, world: int, epoch: torch.Tensor, step_dev: torch.Tensor | None,
+                    stream=None):
+    """flag_ptrs: `world` device addresses (ints) of each rank's uint32[world] flags."""
+    _check(lib().gs_peer_barrier(_ptr_array(flag_ptrs), C.c_int32(rank), C.c_int32(world), _ptr(epoch),
+                                 _ptr(step_dev), _stream(stream)), "gs_peer_barrier")
+
+
+def gs_reduce_adam_bcast(params: GsParams, param_ptrs, grad_ptrs, param_mc: int, grad_mc: int, m_shard, v_shard,
+                         hp: GsAdamHparams, step: int, step_dev: torch.Tensor | None, rank: int, world: int,
+                         stream=None):
+    """param_ptrs / grad_ptrs: `world` device addresses (ints); param_mc / grad_mc: multicast
+    addresses or 0."""
+    _check(lib().gs_reduce_adam_bcast(C.byref(params), _ptr_array(param_ptrs), _ptr_array(grad_ptrs),
+                                      C.c_void_p(param_mc or None), C.c_void_p(grad_mc or None), _ptr(m_shard),
+                                      _ptr(v_shard), C.byref(hp), C.c_int64(step), _ptr(step_dev), C.c_int32(rank),
+                                      C.c_int32(world), _stream(stream)), "gs_reduce_adam_bcast")
 
 
 def gs_densify_temp_size(n: int) -> int:

@@ -466,6 +466,40 @@ gs_status gs_query_status(const void *ws, size_t ws_bytes, gs_stream_t stream, i
     return (h.flags & 1u) ? GS_ERR_CAPACITY : GS_OK;
 }
 
+gs_status gs_comm_shard(int64_t n, int32_t sh_degree, int32_t rank, int32_t world, int64_t *e_begin, int64_t *e_end) {
+    if (!e_begin || !e_end || n < 0 || sh_degree < 0 || sh_degree > 3 || world < 1 || world > 8 || rank < 0 ||
+        rank >= world)
+        return GS_ERR_INVALID_ARG;
+    comm_shard((int64_t)gs_param_rows(sh_degree) * gs_param_ld(n), rank, world, e_begin, e_end);
+    return GS_OK;
+}
+
+gs_status gs_peer_barrier(uint32_t *const *flag_peers, int32_t rank, int32_t world, uint32_t *epoch,
+                          int64_t *step_dev, gs_stream_t stream) {
+    if (!flag_peers || !epoch || world < 1 || world > 8 || rank < 0 || rank >= world) return GS_ERR_INVALID_ARG;
+    for (int q = 0; q < world; q++)
+        if (!flag_peers[q]) return GS_ERR_INVALID_ARG;
+    return cuda_status(launch_peer_barrier(flag_peers, rank, world, epoch, step_dev, (cudaStream_t)stream));
+}
+
+gs_status gs_reduce_adam_bcast(const gs_params *params, float *const *param_peers, float *const *grad_peers,
+                               float *param_mc, float *grad_mc, float *m_shard, float *v_shard,
+                               const gs_adam_hparams *hp, int64_t step, const int64_t *step_dev, int32_t rank,
+                               int32_t world, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    if (!hp || !param_peers || !grad_peers || world < 1 || world > 8 || rank < 0 || rank >= world) return GS_ERR_INVALID_ARG;
+    if (!step_dev && step < 1) return GS_ERR_INVALID_ARG;
+    if (!hp->sgd_mode && (!m_shard || !v_shard)) return GS_ERR_INVALID_ARG;
+    if ((param_mc == nullptr) != (grad_mc == nullptr)) return GS_ERR_INVALID_ARG;
+    for (int q = 0; q < world; q++)
+        if (!param_peers[q] || !grad_peers[q]) return GS_ERR_INVALID_ARG;
+    if (param_peers[rank] != params->data) return GS_ERR_INVALID_ARG;
+    if (params->ld % 4) return GS_ERR_SHAPE;
+    return cuda_status(launch_reduce_adam_bcast(*params, param_peers, grad_peers, param_mc, grad_mc, m_shard, v_shard,
+                                                *hp, step, step_dev, rank, world, (cudaStream_t)stream));
+}
+
 gs_status gs_status_async(const void *ws, size_t ws_bytes, int32_t *dst, gs_stream_t stream) {
     if (!ws || !dst || ws_bytes < sizeof(WsHeader)) return GS_ERR_INVALID_ARG;
     // WsHeader starts with {flags, P}: one async 8-byte copy (a memcpy node when captured)

@@ -246,6 +246,61 @@ int hi_bits_for(int64_t count);
 cudaError_t launch_preprocess(const gs_params &p, const CamBatch &cams, int V, const Layout &L, void *ws,
                               bool count_tiles, cudaStream_t s);
 // exclusive scan of `count` u32 (decoupled look-back); writes the total to hdr->P
+// ---- A11 arithmetic shared by the Adam kernels (pyramid_adam.cu) and the fused reduce + Adam +
+// broadcast over peer memory (comm.cu): one definition, so both give the same bits.
+struct AdamArgs {
+    float lr[6];      // per class; in Adam mode already divided by (1 - beta1^t)
+    float b1, b2, eps;
+    float rs_bc2;     // 1 / sqrt(1 - beta2^t)
+    int sgd, zero;
+    const int64_t *step_dev;  // non-null: t read on the device; lr[] hold the raw rates
+};
+
+// device-step mode: bias corrections from t = *step_dev, once per CTA
+__device__ __forceinline__ void adam_device_step(AdamArgs &a) {
+    if (!a.step_dev || a.sgd) return;
+    __shared__ float s_lr[6], s_rs;
+    if (threadIdx.x == 0) {
+        const double t = (double)*a.step_dev;
+        const double bc1 = 1.0 - pow((double)a.b1, t), bc2 = 1.0 - pow((double)a.b2, t);
+        for (int k = 0; k < 6; k++) s_lr[k] = (float)((double)a.lr[k] / bc1);
+        s_rs = (float)(1.0 / sqrt(bc2));
+    }
+    __syncthreads();
+    for (int k = 0; k < 6; k++) a.lr[k] = s_lr[k];
+    a.rs_bc2 = s_rs;
+}
+
+__device__ __forceinline__ int row_class(int row) {
+    return row < 3 ? 0 : row < 7 ? 1 : row < 10 ? 2 : row == 10 ? 3 : row < 14 ? 4 : 5;
+}
+
+// p -= lr m_hat / (sqrt(v_hat) + eps) with m_hat = m / bc1, v_hat = v / bc2, rewritten as
+// p -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps); sqrt and the division use the SFU
+// approximations (rel. error ~1e-7, inside the 1e-6 parity contract), which keeps the kernel
+// at the HBM roofline instead of the IEEE div/sqrt instruction sequences.
+__device__ __forceinline__ void adam1(float &p, float &g, float &m, float &v, float lr, const AdamArgs &a) {
+    if (a.sgd) {
+        p = p - lr * g;
+    } else {
+        m = a.b1 * m + (1.f - a.b1) * g;
+        v = a.b2 * v + (1.f - a.b2) * g * g;
+        float sq = v > 0.f ? v * rsqrtf(v) : 0.f;
+        p = p - __fdividef(lr * m, sq * a.rs_bc2 + a.eps);
+    }
+    if (a.zero) g = 0.f;
+}
+
+AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero, const int64_t *step_dev = nullptr);
+
+// fused A10 + A11 over peer memory (comm.cu)
+void comm_shard(int64_t total, int rank, int world, int64_t *e0, int64_t *e1);
+cudaError_t launch_peer_barrier(uint32_t *const *flags, int rank, int world, uint32_t *epoch_dev, int64_t *step_dev,
+                                cudaStream_t s);
+cudaError_t launch_reduce_adam_bcast(const gs_params &p, float *const *param_peers, float *const *grad_peers,
+                                     float *p_mc, float *g_mc, float *m, float *v, const gs_adam_hparams &hp,
+                                     int64_t step, const int64_t *step_dev, int rank, int world, cudaStream_t s);
+
 cudaError_t launch_scan_u32(const uint32_t *in, uint32_t *out, int64_t count, uint64_t *flags, WsHeader *hdr,
                             cudaStream_t s, int in_stride = 1);
 // binning mode: 0 = tile buckets + in-tile sort (bin.cu), 1 = global onesweep LSD radix sort

@@ -64,49 +64,6 @@ cudaError_t launch_pyramid(const float *img, int N, int C, int H, int W, int lev
     return cudaGetLastError();
 }
 
-struct AdamArgs {
-    float lr[6];      // per class; in Adam mode already divided by (1 - beta1^t)
-    float b1, b2, eps;
-    float rs_bc2;     // 1 / sqrt(1 - beta2^t)
-    int sgd, zero;
-    const int64_t *step_dev;  // non-null: t read on the device; lr[] hold the raw rates
-};
-
-// device-step mode: bias corrections from t = *step_dev, once per CTA
-__device__ __forceinline__ void adam_device_step(AdamArgs &a) {
-    if (!a.step_dev || a.sgd) return;
-    __shared__ float s_lr[6], s_rs;
-    if (threadIdx.x == 0) {
-        const double t = (double)*a.step_dev;
-        const double bc1 = 1.0 - pow((double)a.b1, t), bc2 = 1.0 - pow((double)a.b2, t);
-        for (int k = 0; k < 6; k++) s_lr[k] = (float)((double)a.lr[k] / bc1);
-        s_rs = (float)(1.0 / sqrt(bc2));
-    }
-    __syncthreads();
-    for (int k = 0; k < 6; k++) a.lr[k] = s_lr[k];
-    a.rs_bc2 = s_rs;
-}
-
-__device__ __forceinline__ int row_class(int row) {
-    return row < 3 ? 0 : row < 7 ? 1 : row < 10 ? 2 : row == 10 ? 3 : row < 14 ? 4 : 5;
-}
-
-// p -= lr m_hat / (sqrt(v_hat) + eps) with m_hat = m / bc1, v_hat = v / bc2, rewritten as
-// p -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps); sqrt and the division use the SFU
-// approximations (rel. error ~1e-7, inside the 1e-6 parity contract), which keeps the kernel
-// at the HBM roofline instead of the IEEE div/sqrt instruction sequences.
-__device__ __forceinline__ void adam1(float &p, float &g, float &m, float &v, float lr, const AdamArgs &a) {
-    if (a.sgd) {
-        p = p - lr * g;
-    } else {
-        m = a.b1 * m + (1.f - a.b1) * g;
-        v = a.b2 * v + (1.f - a.b2) * g * g;
-        float sq = v > 0.f ? v * rsqrtf(v) : 0.f;
-        p = p - __fdividef(lr * m, sq * a.rs_bc2 + a.eps);
-    }
-    if (a.zero) g = 0.f;
-}
-
 constexpr int ADAM_THREADS = 256;
 constexpr int ADAM_UNROLL = 2;
 
@@ -250,7 +207,7 @@ cudaError_t launch_grad_accumulate(const gs_params &p, const Layout &L, void *ws
     return cudaGetLastError();
 }
 
-static AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero, const int64_t *step_dev = nullptr) {
+AdamArgs adam_args(const gs_adam_hparams &hp, int64_t step, int zero, const int64_t *step_dev) {
     AdamArgs a;
     a.step_dev = step_dev;
     if (step_dev) step = 1;  // placeholder; the kernel derives the corrections from *step_dev

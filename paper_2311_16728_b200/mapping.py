@@ -149,7 +149,7 @@ class MappingEngine:
     def __init__(self, scene, cams, gts, n_levels: int = 2, lam: float = 0.2, adam: AdamConfig | None = None,
                  device: str = "cuda", capacity_margin: float = 1.3, group=None, bg=(0.0, 0.0, 0.0),
                  shard_optimizer: bool = True, densify_cfg: DensifyConfig | None = None,
-                 spatial_order: bool = True):
+                 spatial_order: bool = True, comm: str = "nccl"):
         self.device = device
         self.n = scene.means.shape[0]
         self.D = int(round(math.sqrt(scene.sh.shape[1]))) - 1
@@ -166,10 +166,20 @@ class MappingEngine:
             packed = permute_columns(packed, perm, self.n)
             self.order = perm.to(torch.int64)
         self.sharded = None
+        self.peer = None
         self._pipe = None
         self._status = None
         self.graph = None
-        if shard_optimizer and dist.is_available() and dist.is_initialized():
+        self.adam_cfg = adam
+        if comm not in ("nccl", "peer"):
+            raise ValueError("comm: 'nccl' (collectives) or 'peer' (fused kernel over peer memory)")
+        if comm == "peer" and dist.is_available() and dist.is_initialized():
+            # A10 + A11 as one kernel over symmetric peer memory (comm.py, gs_reduce_adam_bcast)
+            from .comm import PeerAdam
+            self.peer = PeerAdam(self.n, self.D, adam, group, device)
+            self.peer.params[:, :packed.shape[1]] = packed
+            self.params, self.grads = self.peer.params, self.peer.grads
+        elif shard_optimizer and dist.is_available() and dist.is_initialized():
             # reduce-scatter -> row-sharded Adam -> all-gather (parameters / gradients live in
             # the first K rows of buffers padded to world x R rows)
             pp = self._padded(packed)
@@ -186,7 +196,7 @@ class MappingEngine:
         # 1 = temporary primitive from geometry-based densification
         self.temporary = torch.zeros(self.n, dtype=torch.uint8, device=device)
         # replicated optimiser state (single GPU / unsharded DP); the sharded one keeps its rows only
-        self.adam = Adam(self.params, self.n, self.D, adam) if self.sharded is None else None
+        self.adam = Adam(self.params, self.n, self.D, adam) if self.sharded is None and self.peer is None else None
         self.cams0 = list(cams)
         self.V = len(self.cams0)
         self.n_levels = n_levels
@@ -274,12 +284,14 @@ class MappingEngine:
                                self.max_radius)
         loss, dL = self.losses[level](rgb, self._pyramid(level))             # A7
         if fused is None:
-            fused = self.sharded is None and not self.distributed()
+            fused = self.sharded is None and self.peer is None and not self.distributed()
         if fused:
             r.backward_adam(self.params, cams, dL, self.adam, self.grad2d_norm, self.bg)  # A8-A9 + A11
         else:
             r.backward(self.params, cams, dL, self.grads, self.grad2d_norm, self.bg)  # A8-A9
-            if self.sharded is not None:
+            if self.peer is not None:
+                self.peer.step()                                             # A10 + A11 fused, peer memory
+            elif self.sharded is not None:
                 self.sharded.step()                                          # A10 + A11, row-sharded
             else:
                 reduce_gradients(self.grads, self.group)                     # A10
@@ -301,6 +313,8 @@ class MappingEngine:
 
     def _moments(self) -> tuple:
         """The full [K][ld] Adam moments of the current map (all-gathered when row-sharded)."""
+        if self.peer is not None:
+            return self.peer.full_state()
         if self.sharded is not None:
             m, v = self.sharded.full_state()
             K = self.params.shape[0]
@@ -312,7 +326,14 @@ class MappingEngine:
         buffers and per-level workspaces follow; captured graphs refer to the old buffers and are
         dropped."""
         self.n = n
-        if self.sharded is not None:
+        if self.peer is not None:
+            from .comm import PeerAdam
+            t = self.peer.t
+            self.peer = PeerAdam(n, self.D, self.adam_cfg, self.group, p.device)
+            self.peer.params[:, :p.shape[1]] = p[:, :self.peer.ld]
+            self.peer.load_state(m, v, t)
+            self.params, self.grads = self.peer.params, self.peer.grads
+        elif self.sharded is not None:
             pp = self._padded(p)
             self.sharded.rebind(pp, torch.zeros_like(pp), n, m, v)
             self.params, self.grads = self.sharded.params, self.sharded.grads
@@ -404,9 +425,11 @@ class MappingEngine:
         the targets and the D2H copy of the losses) -- into a CUDA graph; `replay()` then runs it
         with a single launch.  Single GPU only (the fused backward+Adam with a device-resident
         step counter; the DP path has an NCCL collective between backward and Adam)."""
-        if self.distributed() or self.sharded is not None:
-            raise RuntimeError("graph capture is for the single-GPU fused path")
-        self.adam.use_device_step()
+        if (self.distributed() and self.peer is None) or self.sharded is not None:
+            raise RuntimeError("graph capture: the single-GPU fused path or the peer-memory DP step (no NCCL call "
+                               "inside the step)")
+        if self.adam is not None:
+            self.adam.use_device_step()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         host = gts_pinned is not None

@@ -270,3 +270,21 @@ def test_gloo_world2_sharded_state_gather_and_rebind(tmp_path):
         mine = np.load(tmp_path / f"mine{r}.npy")
         full = np.arange(14 * 3, dtype=np.float64).reshape(14, 3)
         assert np.array_equal(mine, full[7 * r:7 * (r + 1)])
+
+
+def test_comm_shard_partition():
+    """gs_comm_shard (C ABI, host arithmetic): the world ranges tile [0, K ld) in order, each a
+    whole number of float4s, every rank but the last the same length."""
+    from paper_2311_16728_b200.comm import comm_shard
+    from paper_2311_16728_b200 import _lib as L
+    from paper_2311_16728_b200.core import param_rows
+    for n, D in ((1, 0), (1000, 0), (200_000, 3), (77, 2)):
+        total = param_rows(D) * L.param_ld(n)
+        for world in (1, 2, 3, 8):
+            rs = [comm_shard(n, D, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            assert all(e0 % 4 == 0 and e1 % 4 == 0 for e0, e1 in rs)
+            assert len({e1 - e0 for e0, e1 in rs[:-1]}) <= 1
+    with pytest.raises(L.GsError):
+        comm_shard(10, 0, 2, 2)

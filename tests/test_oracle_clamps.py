@@ -11,9 +11,10 @@
 * The fp32 scale recipe e = (float)exp((double)s) is the
   correctly rounded fp32 exp -- pinned against 60-digit mpmath, not against another rounding of
   a double exp.
-* orc_backward's `mag` (sum of absolute per-pixel terms through |chain Jacobian|): equals the
-  brute-force sum over pixels of |per-pixel gradient| where every per-pixel term has one sign
-  (opacity, SH DC of a lone Gaussian), bounds it everywhere (triangle inequality).
+* orc_backward's `mag` (sum of absolute per-pixel terms, each weighted by its pixel's
+  transmittance conditioning, through the absolute chain): equals the brute-force sum over
+  pixels of |per-pixel gradient| / T_final (= kappa for one layer) where every per-pixel term has
+  one sign (opacity, SH DC of a lone Gaussian), bounds |g| everywhere (triangle inequality).
 """
 import math
 
@@ -260,11 +261,13 @@ def test_mag_equals_bruteforce_for_single_signed_terms_and_bounds_everything():
                    np.int32)
     G = rng.uniform(0.1, 1.0, size=(pix.shape[0], 3))   # one sign: every per-pixel term of one sign
     g = orc.backward(s, [cam], G, "fp64", pixels=pix, mag=True)
+    # one layer per pixel: the transmittance conditioning kappa = 1 + alpha/(1 - alpha) = 1/T_final
+    Tf = orc.render(s, [cam], "fp64", pixels=pix)["T"]
     per = {c: np.zeros_like(g[c]) for c in CLASSES}
     for q in range(pix.shape[0]):
         gq = orc.backward(s, [cam], G[q:q + 1], "fp64", pixels=pix[q:q + 1])
         for c in CLASSES:
-            per[c] += np.abs(gq[c])
+            per[c] += np.abs(gq[c]) / Tf[q]
     assert per["opacity_logits"][0] > 0
     np.testing.assert_allclose(g["mag"]["opacity_logits"], per["opacity_logits"], rtol=1e-12)
     np.testing.assert_allclose(g["mag"]["sh"], per["sh"], rtol=1e-12)
