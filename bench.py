@@ -236,7 +236,9 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-CHUNK_MAX_TILES = 600  # views x tiles below this use the chunked raster path (gs_internal.cuh)
+def use_chunked(view_tiles: int, cap: int) -> bool:
+    """Mirror of gs_internal.cuh use_chunked: the chunk-parallel raster path."""
+    return view_tiles < 1000 or (view_tiles < 32768 and cap >= 200 * view_tiles)
 FUSED_SCHEDULE_TILES = 8192  # views x tiles up to this: one-CTA tile scan + schedule (raster.cu)
 
 
@@ -289,7 +291,7 @@ def run_ours(args):
     p0 = pack_params(scene)
     gt = rtmp.forward(p0, cams)[0].clone()
     del rtmp, p0
-    eng = MappingEngine(perturb(scene, 99), cams, gt, n_levels=cfg["levels"])
+    eng = MappingEngine(perturb(scene, 99), cams, gt, n_levels=cfg["levels"], comm=args.comm)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     iters_per_step = cfg["levels"] + 1
@@ -312,6 +314,26 @@ def run_ours(args):
             print(json.dumps({"launch_list": True, "config": args.config}), flush=True)
         return 0
 
+    if args.quick:  # A/B runs: the headline graph replay only
+        use_graph = world == 1 and not args.no_graph
+        if use_graph:
+            eng.capture()
+            for _ in range(3):
+                eng.replay()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            eng.replay() if use_graph else step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        eng.check()
+        ms = t0.elapsed_time(t1) / args.steps
+        if rank == 0:
+            print(json.dumps({"quick": True, "config": args.config, "value": iters_per_step * len(cams) * world / (ms * 1e-3),
+                              "ms_per_step": ms}), flush=True)
+        return 0
+
     # ---- per-stage breakdown (separate instrumented pass; not the headline)
     stage = {k: 0.0 for k in ("pyramid", "preprocess", "render_fwd", "loss", "backward", "allreduce", "adam")}
     reps = 5
@@ -331,7 +353,10 @@ def run_ours(args):
                 e[3].record(); r.backward(eng.params, c, dL, eng.grads, eng.grad2d_norm, eng.bg)
                 e[4].record()
                 from paper_2311_16728_b200.mapping import all_gather_rows, reduce_gradients, reduce_scatter_rows
-                if eng.sharded is not None:  # reduce-scatter | row-sharded Adam + all-gather
+                if eng.peer is not None:  # barrier | fused reduce + Adam + broadcast over peer memory
+                    e[5].record()
+                    eng.peer.step()
+                elif eng.sharded is not None:  # reduce-scatter | row-sharded Adam + all-gather
                     sh = eng.sharded
                     reduce_scatter_rows(sh.padded_grads, sh.R)
                     e[5].record()
@@ -372,7 +397,7 @@ def run_ours(args):
     # CUDA events recorded by libgs.so on its launching stream (gs_profile_kernel), one family per
     # pass of K eager steps; share = its summed launch time / the pass's step time
     live = {}
-    akern = "k_adam_fused" if world == 1 else "k_adam"
+    akern = "k_adam_fused" if world == 1 else ("k_reduce_adam_bcast" if eng.peer is not None else "k_adam")
     families = ["k_preprocess", "k_tile_scan", "k_bin_scatter", "k_tile_sort", "k_raster_fwd", "k_ssim",
                 "k_raster_bwd", "k_preprocess_bwd", akern]
     if world > 1:
@@ -395,7 +420,8 @@ def run_ours(args):
 
     # ---- headline: K timed steps (one CUDA-graph replay per step on a single GPU; eager
     # launches under torchrun, where the NCCL all-reduce sits inside the iteration)
-    use_graph = world == 1 and not args.no_graph
+    # one GPU, or the peer-memory DP step (no NCCL call inside a step): CUDA-graph replay
+    use_graph = (world == 1 or eng.peer is not None) and not args.no_graph
     if use_graph:
         eng.capture()
         for _ in range(2):
@@ -542,6 +568,8 @@ def run_ours(args):
     }
     if world == 1:
         adam_bytes = K * n * 24 + 4 * n  # fused: p, m, v read + written, a 4-byte slot per Gaussian
+    elif eng.peer is not None:  # this rank's range: G gradients read, m, v read + written, p read, G p + G g written
+        adam_bytes = (eng.peer.e1 - eng.peer.e0) * 4 * (world + 5 + 2 * world)
     elif eng.sharded is not None:  # this rank's rows only
         adam_bytes = (eng.sharded.r1 - eng.sharded.r0) * ld * 32
     else:
@@ -598,7 +626,7 @@ def run_ours(args):
     for r in eng.renderers:
         t = r.ws.tiles_x * r.ws.tiles_y * len(cams)
         bits = 32 + max(1, math.ceil(math.log2(max(t, 2))))
-        launches_step += launches_per_iteration(bits, world == 1, chunked=t < CHUNK_MAX_TILES, view_tiles=t)
+        launches_step += launches_per_iteration(bits, world == 1, chunked=use_chunked(t, r.ws.capacity), view_tiles=t)
     launches = args.steps * launches_step
 
     # ---- sorted keys/s (A4): the level-0 pairs of this step (keys (tile << 32 | depth bits),
@@ -634,7 +662,7 @@ def run_ours(args):
                   torch.equal((kk * 0 + vv.to(torch.int64)).sum(), v0["vals"][:P0].to(torch.int64).sum()))
         radix_ms = tot / reps
         bucket_ms = None
-        if eng.renderers[0].ws.tiles_x * eng.renderers[0].ws.tiles_y * len(cams) >= CHUNK_MAX_TILES:
+        if True:
             # level-0 share of the bucket kernels: launches are per level, level 0 is the last of each step
             L.gs_profile_kernel("k_tile_sort")
             eng.render(0)
@@ -711,6 +739,10 @@ def main():
                     help="oracle sample: level-0 pixels per step (the same fraction of every level and stage)")
     ap.add_argument("--launch-list", action="store_true", help="profile exactly one step (ncu range)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of graph replays")
+    ap.add_argument("--quick", action="store_true", help="A/B experiments: headline timing only (no extra keys)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N>1 optimiser exchange: NCCL reduce-scatter + row-sharded Adam + all-gather, or the "
+                         "fused reduce + Adam + broadcast kernel over peer memory (unmeasured on >1 GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -67,7 +67,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.big_tiles = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.tile_order = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.prec = take((size_t)3 * L.cap * sizeof(float4));
-    L.max_chunks = use_chunked((int64_t)V * L.tiles) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;
+    L.max_chunks = use_chunked((int64_t)V * L.tiles, L.cap) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;
     L.chunk_base = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.chunk_tile = take((size_t)std::max<int64_t>(L.max_chunks, 1) * sizeof(uint32_t));
     L.chunk_order = take((size_t)std::max<int64_t>(L.max_chunks, 1) * sizeof(uint32_t));

@@ -52,8 +52,17 @@ struct WsHeader {
 // list is replayed by its own CTAs from state the forward recorded (raster.cu).
 constexpr int CHUNK = 64;              // list entries per chunk of the chunked raster path
 constexpr int TILE_PIX = 256;          // pixels per 16x16 tile (per-chunk record stride)
-constexpr int CHUNK_MAX_TILES = 600;  // V * tiles below this uses the chunked path
-__host__ __device__ inline bool use_chunked(int64_t view_tiles) { return view_tiles < CHUNK_MAX_TILES; }
+// The chunked path wins where tile lists are long or tiles few (the tile-serial backward then
+// has a long tail: one CTA's list walk bounds the kernel); it loses ~1 % on short lists (TUM
+// level 0, ~120 pairs per tile).  Measured (graph replay, round 2): Replica 1.728 -> 1.655 ms,
+// EuRoC 16 views 7.47 -> 5.79 ms.  The per-(chunk, pixel) records cost 4 KB per chunk, so very
+// large view batches (the 64-view stress batch at level 0) keep the tile path.
+constexpr int CHUNK_MAX_TILES = 1000;        // V * tiles below this: always chunked
+constexpr int CHUNK_MAX_TILES_LONG = 32768;  // below this: chunked when lists are long
+constexpr int CHUNK_LONG_PAIRS = 200;        // "long": pair capacity >= this per (view, tile)
+__host__ __device__ inline bool use_chunked(int64_t view_tiles, int64_t cap) {
+    return view_tiles < CHUNK_MAX_TILES || (view_tiles < CHUNK_MAX_TILES_LONG && cap >= CHUNK_LONG_PAIRS * view_tiles);
+}
 
 // Byte offsets of every buffer inside a render workspace (pure function of n, V, W, H, cap).
 struct Layout {

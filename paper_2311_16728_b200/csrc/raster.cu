@@ -396,6 +396,34 @@ __device__ __forceinline__ float warp_sum9_transposed(float a[8], float b, int l
 // chunk back to front from (T after the chunk, colour behind it) -- the chunks run in parallel
 // instead of one after the other, and the longest dependent chain is CHUNK entries.
 
+// exclusive scan over the 1024 threads of a CTA (s_warp: 33 words of shared memory)
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    __syncthreads();  // s_warp may still be read by a previous call
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_warp[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += u;
+        }
+        s_warp[lane] = wi - w;
+        if (lane == 31) s_warp[32] = wi;
+    }
+    __syncthreads();
+    total = s_warp[32];
+    return s_warp[warp] + incl - v;
+}
+
 __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ ranges, int VT,
                                                       uint32_t *__restrict__ chunk_base,
                                                       uint32_t *__restrict__ chunk_tile,
@@ -403,58 +431,41 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
                                                       int64_t max_chunks) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
-    __shared__ uint32_t s[1024];
+    __shared__ uint32_t s_warp[33];
+    __shared__ uint32_t cnt[256];
     const int t = threadIdx.x;
-    uint32_t nch = 0;
-    if (t < VT) {
-        const uint2 r = ranges[t];
-        nch = (r.y - r.x + CHUNK - 1) / CHUNK;
+    const int per = (VT + 1023) / 1024;  // consecutive tiles per thread
+    const int i0 = t * per, i1 = min(VT, i0 + per);
+    auto nchunks = [&](int i) { const uint2 r = ranges[i]; return (r.y - r.x + CHUNK - 1) / CHUNK; };
+    uint32_t nsum = 0;
+    for (int i = i0; i < i1; i++) nsum += nchunks(i);
+    if (t < 256) cnt[t] = 0;
+    uint32_t total;
+    uint32_t cb = block_exclusive_scan(nsum, s_warp, total);
+    if (t == 0) hdr->nchunks = (uint32_t)min((int64_t)total, max_chunks);
+    for (int i = i0; i < i1; i++) {
+        const uint32_t nch = nchunks(i);
+        chunk_base[i] = cb;
+        for (uint32_t k = 0; k < nch; k++) {
+            if (cb + k < max_chunks) chunk_tile[cb + k] = (uint32_t)i;
+            atomicAdd(&cnt[min(k, 255u)], 1u);
+        }
+        cb += nch;
     }
-    s[t] = nch;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {  // inclusive scan
-        uint32_t v = t >= o ? s[t - o] : 0u;
-        __syncthreads();
-        s[t] += v;
-        __syncthreads();
-    }
-    const uint32_t base = s[t] - nch;
-    if (t < VT) chunk_base[t] = base;
-    if (t == 1023) hdr->nchunks = (uint32_t)min((int64_t)s[1023], max_chunks);
-    for (uint32_t k = 0; k < nch; k++)
-        if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
     // chunk order for the backward: by position in the tile list, first chunks first (most
     // pixels are still active there: the longest replays start first)
     __syncthreads();
-    uint32_t *cnt = s;  // reuse: [0, 256) counts per position class, then running offsets
-    if (t < 256) cnt[t] = 0;
+    const uint32_t hv = t < 256 ? cnt[t] : 0u;
+    uint32_t dummy;
+    const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
+    if (t < 256) cnt[t] = hb;
     __syncthreads();
-    for (uint32_t k = 0; k < nch; k++) atomicAdd(&cnt[min(k, 255u)], 1u);
-    __syncthreads();
-    if (t < 32) {  // exclusive scan of the 256 class counts by one warp
-        uint32_t v[8], sum = 0;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            v[k] = cnt[t * 8 + k];
-            sum += v[k];
+    for (int i = i0; i < i1; i++) {
+        const uint32_t nch = nchunks(i), base = chunk_base[i];
+        for (uint32_t k = 0; k < nch; k++) {
+            const uint32_t pos = atomicAdd(&cnt[min(k, 255u)], 1u);
+            if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
         }
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (t >= o) incl += u;
-        }
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            cnt[t * 8 + k] = run;
-            run += v[k];
-        }
-    }
-    __syncthreads();
-    for (uint32_t k = 0; k < nch; k++) {
-        const uint32_t pos = atomicAdd(&cnt[min(k, 255u)], 1u);
-        if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
     }
 }
 
@@ -800,33 +811,6 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2 *__restrict__ r
 // longest-list-first tile order -- so neither needs a launch of its own.
 constexpr int TSCAN_ITEMS = 8;  // counts per thread (1024 threads: up to 8192 tiles)
 
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-    }
-    __syncthreads();  // s_warp may still be read by a previous call
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t w = s_warp[lane];
-        uint32_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += u;
-        }
-        s_warp[lane] = wi - w;
-        if (lane == 31) s_warp[32] = wi;
-    }
-    __syncthreads();
-    total = s_warp[32];
-    return s_warp[warp] + incl - v;
-}
-
 __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__ counts, int VT, int64_t cap,
                                                     uint32_t *__restrict__ tile_start, WsHeader *hdr, int chunked,
                                                     uint32_t *__restrict__ chunk_base, uint32_t *__restrict__ chunk_tile,
@@ -856,26 +840,40 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
     const bool ok = (int64_t)P <= cap;  // overflow: nothing is binned, nothing to schedule
     if (t < 256) hist[t] = 0;
     __syncthreads();
-    if (chunked) {  // VT < CHUNK_MAX_TILES <= 1024: tile t = thread t (its counts are c[] of thread t / 8)
-        const uint32_t len = t < VT ? counts[(size_t)t * CNT_STRIDE] : 0u;
-        const uint32_t nch = ok ? (len + CHUNK - 1) / CHUNK : 0u;
+    if (chunked) {  // every thread its TSCAN_ITEMS tiles (c[] holds their list lengths)
+        uint32_t nsum = 0;
+#pragma unroll
+        for (int k = 0; k < TSCAN_ITEMS; k++) nsum += ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
         uint32_t total;
-        const uint32_t base = block_exclusive_scan(nch, s_warp, total);
-        if (t < VT) chunk_base[t] = base;
+        uint32_t cb = block_exclusive_scan(nsum, s_warp, total);
         if (t == 0) hdr->nchunks = (uint32_t)min((int64_t)total, max_chunks);
-        for (uint32_t k = 0; k < nch; k++)
-            if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)t;
-        // first chunks first: counts per position in the list, scanned, then scattered
-        for (uint32_t k = 0; k < nch; k++) atomicAdd(&hist[min(k, 255u)], 1u);
+#pragma unroll
+        for (int k = 0; k < TSCAN_ITEMS; k++) {
+            const int i = t * TSCAN_ITEMS + k;
+            const uint32_t nch = ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
+            if (i < VT) chunk_base[i] = cb;
+            for (uint32_t j = 0; j < nch; j++) {
+                if (cb + j < max_chunks) chunk_tile[cb + j] = (uint32_t)i;
+                atomicAdd(&hist[min(j, 255u)], 1u);  // first chunks first: counts per list position
+            }
+            cb += nch;
+        }
         __syncthreads();
         const uint32_t hv = t < 256 ? hist[t] : 0u;
         uint32_t dummy;
         const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
         if (t < 256) hist[t] = hb;
         __syncthreads();
-        for (uint32_t k = 0; k < nch; k++) {
-            const uint32_t pos = atomicAdd(&hist[min(k, 255u)], 1u);
-            if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
+        cb = 0;
+#pragma unroll
+        for (int k = 0; k < TSCAN_ITEMS; k++) {
+            const int i = t * TSCAN_ITEMS + k;
+            const uint32_t nch = ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
+            const uint32_t base = i < VT ? chunk_base[i] : 0u;
+            for (uint32_t j = 0; j < nch; j++) {
+                const uint32_t pos = atomicAdd(&hist[min(j, 255u)], 1u);
+                if (pos < max_chunks && base + j < max_chunks) chunk_order[pos] = base + j;
+            }
         }
     } else {  // longest list first: bucket by length / 8, descending
 #pragma unroll

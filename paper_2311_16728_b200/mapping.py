@@ -219,6 +219,30 @@ class MappingEngine:
         self.gt0.copy_(g.to(self.device, non_blocking=True).view_as(self.gt0))
         self.build_pyramids()
 
+    def add_keyframe(self, cam, gt):
+        """A new keyframe (keyframes reach photorealistic mapping one at a time):
+        its level-0 camera and [3, H, W] target join the batch this engine maps; parameters and
+        optimiser state carry on; the pyramids, losses and level workspaces are rebuilt, and
+        captured graphs (which refer to the old buffers) are dropped."""
+        g = torch.as_tensor(np.asarray(gt, np.float32) if not torch.is_tensor(gt) else gt).to(self.device)
+        H, W = self.cams0[0].height, self.cams0[0].width
+        if (cam.height, cam.width) != (H, W) or tuple(g.shape) != (3, H, W):
+            raise ValueError("add_keyframe: camera / target size differs from the engine's keyframes")
+        self.cams0.append(cam)
+        self.V = len(self.cams0)
+        self.cams = [[level_camera(c, l) for c in self.cams0] for l in range(self.n_levels + 1)]
+        gt0 = torch.empty((self.V, 3, H, W), dtype=torch.float32, device=self.device)
+        gt0[:-1] = self.gt0
+        gt0[-1] = g
+        self.gt0 = gt0
+        self.build_pyramids()
+        self.losses = [PhotometricLoss(self.V, h, w, self.lam, self.device) for (h, w) in self.shapes]
+        self.renderers = [None] * (self.n_levels + 1)
+        self.graph = None
+        self._pipe = None
+        self.calibrate()
+        return self.V - 1
+
     def build_pyramids(self, overlap: bool = False):
         """A0: GP^l(I_gt), l = 1..n, once per keyframe.  overlap: build them on a
         side stream; the first loss that needs them waits for it (iteration), so the pyramid

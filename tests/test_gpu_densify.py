@@ -234,3 +234,25 @@ def test_mapping_engine_densify_with_row_sharded_optimizer(tmp_path):
         assert np.isfinite([x.item() for x in eng.step()]).all()
     finally:
         dist.destroy_process_group()
+
+
+def test_mapping_engine_add_keyframe_keeps_state():
+    """Keyframes arrive one at a time: add_keyframe grows the batch; parameters
+    and Adam state carry on; an iteration then renders and optimises both views."""
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 2)
+    params = pack_params(scene)
+    r = Renderer(scene.n, 0, 2, cams[0].width, cams[0].height, 1 << 16)
+    gts = r.forward(params, cams)[0].clone()
+    eng = MappingEngine(perturb(scene, 4), cams[:1], gts[:1], n_levels=1)
+    for _ in range(3):
+        eng.step()
+    p_before = eng.params.clone()
+    m_before = eng.adam.m.clone()
+    k = eng.add_keyframe(cams[1], gts[1])
+    assert k == 1 and eng.V == 2 and eng.gt0.shape[0] == 2
+    assert torch.equal(eng.params, p_before) and torch.equal(eng.adam.m, m_before)
+    losses = eng.step()
+    assert all(l.shape[0] == 2 for l in losses) and np.isfinite([l.cpu().numpy() for l in losses]).all()
+    with pytest.raises(ValueError):
+        eng.add_keyframe(make_cameras("tum", 1)[0], torch.zeros(3, 480, 640))

@@ -132,3 +132,36 @@ def test_pyramid_parity_full_size(H, W):
     ref = orc.pyramid(img[0], 2)
     for l in range(3):
         np.testing.assert_allclose(lv[l][0].cpu().numpy(), ref[l], atol=1e-6, rtol=0)
+
+
+@pytest.mark.parametrize("cfg,views,level,cap_per_tile", [("replica", 1, 0, None), ("euroc", 16, 1, 260),
+                                                           ("euroc", 16, 0, 260)])
+def test_chunked_path_many_tiles(cfg, views, level, cap_per_tile):
+    """The chunk-parallel raster path with more than 1024 (view, tile) lists -- the one-CTA tile
+    scan (<= 8192 lists: Replica level 0, 3225; EuRoC 16 views level 1, 5760) and the separate
+    chunk index (22560 lists: EuRoC 16 views level 0) -- against the oracle on sampled pixels,
+    forward and backward (use_chunked: capacity >= 200 pairs per list)."""
+    from bench import use_chunked
+    scene = make_scene(cfg)
+    cams = [orc.level_camera(c, level) for c in make_cameras(cfg, views)]
+    keys, vals, ranges, tt = orc.bin_pairs(scene, cams)
+    H, W = cams[0].height, cams[0].width
+    VT = views * ((W + 15) // 16) * ((H + 15) // 16)
+    cap = int(tt.sum()) + 4096 if cap_per_tile is None else max(int(tt.sum()) + 4096, cap_per_tile * VT)
+    assert VT > 1024 and use_chunked(VT, cap)
+    r, params, D = _renderer(scene, cams, cap)
+    rgb, T = r.forward(params, cams)
+    st, flags, P = r.ws.status()
+    assert st == L.GS_OK and P == keys.size
+    pix = _sample_pixels(views, H, W, 4096, 5)
+    ref = orc.render(scene, cams, "recipe", pixels=pix)
+    _check_colour(rgb.cpu().numpy()[pix[:, 0], :, pix[:, 1], pix[:, 2]], T.cpu().numpy()[pix[:, 0], pix[:, 1], pix[:, 2]],
+                  ref)
+    gp = np.random.default_rng(6).normal(size=(pix.shape[0], 3)).astype(np.float32)
+    G = np.zeros((views, 3, H, W), np.float32)
+    G[pix[:, 0], :, pix[:, 1], pix[:, 2]] = gp
+    grads = torch.zeros_like(params)
+    r.backward(params, cams, torch.from_numpy(G).cuda(), grads)
+    got = unpack(grads, scene.n, D)
+    gref = orc.backward(scene, cams, gp, "recipe", pixels=pix, mag=True)
+    _check_grads(got, gref, gref["flagged"], f"chunked_{cfg}_v{views}_l{level}")

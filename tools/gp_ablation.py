@@ -1,11 +1,24 @@
-"""Gaussian-pyramid ablation direction check (Table 3; Eq. 5).
+"""the Table 3 ablation on a synthetic incremental-mapping run,
+with gradient densify / prune (f1) and geometry-based densification (Geo, f2) on, for the
+paper's rows: (1) w/o Geo, n = 2; (2) w/ Geo, w/o GP; (3) w/o Geo, w/o GP; (4) w/ Geo, n = 1;
+(5) w/ Geo, n = 3; default w/ Geo, n = 2.
 
-For n in {0, 1, 2, 3} pyramid levels above the full resolution, optimise the same perturbed
-synthetic map against the same keyframe with the Eq. 5 schedule (level = gp_level(i, n, T / (n+1)),
-SPEC.md:443-451) for T iterations, then report the level-0 PSNR against the target and the device
-time of the T iterations.  Writes profiles/<tag>_gp_ablation.{json,md}.
+Setup (all synthetic, seeded): the target map is the config's scene; `keyframes` views of it are
+the keyframe images (renders of the target map by this path).  Mapping starts from the sparse
+map the geometry thread would hand over ("the geometry mapping component only
+establishes sparse hyper primitives"): a random `sparse` fraction of the target's Gaussians,
+perturbed.  Keypoints of a keyframe (monocular) are the pixels of target
+Gaussians visible in it; `active_frac` of them are active (observed map points with their true
+depth), the rest are inactive -- Geo back-projects those at the inverse-distance depth of their
+4 nearest active neighbours (mono, R32), i.e. at inaccurate positions, the case the paper
+credits GP with fixing.  Keyframes arrive one at a time; after each arrival (Geo: its temporary
+primitives are added) the engine runs `iters` iterations over all keyframes so far, with the
+Eq. 5 schedule restarted for the new keyframe (level = gp_level(i, n, iters / (n + 1))), and
+densify / prune every `densify_every` iterations.  Reported per row: level-0 PSNR over all
+keyframes, model size (Gaussians, MB), render FPS of one level-0 view (graph replay), device ms
+of the mapping iterations.  Writes profiles/<tag>_gp_ablation.{json,md}.
 
-    python tools/gp_ablation.py [--config tum] [--iters 600] [--tag r01]
+    python tools/gp_ablation.py [--config tum] [--keyframes 6] [--iters 150] [--tag r02]
 """
 import argparse
 import json
@@ -16,54 +29,132 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+ROWS = [("(1)", False, 2), ("(2)", True, 0), ("(3)", False, 0), ("(4)", True, 1), ("(5)", True, 3),
+        ("default", True, 2)]
+
+
+def keypoints(scene, cam, n_kp, active_frac, seed):
+    """Keypoint pixels = projections of target Gaussians in view (test input construction)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    P = scene.means.astype(np.float64)
+    pc = P @ cam.R.astype(np.float64).T + cam.t.astype(np.float64)
+    z = pc[:, 2]
+    ok = z > 0.3
+    u = np.where(ok, cam.fx * pc[:, 0] / np.maximum(z, 1e-9) + cam.cx, -1)
+    v = np.where(ok, cam.fy * pc[:, 1] / np.maximum(z, 1e-9) + cam.cy, -1)
+    ok &= (u >= 0) & (u <= cam.width - 1) & (v >= 0) & (v <= cam.height - 1)
+    idx = np.nonzero(ok)[0]
+    pick = rng.choice(idx, size=min(n_kp, idx.size), replace=False)
+    uv = np.stack([u[pick], v[pick]], 1).astype(np.float32)
+    active = (rng.uniform(size=pick.size) < active_frac).astype(np.int32)
+    kd = np.where(active == 1, z[pick], 0.0).astype(np.float32)
+    return uv, active, kd
+
 
 def main():
+    import numpy as np
     import torch
     from paper_2311_16728_b200.build import build
-    from paper_2311_16728_b200.core import Renderer, pack_params
+    from paper_2311_16728_b200.core import DensifyConfig, Renderer, pack_params
     from paper_2311_16728_b200.mapping import MappingEngine, gp_level
     from synth import make_cameras, make_scene, perturb
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="tum")
-    ap.add_argument("--iters", type=int, default=600)
-    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--keyframes", type=int, default=6)
+    ap.add_argument("--iters", type=int, default=150, help="iterations after each keyframe arrival")
+    ap.add_argument("--sparse", type=float, default=0.15)
+    ap.add_argument("--active-frac", type=float, default=0.3)
+    ap.add_argument("--keypoints", type=int, default=3000)
+    ap.add_argument("--densify-every", type=int, default=50)
+    ap.add_argument("--tag", default="r02")
     args = ap.parse_args()
     build()
-    scene = make_scene(args.config)
-    cams = make_cameras(args.config, 1)
-    p0 = pack_params(scene)
-    r = Renderer(scene.n, 3, 1, cams[0].width, cams[0].height, 1 << 22)
-    gt = r.forward(p0, cams)[0].clone()
+    target = make_scene(args.config)
+    cams = make_cameras(args.config, args.keyframes, seed=77)
+    H, W = cams[0].height, cams[0].width
+    r = Renderer(target.n, target.sh_degree, len(cams), W, H, 8 << 20)
+    gts = r.forward(pack_params(target), cams)[0].clone()
     del r
-    start = perturb(scene, 7)
+    rng = np.random.default_rng(3)
+    sparse = perturb(target.subset(np.sort(rng.choice(target.n, int(args.sparse * target.n), replace=False))), 7)
+    kps = [keypoints(target, c, args.keypoints, args.active_frac, 100 + k) for k, c in enumerate(cams)]
     rows = []
-    for n in (0, 1, 2, 3):
-        eng = MappingEngine(start, cams, gt, n_levels=n)
-        per = max(1, args.iters // (n + 1))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(args.iters):
-            eng.iteration(gp_level(i, n, per))
-        e1.record()
-        torch.cuda.synchronize()
+    for name, geo, n in ROWS:
+        dcfg = DensifyConfig(grad_threshold=2e-4, scene_extent=2.5)
+        eng = None
+        dev_ms, added = 0.0, 0
+        seed = 0
+        for k in range(len(cams)):
+            # keyframe k arrives: the engine maps keyframes 0..k (parameters, Adam state carry on)
+            if eng is None:
+                eng = MappingEngine(sparse, cams[:1], gts[:1], n_levels=n, densify_cfg=dcfg)
+            else:
+                eng.add_keyframe(cams[k], gts[k])
+            if geo:
+                uv, act, kd = kps[k]
+                added += eng.add_keyframe_features(k, uv, act, kd, None, gts[k], mode=0)
+            per = max(1, args.iters // (n + 1))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for i in range(args.iters):
+                eng.build_pyramids() if i == 0 else None
+                eng.iteration(gp_level(i, n, per))
+                if (i + 1) % args.densify_every == 0 and i + 1 < args.iters:
+                    e1.record()
+                    torch.cuda.synchronize()
+                    dev_ms += e0.elapsed_time(e1)
+                    seed += 1
+                    eng.densify_and_prune(seed)
+                    torch.cuda.synchronize()
+                    e0.record()
+            e1.record()
+            torch.cuda.synchronize()
+            dev_ms += e0.elapsed_time(e1)
         img = eng.render(0)[0]
-        mse = float(((img - gt) ** 2).mean().item())
+        mse = float(((img - gts) ** 2).mean().item())
         psnr = 10.0 * math.log10(1.0 / max(mse, 1e-12))
-        loss0 = float(eng.losses[0](img, gt, grad=False)[0][0].item())
-        rows.append({"n_levels_above_0": n, "iterations": args.iters, "iters_per_level": per,
-                     "device_ms": e0.elapsed_time(e1), "psnr_level0": psnr, "loss_level0": loss0})
-        print(json.dumps(rows[-1]), flush=True)
-    out = {"config": args.config, "n_gaussians": scene.n, "schedule": "Eq. 5: level = max(0, n - i // per)",
-           "target": "render of the unperturbed synthetic map (perturbed start, seed 7)", "runs": rows}
+        # render FPS of one level-0 view (CUDA-graph replay of A1-A6)
+        one = Renderer(eng.n, eng.D, 1, W, H, max(eng.renderers[0].ws.capacity, 1 << 16))
+        one.forward(eng.params, cams[:1])
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            one.forward(eng.params, cams[:1])
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(g):
+            one.forward(eng.params, cams[:1])
+        for _ in range(3):
+            g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(50):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        fps = 1000.0 / (a.elapsed_time(b) / 50)
+        row = {"row": name, "geo": geo, "gp_levels_above_0": n, "psnr_level0": psnr, "gaussians": eng.n,
+               "model_mb": eng.n * eng.params.shape[0] * 4 / 1e6, "render_fps": fps, "mapping_device_ms": dev_ms,
+               "geo_added": added}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    out = {"config": args.config, "keyframes": args.keyframes, "iters_per_keyframe": args.iters,
+           "sparse_start": f"{args.sparse:.0%} of the {target.n} target Gaussians, perturbed",
+           "keypoints_per_keyframe": args.keypoints, "active_frac": args.active_frac,
+           "densify_every": args.densify_every, "geo_mode": "mono (R32)", "rows": rows}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", f"{args.tag}_gp_ablation.json"), "w"), indent=1)
-    lines = [f"# {args.tag}: Gaussian-pyramid ablation ({args.config}, {scene.n} Gaussians, {args.iters} iterations)",
-             "", "| levels above 0 (n) | iters/level | device ms | PSNR L0 (dB) | loss L0 |", "|---|---|---|---|---|"]
+    lines = [f"# {args.tag}: Table 3 ablation, synthetic ({args.config}, {args.keyframes} keyframes x {args.iters} "
+             f"iterations, sparse start {args.sparse:.0%}, densify/prune every {args.densify_every}, mono Geo)", "",
+             "| row | Geo | GP (n) | PSNR L0 (dB) | Gaussians | MB | render FPS | mapping ms | Geo added |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for x in rows:
-        lines.append(f"| {x['n_levels_above_0']} | {x['iters_per_level']} | {x['device_ms']:.1f} | "
-                     f"{x['psnr_level0']:.2f} | {x['loss_level0']:.5f} |")
+        lines.append(f"| {x['row']} | {'w/' if x['geo'] else 'w/o'} | {x['gp_levels_above_0'] or 'w/o'} | "
+                     f"{x['psnr_level0']:.2f} | {x['gaussians']} | {x['model_mb']:.1f} | {x['render_fps']:.0f} | "
+                     f"{x['mapping_device_ms']:.0f} | {x['geo_added']} |")
     open(os.path.join(ROOT, "profiles", f"{args.tag}_gp_ablation.md"), "w").write("\n".join(lines) + "\n")
 
 
