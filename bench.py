@@ -238,7 +238,7 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU arm
 def use_chunked(view_tiles: int, cap: int) -> bool:
     """Mirror of gs_internal.cuh use_chunked: the chunk-parallel raster path."""
-    return view_tiles < 1000 or (view_tiles < 32768 and cap >= 200 * view_tiles)
+    return view_tiles < 1000
 FUSED_SCHEDULE_TILES = 8192  # views x tiles up to this: one-CTA tile scan + schedule (raster.cu)
 
 

@@ -52,17 +52,14 @@ struct WsHeader {
 // list is replayed by its own CTAs from state the forward recorded (raster.cu).
 constexpr int CHUNK = 64;              // list entries per chunk of the chunked raster path
 constexpr int TILE_PIX = 256;          // pixels per 16x16 tile (per-chunk record stride)
-// The chunked path wins where tile lists are long or tiles few (the tile-serial backward then
-// has a long tail: one CTA's list walk bounds the kernel); it loses ~1 % on short lists (TUM
-// level 0, ~120 pairs per tile).  Measured (graph replay, round 2): Replica 1.728 -> 1.655 ms,
-// EuRoC 16 views 7.47 -> 5.79 ms.  The per-(chunk, pixel) records cost 4 KB per chunk, so very
-// large view batches (the 64-view stress batch at level 0) keep the tile path.
-constexpr int CHUNK_MAX_TILES = 1000;        // V * tiles below this: always chunked
-constexpr int CHUNK_MAX_TILES_LONG = 32768;  // below this: chunked when lists are long
-constexpr int CHUNK_LONG_PAIRS = 200;        // "long": pair capacity >= this per (view, tile)
-__host__ __device__ inline bool use_chunked(int64_t view_tiles, int64_t cap) {
-    return view_tiles < CHUNK_MAX_TILES || (view_tiles < CHUNK_MAX_TILES_LONG && cap >= CHUNK_LONG_PAIRS * view_tiles);
-}
+// Chunk-parallel raster (raster.cu) below CHUNK_MAX_TILES (view, tile) lists: the coarse GP
+// levels, where few tiles with long lists would leave the tile-serial kernels with a long tail.
+// Measured (graph replay, round 2): 600 -> 1000 takes Replica level 1 (836 lists) onto it,
+// 1.787 -> 1.728 ms per step; chunking larger levels (Replica level 0, EuRoC's 16-view levels)
+// is slower (1.837 vs 1.764 ms, 7.90 vs 7.25 ms): there the tile kernels fill the GPU and the
+// chunk records cost more than the tail.
+constexpr int CHUNK_MAX_TILES = 1000;
+__host__ __device__ inline bool use_chunked(int64_t view_tiles, int64_t /*cap*/) { return view_tiles < CHUNK_MAX_TILES; }
 
 // Byte offsets of every buffer inside a render workspace (pure function of n, V, W, H, cap).
 struct Layout {

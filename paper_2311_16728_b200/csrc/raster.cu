@@ -840,7 +840,8 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
     const bool ok = (int64_t)P <= cap;  // overflow: nothing is binned, nothing to schedule
     if (t < 256) hist[t] = 0;
     __syncthreads();
-    if (chunked) {  // every thread its TSCAN_ITEMS tiles (c[] holds their list lengths)
+    if (chunked) {
+        // chunk bases in tile order from the contiguous per-thread items (c[] = list lengths) ...
         uint32_t nsum = 0;
 #pragma unroll
         for (int k = 0; k < TSCAN_ITEMS; k++) nsum += ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
@@ -850,13 +851,19 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
 #pragma unroll
         for (int k = 0; k < TSCAN_ITEMS; k++) {
             const int i = t * TSCAN_ITEMS + k;
-            const uint32_t nch = ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
             if (i < VT) chunk_base[i] = cb;
+            cb += ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
+        }
+        __syncthreads();
+        // ... then the per-chunk loops with tiles strided over the threads (tile t = thread t for
+        // up to 1024 lists: the loops over a tile's chunks run in parallel)
+        for (int i = t; i < VT; i += 1024) {
+            const uint32_t nch = ok ? (counts[(size_t)i * CNT_STRIDE] + CHUNK - 1) / CHUNK : 0u;
+            const uint32_t base = chunk_base[i];
             for (uint32_t j = 0; j < nch; j++) {
-                if (cb + j < max_chunks) chunk_tile[cb + j] = (uint32_t)i;
+                if (base + j < max_chunks) chunk_tile[base + j] = (uint32_t)i;
                 atomicAdd(&hist[min(j, 255u)], 1u);  // first chunks first: counts per list position
             }
-            cb += nch;
         }
         __syncthreads();
         const uint32_t hv = t < 256 ? hist[t] : 0u;
@@ -864,12 +871,9 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
         const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
         if (t < 256) hist[t] = hb;
         __syncthreads();
-        cb = 0;
-#pragma unroll
-        for (int k = 0; k < TSCAN_ITEMS; k++) {
-            const int i = t * TSCAN_ITEMS + k;
-            const uint32_t nch = ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
-            const uint32_t base = i < VT ? chunk_base[i] : 0u;
+        for (int i = t; i < VT; i += 1024) {
+            const uint32_t nch = ok ? (counts[(size_t)i * CNT_STRIDE] + CHUNK - 1) / CHUNK : 0u;
+            const uint32_t base = chunk_base[i];
             for (uint32_t j = 0; j < nch; j++) {
                 const uint32_t pos = atomicAdd(&hist[min(j, 255u)], 1u);
                 if (pos < max_chunks && base + j < max_chunks) chunk_order[pos] = base + j;

@@ -134,21 +134,18 @@ def test_pyramid_parity_full_size(H, W):
         np.testing.assert_allclose(lv[l][0].cpu().numpy(), ref[l], atol=1e-6, rtol=0)
 
 
-@pytest.mark.parametrize("cfg,views,level,cap_per_tile", [("replica", 1, 0, None), ("euroc", 16, 1, 260),
-                                                           ("euroc", 16, 0, 260)])
-def test_chunked_path_many_tiles(cfg, views, level, cap_per_tile):
-    """The chunk-parallel raster path with more than 1024 (view, tile) lists -- the one-CTA tile
-    scan (<= 8192 lists: Replica level 0, 3225; EuRoC 16 views level 1, 5760) and the separate
-    chunk index (22560 lists: EuRoC 16 views level 0) -- against the oracle on sampled pixels,
-    forward and backward (use_chunked: capacity >= 200 pairs per list)."""
-    from bench import use_chunked
+@pytest.mark.parametrize("cfg,views,level", [("replica", 1, 0), ("euroc", 16, 1), ("euroc", 16, 0)])
+def test_raster_parity_many_lists(cfg, views, level):
+    """More than 1024 (view, tile) lists -- Replica level 0 (3225), EuRoC 16 views level 1 (5760,
+    the one-CTA tile scan) and level 0 (22560, the decoupled look-back scan + tile order) --
+    against the oracle on sampled pixels, forward and backward."""
     scene = make_scene(cfg)
     cams = [orc.level_camera(c, level) for c in make_cameras(cfg, views)]
     keys, vals, ranges, tt = orc.bin_pairs(scene, cams)
     H, W = cams[0].height, cams[0].width
     VT = views * ((W + 15) // 16) * ((H + 15) // 16)
-    cap = int(tt.sum()) + 4096 if cap_per_tile is None else max(int(tt.sum()) + 4096, cap_per_tile * VT)
-    assert VT > 1024 and use_chunked(VT, cap)
+    cap = int(tt.sum()) + 4096
+    assert VT > 1024
     r, params, D = _renderer(scene, cams, cap)
     rgb, T = r.forward(params, cams)
     st, flags, P = r.ws.status()
@@ -164,4 +161,4 @@ def test_chunked_path_many_tiles(cfg, views, level, cap_per_tile):
     r.backward(params, cams, torch.from_numpy(G).cuda(), grads)
     got = unpack(grads, scene.n, D)
     gref = orc.backward(scene, cams, gp, "recipe", pixels=pix, mag=True)
-    _check_grads(got, gref, gref["flagged"], f"chunked_{cfg}_v{views}_l{level}")
+    _check_grads(got, gref, gref["flagged"], f"manylists_{cfg}_v{views}_l{level}")
