@@ -102,8 +102,11 @@ gs_status gs_workspace_size(int64_t n, int32_t n_views, int32_t width, int32_t h
 gs_status gs_preprocess(const gs_params *params, const gs_camera *cams, int32_t n_views, void *ws,
                         size_t ws_bytes, gs_stream_t stream);
 
-/* A3-A6: key duplication (key = (view*tiles + tile) << 32 | float_bits(depth), value =
-   Gaussian index), stable LSD radix sort, tile ranges and per-tile front-to-back alpha
+/* A3-A6: the pairs of every (view, tile) in the order of a stable sort by key = (view*tiles +
+   tile) << 32 | float_bits(depth), value = Gaussian index (SPEC.md:348 (2)-(3)) -- by default
+   tile buckets filled by a scatter and each sorted by (depth, id) (bin.cu); gs_set_binning(1)
+   selects key duplication + a stable onesweep LSD radix sort; both give the same pairs bit for
+   bit -- tile ranges, and per-tile front-to-back alpha
    compositing of Eq. 3: alpha = min(0.99, sigma e^power),
    power cut at Mahalanobis^2 > 9 (R9), skip alpha < 1/255, stop when T (1 - alpha) < 1e-4
    (R7, R8).  Requires gs_preprocess on the same params/cams/workspace first.

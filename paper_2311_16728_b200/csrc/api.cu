@@ -64,7 +64,7 @@ Layout make_layout(int64_t n, int V, int W, int H, int64_t cap) {
     L.tile_start = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.tile_cursor = take((size_t)V * L.tiles * CNT_STRIDE * sizeof(uint32_t));
     L.bin_big = take((size_t)2 * L.cap * sizeof(uint64_t));
-    L.big_tiles = take((size_t)V * L.tiles * sizeof(uint32_t));
+    L.big_tiles = take(((size_t)V * L.tiles + (size_t)L.cap / 4096 + 1) * sizeof(uint2));  // (tile, window) items
     L.tile_order = take((size_t)V * L.tiles * sizeof(uint32_t));
     L.prec = take((size_t)3 * L.cap * sizeof(float4));
     L.max_chunks = use_chunked((int64_t)V * L.tiles, L.cap) ? L.cap / CHUNK + (int64_t)V * L.tiles : 0;

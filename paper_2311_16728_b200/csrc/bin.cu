@@ -11,8 +11,8 @@
 //      two -- (depth, id) is unique, so the order is exactly the stable order of the global
 //      sort -- and the sorted values, the full keys and the range are written.  Buckets of up
 //      to 256 pairs are sorted by a group of two warps (k_tile_sort_small), longer ones are
-//      queued for k_tile_sort_big (a CTA of 16 warps, up to 4096 pairs; beyond that the same
-//      network in global memory -- correct, slower, only for extreme tile lists).  Keys live
+//      queued for k_tile_sort_big (a CTA of 16 warps, up to 4096 pairs; a longer list is sorted
+//      as 4096-pair windows by separate CTAs, then merged by the CTA that finishes last).  Keys live
 //      in registers; short exchange distances use shuffles, long ones shared memory.  The
 //      sorted pairs' 48-byte raster records are gathered in the same pass (raster.cu).
 // Compared with the global LSD sort this reads/writes each pair ~3 times instead of
@@ -236,59 +236,6 @@ __device__ __forceinline__ void group_sort(const uint64_t *__restrict__ tmp, uin
     }
 }
 
-// A bucket longer than one window (LP = 32 E W keys): the same network on the padded bucket in
-// global scratch g (its own region of the overflow buffer): every LP-window sorted in registers
-// / shared memory, then each merge step k > LP as its global stages j >= LP followed by one
-// register / shared-memory pass per window for j < LP.
-template <int E, int W>
-__device__ void long_sort(const uint64_t *__restrict__ tmp, uint32_t start, uint32_t len, uint64_t hi,
-                          uint64_t *__restrict__ keys, uint32_t *__restrict__ vals, uint64_t *sk, uint64_t *g,
-                          int gt_idx, const RecSrc &rs) {
-    constexpr int LP = 32 * E * W, NTH = 32 * W;
-    const int lane = gt_idx & 31;
-    const int gw = (gt_idx >> 5) * 32 * E;
-    int lp = LP;
-    while (lp < (int)len) lp <<= 1;
-    uint64_t x[E];
-    for (int base = 0; base < lp; base += LP) {
-#pragma unroll
-        for (int e = 0; e < E; e++) {
-            const uint32_t i = base + gw + e * 32 + lane;
-            x[e] = i < len ? tmp[start + i] : ~0ull;
-        }
-        sort_window<E, W>(x, sk, gt_idx, 1, base);
-#pragma unroll
-        for (int e = 0; e < E; e++) g[base + gw + e * 32 + lane] = x[e];
-    }
-    __threadfence_block();
-    __syncthreads();
-    for (int k = 2 * LP; k <= lp; k <<= 1) {
-        for (int j = k >> 1; j >= LP; j >>= 1) {
-            for (int q = gt_idx; q < lp / 2; q += NTH) {
-                const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
-                const int p = i + j;
-                const uint64_t a = g[i], c = g[p];
-                if ((a > c) == ((i & k) == 0)) {
-                    g[i] = c;
-                    g[p] = a;
-                }
-            }
-            __threadfence_block();
-            __syncthreads();
-        }
-        for (int base = 0; base < lp; base += LP) {
-#pragma unroll
-            for (int e = 0; e < E; e++) x[e] = g[base + gw + e * 32 + lane];
-            merge_window<E, W>(x, sk, gt_idx, 1, base, k);
-#pragma unroll
-            for (int e = 0; e < E; e++) g[base + gw + e * 32 + lane] = x[e];
-        }
-        __threadfence_block();
-        __syncthreads();
-    }
-    for (int i = gt_idx; i < (int)len; i += NTH) emit_pair(g[i], start + i, hi, keys, vals, rs);
-}
-
 constexpr int SG_WARPS = 2;   // warps of the small-bucket CTA (<= 256 pairs)
 constexpr int BG_WARPS = 16;   // warps of the long-bucket CTA (<= 4096 pairs)
 constexpr int BG_MAX = 4096;    // longest bucket sorted in one register / shared-memory window
@@ -299,7 +246,7 @@ constexpr int BG_MAX = 4096;    // longest bucket sorted in one register / share
 __global__ void __launch_bounds__(SG_WARPS * 32) k_tile_sort_small(
     const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, int64_t cap,
     const uint64_t *__restrict__ tmp, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
-    uint2 *__restrict__ ranges, uint32_t *__restrict__ big_tiles, WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
+    uint2 *__restrict__ ranges, uint2 *__restrict__ big_items, WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ uint64_t sk[256];
@@ -315,22 +262,59 @@ __global__ void __launch_bounds__(SG_WARPS * 32) k_tile_sort_small(
     if (len <= 64) group_sort<1, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
     else if (len <= 128) group_sort<2, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
     else if (len <= 256) group_sort<4, SG_WARPS>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-    else if (threadIdx.x == 0) big_tiles[atomicAdd(&hdr->n_big, 1u)] = (uint32_t)gt;
+    else if (threadIdx.x == 0) {  // one work item per BG_MAX-pair window of the bucket
+        const uint32_t nwin = (len + BG_MAX - 1) / BG_MAX;
+        const uint32_t b = atomicAdd(&hdr->n_big, nwin);
+        for (uint32_t w = 0; w < nwin; w++) big_items[b + w] = make_uint2((uint32_t)gt, w);
+    }
 }
 
-// Pass 2: one CTA of 16 warps per queued bucket (grid-stride): up to 4096 pairs in registers and
-// shared memory, longer buckets with long_sort (4096-pair windows + global merge stages).
+// Merge of the sorted runs [0, r), [r, 2r), ... of src (length len) into dst, pairwise, by the
+// whole CTA: each thread takes a contiguous slice of the merged output of a pair and finds where
+// it starts in the two runs by binary search on the diagonal (merge path; keys are unique, so
+// the split is exact), then merges its slice sequentially.
+__device__ void merge_pairs(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst, uint32_t len, uint32_t r,
+                            int tid, int nth) {
+    for (uint32_t lo = 0; lo < len; lo += 2 * r) {
+        const uint32_t la = min(r, len - lo), lb = min(r, len - lo - la);
+        const uint64_t *a = src + lo, *b = a + la;
+        const uint32_t tot = la + lb, per = (tot + nth - 1) / nth;
+        const uint32_t d0 = min(tot, (uint32_t)tid * per), d1 = min(tot, d0 + per);
+        if (d0 < d1) {
+            // smallest i with a[i] > b[d0 - i - 1] (i elements of a precede output d0)
+            uint32_t ilo = d0 > lb ? d0 - lb : 0u, ihi = min(d0, la);
+            while (ilo < ihi) {
+                const uint32_t i = (ilo + ihi) / 2;
+                if (a[i] < b[d0 - i - 1]) ilo = i + 1; else ihi = i;
+            }
+            uint32_t i = ilo, j = d0 - ilo;
+            for (uint32_t d = d0; d < d1; d++) {
+                const bool ta = j >= lb || (i < la && a[i] < b[j]);
+                dst[lo + d] = ta ? a[i++] : b[j++];
+            }
+        }
+    }
+}
+
+// Pass 2: one CTA of 16 warps per queued work item (grid-stride): buckets of up to 4096 pairs
+// are sorted in registers and shared memory and emitted; a longer bucket is one item per
+// 4096-pair window -- each window sorted by its own CTA into the bucket's scratch region (so the
+// windows of one long tile list sort in parallel), and the CTA that finishes the bucket's last
+// window (per-bucket counter: slot 1 of the tile's padded cursor line, zeroed with the cursors)
+// merges the sorted windows pairwise (merge path) and emits the pairs.
 __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(
     const uint32_t *__restrict__ tile_start, const uint32_t *__restrict__ tile_count, const uint64_t *__restrict__ tmp,
-    uint64_t *__restrict__ keys, uint32_t *__restrict__ vals, const uint32_t *__restrict__ big_tiles,
-    uint64_t *__restrict__ big, const WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
+    uint64_t *__restrict__ keys, uint32_t *__restrict__ vals, const uint2 *__restrict__ big_items,
+    uint64_t *__restrict__ big, uint32_t *__restrict__ done, const WsHeader *hdr, RecSrc rs, int64_t n, int tiles) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
-    constexpr int W = BG_WARPS;
+    constexpr int W = BG_WARPS, NTH = 32 * BG_WARPS;
     __shared__ __align__(16) uint64_t sk[BG_MAX];
+    __shared__ bool s_last;
     const uint32_t nb = hdr->n_big;
     for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const uint32_t gt = big_tiles[b];
+        const uint2 item = big_items[b];
+        const uint32_t gt = item.x, w = item.y;
         const uint32_t start = tile_start[gt];
         const uint32_t len = tile_count[(size_t)gt * CNT_STRIDE];
         const uint64_t hi = (uint64_t)gt << 32;
@@ -339,8 +323,44 @@ __global__ void __launch_bounds__(BG_WARPS * 32) k_tile_sort_big(
         else if (len <= 1024) group_sort<2, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
         else if (len <= 2048) group_sort<4, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
         else if (len <= BG_MAX) group_sort<8, W>(tmp, start, len, hi, keys, vals, sk, threadIdx.x, 1, rs);
-        else  // padded copy in this bucket's own region [2 start, 2 start + 2 len) of the overflow buffer
-            long_sort<8, W>(tmp, start, len, hi, keys, vals, sk, big + 2 * (size_t)start, threadIdx.x, rs);
+        else {
+            // window w, sorted into the bucket's scratch region [2 start, 2 start + 2 len): runs
+            // in the first half, the merge ping-pongs with the second
+            uint64_t *A = big + 2 * (size_t)start, *B = A + len;
+            const uint32_t w0 = w * BG_MAX, wlen = min((uint32_t)BG_MAX, len - w0);
+            constexpr int E = 8;
+            const int lane = threadIdx.x & 31, gw = (threadIdx.x >> 5) * 32 * E;
+            uint64_t x[E];
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint32_t g = gw + e * 32 + lane;
+                x[e] = g < wlen ? tmp[start + w0 + g] : ~0ull;
+            }
+            sort_window<E, W>(x, sk, threadIdx.x, 1, 0);
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                const uint32_t g = gw + e * 32 + lane;
+                if (g < wlen) A[w0 + g] = x[e];
+            }
+            __threadfence();
+            __syncthreads();
+            const uint32_t nwin = (len + BG_MAX - 1) / BG_MAX;
+            if (threadIdx.x == 0) s_last = atomicAdd(&done[(size_t)gt * CNT_STRIDE + 1], 1u) == nwin - 1;
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                uint64_t *src = A, *dst = B;
+                for (uint32_t r = BG_MAX; r < len; r *= 2) {
+                    merge_pairs(src, dst, len, r, threadIdx.x, NTH);
+                    __threadfence_block();
+                    __syncthreads();
+                    uint64_t *t = src;
+                    src = dst;
+                    dst = t;
+                }
+                for (uint32_t i = threadIdx.x; i < len; i += NTH) emit_pair(src[i], start + i, hi, keys, vals, rs);
+            }
+        }
         __syncthreads();
     }
 }
@@ -368,7 +388,7 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
     launch_pdl(k_tile_sort_small, (unsigned)VT, SG_WARPS * 32, 0, s,
                at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), L.cap, at<uint64_t>(ws, L.keys1),
                at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.ranges),
-               at<uint32_t>(ws, L.big_tiles), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
+               at<uint2>(ws, L.big_tiles), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
     static int sms = 0;
     if (sms == 0) {
         int dev = 0;
@@ -378,8 +398,9 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
     // 16-warp CTAs: up to 4 resident per SM
     launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT, 4 * sms), BG_WARPS * 32, 0, s,
                at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
-               at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint32_t>(ws, L.big_tiles),
-               at<uint64_t>(ws, L.bin_big), at<WsHeader>(ws, L.hdr), rs, L.n, L.tiles);
+               at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.big_tiles),
+               at<uint64_t>(ws, L.bin_big), at<uint32_t>(ws, L.tile_cursor), at<WsHeader>(ws, L.hdr), rs, L.n,
+               L.tiles);
     return cudaGetLastError();
 }
 

@@ -3,7 +3,7 @@
 // L_v = (1 - lambda) mean|x - y| + lambda (1 - mean SSIM(x, y)) per view, lambda = 0.2
 // (PAPER.md:568).  SSIM per channel with an 11x11 Gaussian window (sigma 1.5), C1 = 0.01^2,
 // C2 = 0.03^2, zero-padded 'same' (R17).  The window is separable, so each
-// 16x16 output tile loads a 26x26 halo of x and y into shared memory and runs a horizontal
+// 32x32 output tile loads a 42x42 halo of x and y into shared memory and runs a horizontal
 // then a vertical 11-tap pass over the five moment maps (x, y, x^2, y^2, xy).  The gradient
 // is the windowed-correlation form: dSSIM/dx_p = (w * A)_p + 2 x_p (w * B)_p + y_p (w * C)_p
 // with A = dS/dmu_x, B = dS/dE[x^2], C = dS/dE[xy] per pixel, so a second kernel applies

@@ -65,33 +65,37 @@ def test_permute_columns_gathers_and_keeps_padding():
 
 
 def test_engine_with_spatial_order_optimises_the_same_map():
+    """The Morton layout changes where Gaussians sit in memory, not what the method computes:
+    renders agree and three optimiser steps (SGD mode: -lr g, no Adam normalisation of
+    last-bit noise) move every Gaussian the same way up to fp32 summation order."""
+    from paper_2311_16728_b200.core import AdamConfig
     scene = make_scene("tum", n=30000)
     cams = make_cameras("tum", 1)
     params = pack_params(scene)
     r = Renderer(scene.n, 3, 1, cams[0].width, cams[0].height, 1 << 20)
     gt = r.forward(params, cams)[0].clone()
     start = perturb(scene, 5)
-    a = MappingEngine(start, cams, gt, n_levels=2, spatial_order=True)
-    b = MappingEngine(start, cams, gt, n_levels=2, spatial_order=False)
+    cfg = AdamConfig(sgd=True)
+    a = MappingEngine(start, cams, gt, n_levels=2, spatial_order=True, adam=cfg)
+    b = MappingEngine(start, cams, gt, n_levels=2, spatial_order=False, adam=cfg)
     order = a.order
     assert torch.equal(a.params[:, :a.n], b.params[:, order])  # the same Gaussians, re-ordered
+    p0 = b.params[:, order].clone()
     ra, _ = a.render(0)
     rb, _ = b.render(0)
     # the index only breaks ties between equal fp32 depths (SPEC.md:348 (3)); this map has ~60
     # tied depth values among its 30000 Gaussians, so the pixels two tied, overlapping Gaussians
     # share may differ -- all others agree to rounding
     d = (ra - rb).abs().amax(dim=1)
-    assert (d > 1e-5).float().mean().item() <= 5e-3 and d.max().item() <= 5e-2
+    assert (d > 1e-5).float().mean().item() <= 5e-4 and d.max().item() <= 5e-2
     for _ in range(3):
         a.build_pyramids()
         b.build_pyramids()
         la = torch.stack(a.step()).cpu().numpy()
         lb = torch.stack(b.step()).cpu().numpy()
-        np.testing.assert_allclose(la, lb, rtol=1e-3)
-    # after three Adam steps the two maps agree up to the atomics' summation order and the tied
-    # pixels; Adam normalises the step, so an element whose gradient is ~0 (or touched by a tie)
-    # can move by up to lr in either direction (as in test_gpu_parity's graph-replay test)
+        np.testing.assert_allclose(la, lb, rtol=1e-5)
     diff = (a.params[:, :a.n] - b.params[:, order]).abs()
-    close = diff <= 1e-5 + 1e-4 * b.params[:, order].abs()
-    assert close.float().mean().item() > 1 - 1e-3
-    assert diff.max().item() <= 2 * 5e-2 * 3
+    moved = (b.params[:, order] - p0).abs()
+    tol = 1e-3 * moved + 4 * torch.finfo(torch.float32).eps * p0.abs() + 1e-9
+    bad = diff > tol
+    assert bad.float().mean().item() <= 1e-4, (int(bad.sum()), float(diff.max()))

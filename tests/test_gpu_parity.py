@@ -479,15 +479,19 @@ def test_adam_step_rows_equals_full_step_on_its_rows():
 
 
 def test_graph_replay_matches_eager_steps():
-    """A captured step (device-resident Adam step counter) replayed gives the same trajectory as
-    eager steps: 1 warm-up + 2 replays == 3 eager steps (up to atomic-order rounding)."""
+    """A captured step (device-resident step counter) replayed gives the same trajectory as eager
+    steps: 1 warm-up + 2 replays == 3 eager steps.  Run with the optimiser in SGD mode, where a
+    step is -lr g (Adam's normalisation would turn the atomics' last-bit noise on ~0 gradients
+    into +-lr moves), so the two trajectories must agree to fp32 summation-order rounding; the
+    Adam counter is checked separately."""
     scene = make_scene("tum", n=40000)
     cams = make_cameras("tum", 1)
     r, params, _ = _renderer(scene, cams)
     gt = r.forward(params, cams)[0].clone()
     start = perturb(scene, 3)
-    a = MappingEngine(start, cams, gt, n_levels=2)
-    b = MappingEngine(start, cams, gt, n_levels=2)
+    cfg = AdamConfig(sgd=True)
+    a = MappingEngine(start, cams, gt, n_levels=2, adam=cfg)
+    b = MappingEngine(start, cams, gt, n_levels=2, adam=cfg)
     for _ in range(3):
         a.build_pyramids()
         a.step()
@@ -496,13 +500,12 @@ def test_graph_replay_matches_eager_steps():
     b.replay()
     torch.cuda.synchronize()
     assert int(b.adam.t_dev.item()) == 9 and a.adam.t == 9
-    # fp32 atomics make the two runs differ in the last bits; Adam normalises the step, so a
-    # Gaussian whose gradient is ~0 can move by up to lr in either direction: allow a tiny
-    # fraction of elements to differ by at most 2 lr per step
+    moved = (a.params - pack_params(start)).abs()
     diff = (b.params - a.params).abs()
-    close = diff <= 1e-5 + 1e-4 * a.params.abs()
-    assert close.float().mean().item() > 1 - 1e-5
-    assert diff.max().item() <= 2 * 5e-2 * 9
+    # per element: within 1e-3 of the element's own movement (+ fp32 resolution of the value)
+    tol = 1e-3 * moved + 4 * torch.finfo(torch.float32).eps * a.params.abs() + 1e-9
+    bad = diff > tol
+    assert bad.float().mean().item() <= 1e-5, (int(bad.sum()), float(diff.max()))
 
 
 def test_step_host_prefetch_matches_plain():
