@@ -424,6 +424,59 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *s
     return s_warp[warp] + incl - v;
 }
 
+// Backward schedule of the chunked path: chunks ordered by their position j in the tile list
+// (first chunks first: most pixels are still active there, so the longest replays start
+// first), positions >= 255 in one class.  Without per-chunk atomics: the tiles sorted by chunk
+// count, descending (q(t): one shared atomic per tile for ties), make "the tiles with more
+// than j chunks" a prefix of that order for every j, so chunk (t, j) goes to
+// P_j + q(t) with P_j = sum_{j' < j} #{tiles with > j' chunks}.  chunk_base[] must be written
+// (and visible to the CTA) before the call; nch(i) = chunks of list i; 1024 threads.
+template <class NCH>
+__device__ __forceinline__ void chunk_order_schedule(NCH nch, int VT, const uint32_t *__restrict__ chunk_base,
+                                                     uint32_t *__restrict__ chunk_order, int64_t max_chunks,
+                                                     uint32_t *s_warp, uint32_t *H /* [258] shared */) {
+    const int t = threadIdx.x;
+    if (t < 258) H[t] = 0;
+    __syncthreads();
+    for (int i = t; i < VT; i += 1024) {
+        const uint32_t c = nch(i);
+        atomicAdd(&H[min(c, 256u)], 1u);
+        if (c > 255) atomicAdd(&H[257], c - 255);  // size of the j >= 255 class
+    }
+    __syncthreads();
+    // S[v] = #tiles with min(nch, 256) > v (suffix sums): thread t holds bin 256 - t
+    uint32_t dummy;
+    const uint32_t hv = t <= 256 ? H[256 - t] : 0u;
+    const uint32_t suf = block_exclusive_scan(hv, s_warp, dummy);  // sum over bins > 256 - t
+    __syncthreads();
+    uint32_t *S = H;  // reuse: S[v] for v = 0..256, class-255 size kept in H[257]
+    const uint32_t big = H[257];
+    __syncthreads();
+    if (t <= 256) S[256 - t] = suf;
+    __syncthreads();
+    // P_j = sum_{j' < j} S[j'] for j = 0..255; class 255 holds the S[255] tiles' chunks >= 255
+    const uint32_t m = t < 255 ? S[t] : (t == 255 ? big : 0u);
+    const uint32_t Pj = block_exclusive_scan(m, s_warp, dummy);
+    __shared__ uint32_t P[256], q_cur[257], c255;
+    if (t < 256) P[t] = Pj;
+    if (t <= 256) q_cur[t] = S[t];  // tiles with more chunks than v come first
+    if (t == 0) c255 = 0;
+    __syncthreads();
+    for (int i = t; i < VT; i += 1024) {
+        const uint32_t c = nch(i), base = chunk_base[i];
+        const uint32_t q = atomicAdd(&q_cur[min(c, 256u)], 1u);  // position in the descending order
+        const uint32_t jmax = min(c, 255u);
+        for (uint32_t j = 0; j < jmax; j++) {
+            const uint32_t pos = P[j] + q;
+            if (pos < max_chunks && base + j < max_chunks) chunk_order[pos] = base + j;
+        }
+        for (uint32_t j = 255; j < c; j++) {
+            const uint32_t pos = P[255] + atomicAdd(&c255, 1u);
+            if (pos < max_chunks && base + j < max_chunks) chunk_order[pos] = base + j;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ ranges, int VT,
                                                       uint32_t *__restrict__ chunk_base,
                                                       uint32_t *__restrict__ chunk_tile,
@@ -432,41 +485,27 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t cnt[256];
+    __shared__ uint32_t H[258];
     const int t = threadIdx.x;
-    const int per = (VT + 1023) / 1024;  // consecutive tiles per thread
+    const int per = (VT + 1023) / 1024;  // consecutive lists per thread for the tile-order scan
     const int i0 = t * per, i1 = min(VT, i0 + per);
-    auto nchunks = [&](int i) { const uint2 r = ranges[i]; return (r.y - r.x + CHUNK - 1) / CHUNK; };
+    auto nch = [&](int i) { const uint2 r = ranges[i]; return (r.y - r.x + CHUNK - 1) / CHUNK; };
     uint32_t nsum = 0;
-    for (int i = i0; i < i1; i++) nsum += nchunks(i);
-    if (t < 256) cnt[t] = 0;
+    for (int i = i0; i < i1; i++) nsum += nch(i);
     uint32_t total;
     uint32_t cb = block_exclusive_scan(nsum, s_warp, total);
     if (t == 0) hdr->nchunks = (uint32_t)min((int64_t)total, max_chunks);
     for (int i = i0; i < i1; i++) {
-        const uint32_t nch = nchunks(i);
         chunk_base[i] = cb;
-        for (uint32_t k = 0; k < nch; k++) {
-            if (cb + k < max_chunks) chunk_tile[cb + k] = (uint32_t)i;
-            atomicAdd(&cnt[min(k, 255u)], 1u);
-        }
-        cb += nch;
+        cb += nch(i);
     }
-    // chunk order for the backward: by position in the tile list, first chunks first (most
-    // pixels are still active there: the longest replays start first)
     __syncthreads();
-    const uint32_t hv = t < 256 ? cnt[t] : 0u;
-    uint32_t dummy;
-    const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
-    if (t < 256) cnt[t] = hb;
-    __syncthreads();
-    for (int i = i0; i < i1; i++) {
-        const uint32_t nch = nchunks(i), base = chunk_base[i];
-        for (uint32_t k = 0; k < nch; k++) {
-            const uint32_t pos = atomicAdd(&cnt[min(k, 255u)], 1u);
-            if (pos < max_chunks && base + k < max_chunks) chunk_order[pos] = base + k;
-        }
+    for (int i = t; i < VT; i += 1024) {
+        const uint32_t c = nch(i), base = chunk_base[i];
+        for (uint32_t k = 0; k < c; k++)
+            if (base + k < max_chunks) chunk_tile[base + k] = (uint32_t)i;
     }
+    chunk_order_schedule(nch, VT, chunk_base, chunk_order, max_chunks, s_warp, H);
 }
 
 // ================================================================ two-pixel packed backward
@@ -819,7 +858,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
     __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t hist[256];
+    __shared__ uint32_t hist[258];
     const int t = threadIdx.x;
     uint32_t c[TSCAN_ITEMS], sum = 0;
 #pragma unroll
@@ -855,30 +894,14 @@ __global__ void __launch_bounds__(1024) k_tile_scan(const uint32_t *__restrict__
             cb += ok ? (c[k] + CHUNK - 1) / CHUNK : 0u;
         }
         __syncthreads();
-        // ... then the per-chunk loops with tiles strided over the threads (tile t = thread t for
-        // up to 1024 lists: the loops over a tile's chunks run in parallel)
+        // ... then chunk -> tile and the backward's chunk order, tiles strided over the threads
+        auto nch = [&](int i) { return ok ? (counts[(size_t)i * CNT_STRIDE] + CHUNK - 1) / CHUNK : 0u; };
         for (int i = t; i < VT; i += 1024) {
-            const uint32_t nch = ok ? (counts[(size_t)i * CNT_STRIDE] + CHUNK - 1) / CHUNK : 0u;
-            const uint32_t base = chunk_base[i];
-            for (uint32_t j = 0; j < nch; j++) {
+            const uint32_t c = nch(i), base = chunk_base[i];
+            for (uint32_t j = 0; j < c; j++)
                 if (base + j < max_chunks) chunk_tile[base + j] = (uint32_t)i;
-                atomicAdd(&hist[min(j, 255u)], 1u);  // first chunks first: counts per list position
-            }
         }
-        __syncthreads();
-        const uint32_t hv = t < 256 ? hist[t] : 0u;
-        uint32_t dummy;
-        const uint32_t hb = block_exclusive_scan(hv, s_warp, dummy);
-        if (t < 256) hist[t] = hb;
-        __syncthreads();
-        for (int i = t; i < VT; i += 1024) {
-            const uint32_t nch = ok ? (counts[(size_t)i * CNT_STRIDE] + CHUNK - 1) / CHUNK : 0u;
-            const uint32_t base = chunk_base[i];
-            for (uint32_t j = 0; j < nch; j++) {
-                const uint32_t pos = atomicAdd(&hist[min(j, 255u)], 1u);
-                if (pos < max_chunks && base + j < max_chunks) chunk_order[pos] = base + j;
-            }
-        }
+        chunk_order_schedule(nch, VT, chunk_base, chunk_order, max_chunks, s_warp, hist);
     } else {  // longest list first: bucket by length / 8, descending
 #pragma unroll
         for (int k = 0; k < TSCAN_ITEMS; k++)

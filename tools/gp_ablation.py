@@ -68,6 +68,8 @@ def main():
     ap.add_argument("--active-frac", type=float, default=0.3)
     ap.add_argument("--keypoints", type=int, default=3000)
     ap.add_argument("--densify-every", type=int, default=50)
+    ap.add_argument("--grad-threshold", type=float, default=2e-5,
+                    help="mean ||dL/dmean2d|| (pixels of the level rendered) above which a Gaussian densifies")
     ap.add_argument("--tag", default="r02")
     args = ap.parse_args()
     build()
@@ -80,9 +82,26 @@ def main():
     rng = np.random.default_rng(3)
     sparse = perturb(target.subset(np.sort(rng.choice(target.n, int(args.sparse * target.n), replace=False))), 7)
     kps = [keypoints(target, c, args.keypoints, args.active_frac, 100 + k) for k, c in enumerate(cams)]
+    rows = run_rows(args, ROWS, cams, gts, sparse, kps, {})
+    # online mapping is time-bound (faster rendering buys more iterations): the
+    # same rows again with each row's iterations scaled so its mapping time matches the row
+    # with the same Geo setting and no GP
+    ref = {r["geo"]: r["mapping_device_ms"] for r in rows if r["gp_levels_above_0"] == 0}
+    scale = {r["row"]: ref[r["geo"]] / r["mapping_device_ms"] for r in rows}
+    rows_t = run_rows(args, ROWS, cams, gts, sparse, kps, scale)
+    write(args, target, rows, rows_t)
+
+
+def run_rows(args, row_defs, cams, gts, sparse, kps, scale):
+    import numpy as np
+    import torch
+    from paper_2311_16728_b200.core import DensifyConfig, Renderer
+    from paper_2311_16728_b200.mapping import MappingEngine, gp_level
+    H, W = cams[0].height, cams[0].width
     rows = []
-    for name, geo, n in ROWS:
-        dcfg = DensifyConfig(grad_threshold=2e-4, scene_extent=2.5)
+    for name, geo, n in row_defs:
+        iters = max(args.densify_every + 1, int(round(args.iters * scale.get(name, 1.0))))
+        dcfg = DensifyConfig(grad_threshold=args.grad_threshold, scene_extent=2.5)
         eng = None
         dev_ms, added = 0.0, 0
         seed = 0
@@ -95,14 +114,14 @@ def main():
             if geo:
                 uv, act, kd = kps[k]
                 added += eng.add_keyframe_features(k, uv, act, kd, None, gts[k], mode=0)
-            per = max(1, args.iters // (n + 1))
+            per = max(1, iters // (n + 1))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
-            for i in range(args.iters):
+            for i in range(iters):
                 eng.build_pyramids() if i == 0 else None
                 eng.iteration(gp_level(i, n, per))
-                if (i + 1) % args.densify_every == 0 and i + 1 < args.iters:
+                if (i + 1) % args.densify_every == 0 and i + 1 < iters:
                     e1.record()
                     torch.cuda.synchronize()
                     dev_ms += e0.elapsed_time(e1)
@@ -136,26 +155,40 @@ def main():
         b.record()
         torch.cuda.synchronize()
         fps = 1000.0 / (a.elapsed_time(b) / 50)
-        row = {"row": name, "geo": geo, "gp_levels_above_0": n, "psnr_level0": psnr, "gaussians": eng.n,
+        row = {"row": name, "geo": geo, "gp_levels_above_0": n, "iters_per_keyframe": iters,
+               "psnr_level0": psnr, "gaussians": eng.n,
                "model_mb": eng.n * eng.params.shape[0] * 4 / 1e6, "render_fps": fps, "mapping_device_ms": dev_ms,
                "geo_added": added}
         rows.append(row)
         print(json.dumps(row), flush=True)
+    return rows
+
+
+def write(args, target, rows, rows_t):
     out = {"config": args.config, "keyframes": args.keyframes, "iters_per_keyframe": args.iters,
            "sparse_start": f"{args.sparse:.0%} of the {target.n} target Gaussians, perturbed",
            "keypoints_per_keyframe": args.keypoints, "active_frac": args.active_frac,
-           "densify_every": args.densify_every, "geo_mode": "mono (R32)", "rows": rows}
+           "densify_every": args.densify_every, "grad_threshold": args.grad_threshold, "geo_mode": "mono (R32)",
+           "rows_equal_iterations": rows,
+           "rows_equal_time": rows_t}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     json.dump(out, open(os.path.join(ROOT, "profiles", f"{args.tag}_gp_ablation.json"), "w"), indent=1)
-    lines = [f"# {args.tag}: Table 3 ablation, synthetic ({args.config}, {args.keyframes} keyframes x {args.iters} "
-             f"iterations, sparse start {args.sparse:.0%}, densify/prune every {args.densify_every}, mono Geo)", "",
-             "| row | Geo | GP (n) | PSNR L0 (dB) | Gaussians | MB | render FPS | mapping ms | Geo added |",
-             "|---|---|---|---|---|---|---|---|---|"]
-    for x in rows:
-        lines.append(f"| {x['row']} | {'w/' if x['geo'] else 'w/o'} | {x['gp_levels_above_0'] or 'w/o'} | "
-                     f"{x['psnr_level0']:.2f} | {x['gaussians']} | {x['model_mb']:.1f} | {x['render_fps']:.0f} | "
-                     f"{x['mapping_device_ms']:.0f} | {x['geo_added']} |")
-    open(os.path.join(ROOT, "profiles", f"{args.tag}_gp_ablation.md"), "w").write("\n".join(lines) + "\n")
+    lines = [f"# {args.tag}: Table 3 ablation, synthetic ({args.config}, {args.keyframes} keyframes, sparse start "
+             f"{args.sparse:.0%}, densify/prune every {args.densify_every} iterations, mono Geo)", ""]
+    for title, rr in ((f"equal iterations ({args.iters} per keyframe)", rows),
+                      ("equal mapping time (iterations scaled to the no-GP row of the same Geo setting)", rows_t)):
+        lines += [f"## {title}", "",
+                  "| row | Geo | GP (n) | iters/keyframe | PSNR L0 (dB) | Gaussians | MB | render FPS | mapping ms |"
+                  " Geo added |", "|---|---|---|---|---|---|---|---|---|---|"]
+        for x in rr:
+            lines.append(f"| {x['row']} | {'w/' if x['geo'] else 'w/o'} | {x['gp_levels_above_0'] or 'w/o'} | "
+                         f"{x['iters_per_keyframe']} | {x['psnr_level0']:.2f} | {x['gaussians']} | {x['model_mb']:.1f} | "
+                         f"{x['render_fps']:.0f} | {x['mapping_device_ms']:.0f} | {x['geo_added']} |")
+        lines.append("")
+    for d in ("profiles", "gpurun_out"):  # gpurun_out: what a GPU-box run brings back
+        os.makedirs(os.path.join(ROOT, d), exist_ok=True)
+        open(os.path.join(ROOT, d, f"{args.tag}_gp_ablation.md"), "w").write("\n".join(lines) + "\n")
+        json.dump(out, open(os.path.join(ROOT, d, f"{args.tag}_gp_ablation.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
