@@ -120,7 +120,8 @@ def test_preprocess_and_binning_bit_exact(cfg, n, views, level, binning):
 
 @pytest.mark.parametrize("n,bits,kind", [(1, 40, "rand"), (4095, 44, "depth"), (4096, 44, "rand"),
                                          (4097, 48, "depth"), (300_001, 44, "depth"), (1_000_003, 64, "rand"),
-                                         (2_000_000, 12, "rand")])
+                                         (2_000_000, 12, "rand"), (3_000_017, 50, "depth"), (5_000_000, 20, "rand"),
+                                         (40_000_003, 50, "depth")])
 def test_radix_sort_stable(n, bits, kind):
     rng = np.random.default_rng(n)
     if bits > 32:

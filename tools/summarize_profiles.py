@@ -1,6 +1,6 @@
 """Summarise gpurun_out ncu artefacts into profiles/ (tracked):
 
-    python tools/summarize_profiles.py <tag> [launches.csv] [report.ncu-rep]
+    python tools/summarize_profiles.py <tag> [launches.csv] [report.ncu-rep] [config]
 
 * <tag>_launches.csv / <tag>_launches.md: per-launch device times of one bench step
   (ncu --metrics gpu__time_duration.sum, cold-cache and serialised: compare shares);
@@ -55,7 +55,7 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throug
         "L2 Hit Rate", "Branch Efficiency", "Avg. Active Threads Per Warp"]
 
 
-def report(tag, rep):
+def report(tag, rep, cfg_name="tum"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     traffic = defaultdict(list)
@@ -100,14 +100,20 @@ def report(tag, rep):
                 f.write(f"\ndram bytes (read + write) per launch: {', '.join(f'{x / 1e6:.2f} MB' for x in t)}\n")
     tj = os.path.join(PROF, "traffic.json")
     data = json.load(open(tj)) if os.path.exists(tj) else {}
-    cfg = data.setdefault("tum", {})
+    cfg = data.setdefault(cfg_name, {})
     for k, v in traffic.items():
         cfg[k.replace("gsk::", "")] = sum(v) / len(v)
-    # the raster backward runs as different kernels per level (packed / chunked): bench.py's
-    # roofline uses the mean over all of its launches in the captured step
-    allb = [x for k, v in traffic.items() if k.replace("gsk::", "").startswith("k_raster_bwd") for x in v]
-    if allb:
-        cfg["k_raster_bwd"] = sum(allb) / len(allb)
+    # bench.py times kernel families (one libgs.so scope each per GP level, gs_profile_kernel):
+    # traffic per scope = all member launches' bytes in the captured step / the scope's count
+    fam = {"k_raster_bwd": (("k_raster_bwd",), "k_raster_bwd"), "k_raster_fwd": (("k_raster_fwd", "k_chunk_index",
+           "k_tile_order"), "k_raster_fwd"), "k_tile_sort": (("k_tile_sort_small", "k_tile_sort_big"),
+           "k_tile_sort_small"), "k_ssim": (("k_ssim_fwd", "k_ssim_bwd", "k_loss_final"), "k_ssim_fwd")}
+    names = {k.replace("gsk::", ""): v for k, v in traffic.items()}
+    for f, (members, anchor) in fam.items():
+        tot = sum(x for k, v in names.items() if k.startswith(members) for x in v)
+        n = sum(len(v) for k, v in names.items() if k.startswith(anchor))
+        if n:
+            cfg[f] = tot / n
     json.dump(data, open(tj, "w"), indent=1)
 
 
@@ -117,4 +123,4 @@ if __name__ == "__main__":
     if len(sys.argv) > 2:
         launches(tag, sys.argv[2])
     if len(sys.argv) > 3:
-        report(tag, sys.argv[3])
+        report(tag, sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "tum")
