@@ -638,7 +638,7 @@ def run_ours(args):
         eng.render(0)
         torch.cuda.synchronize()
         v0 = rw.views()
-        P0 = int(levels_meas[-1]["P"] * len(cams))
+        _, _, P0 = rw.status()  # this render's pairs (the map has trained since levels_meas)
         bits = 32 + max(1, math.ceil(math.log2(max(rw.tiles_x * rw.tiles_y * len(cams), 2))))
         perm = torch.randperm(P0, device=dev)
         k_src, v_src = v0["keys"][:P0][perm].clone(), v0["vals"][:P0][perm].clone()

@@ -396,7 +396,8 @@ cudaError_t launch_bin(const Layout &L, void *ws, cudaStream_t s) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     // 16-warp CTAs: up to 4 resident per SM
-    launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT, 4 * sms), BG_WARPS * 32, 0, s,
+    // one CTA per queued item where possible (items: buckets of <= 4096 pairs, windows of longer ones)
+    launch_pdl(k_tile_sort_big, (unsigned)std::min<int64_t>(VT + L.cap / BG_MAX + 1, 4 * sms), BG_WARPS * 32, 0, s,
                at<uint32_t>(ws, L.tile_start), at<uint32_t>(ws, L.tile_count), at<uint64_t>(ws, L.keys1),
                at<uint64_t>(ws, L.keys0), at<uint32_t>(ws, L.vals0), at<uint2>(ws, L.big_tiles),
                at<uint64_t>(ws, L.bin_big), at<uint32_t>(ws, L.tile_cursor), at<WsHeader>(ws, L.hdr), rs, L.n,
