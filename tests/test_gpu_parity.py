@@ -585,3 +585,45 @@ def test_mapping_engine_reduces_loss():
         last = torch.stack(eng.step()).cpu().numpy()
     eng.check()
     assert last[-1] < 0.7 * first[-1], (first, last)
+
+
+def test_pipelined_step_raises_on_capacity_overflow():
+    """The end-to-end pipelined step reads each level's overflow flag back with its losses
+    (gs_status_async) and raises once a step rendered into an overflowing workspace (the level's
+    pairs exceed its capacity: nothing was binned)."""
+    scene = make_scene("tum", n=20000)   # up to 1200 tiles per Gaussian: huge footprints overflow
+    cams = make_cameras("tum", 1)
+    r, params, _ = _renderer(scene, cams)
+    gt = r.forward(params, cams)[0].clone()
+    eng = MappingEngine(perturb(scene, 3), cams, gt, n_levels=1)
+    gts = [eng.gt0.cpu().pin_memory() for _ in range(2)]
+    outs = [torch.empty((2, 1), dtype=torch.float32).pin_memory() for _ in range(2)]
+    eng.capture_pipelined(gts, outs)
+    for _ in range(3):
+        eng.step_pipelined()
+    eng.pipeline_join()
+    torch.cuda.synchronize()
+    eng.pipeline_check()  # no overflow: nothing raised
+    # make every Gaussian huge: far more pairs than the calibrated capacity
+    with torch.no_grad():
+        eng.params[7:10, :eng.n] += 3.0
+    with pytest.raises(RuntimeError, match="capacity"):
+        for _ in range(4):
+            eng.step_pipelined()
+        eng.pipeline_join()
+        torch.cuda.synchronize()
+        eng.pipeline_check()
+
+
+def test_workspace_release_forgets_forward_state():
+    """gs_workspace_release erases the forward-state token: a backward on the released workspace
+    is StaleRenderState (a new workspace at the same address cannot inherit the old token)."""
+    scene = make_scene("tiny")
+    cams = make_cameras("tiny", 1)
+    r, params, D = _renderer(scene, cams)
+    r.forward(params, cams)
+    L.gs_workspace_release(r.ws.buf)
+    grads = torch.zeros_like(params)
+    with pytest.raises(L.GsError) as e:
+        r.backward(params, cams, torch.zeros((1, 3, 48, 64), device="cuda"), grads)
+    assert e.value.status == L.GS_ERR_STALE_STATE
