@@ -162,3 +162,35 @@ def test_raster_parity_many_lists(cfg, views, level):
     got = unpack(grads, scene.n, D)
     gref = orc.backward(scene, cams, gp, "recipe", pixels=pix, mag=True)
     _check_grads(got, gref, gref["flagged"], f"manylists_{cfg}_v{views}_l{level}")
+
+
+@pytest.mark.parametrize("n,W,H", [(0, 64, 48), (1, 64, 48), (37, 1, 1), (300, 17, 5), (500, 33, 129)])
+def test_degenerate_sizes(n, W, H):
+    """Empty map, a single Gaussian, a 1x1 image, images smaller than a tile or of one tile
+    column: the forward equals the oracle on every pixel, the backward on every Gaussian."""
+    from synth import Camera
+    from tests.helpers import camera, random_small_scene
+    scene, _ = random_small_scene(max(n, 1), 3, D=1, width=W, height=H, f=60.0)
+    scene = scene.subset(np.arange(n))
+    cam = camera(fx=60.0, fy=60.0, cx=(W - 1) / 2, cy=(H - 1) / 2, width=W, height=H, lim=1.3 * (W / 2) / 60.0)
+    cams = [cam]
+    D = 1
+    params = pack_params(scene) if n else torch.zeros((11 + 3 * 4, 64), device="cuda")
+    r = Renderer(n, D, 1, W, H, 1 << 16)
+    rgb, T = r.forward(params, cams, bg=(0.25, 0.5, 0.75))
+    st, flags, P = r.ws.status()
+    assert st == L.GS_OK
+    ref = orc.render(scene, cams, "recipe", bg=(0.25, 0.5, 0.75))
+    _check_colour(rgb.cpu().numpy()[0].transpose(1, 2, 0).reshape(-1, 3),
+                  T.cpu().numpy()[0].reshape(-1), dict(rgb=ref["rgb"][0].transpose(1, 2, 0).reshape(-1, 3),
+                                                       T=ref["T"][0].reshape(-1), flag=ref["flag"][0].reshape(-1)))
+    G = np.random.default_rng(1).normal(size=(1, 3, H, W)).astype(np.float32)
+    grads = torch.zeros_like(params)
+    r.backward(params, cams, torch.from_numpy(G).cuda(), grads, bg=(0.25, 0.5, 0.75))
+    torch.cuda.synchronize()
+    if n == 0:
+        assert float(grads.abs().max()) == 0.0
+        return
+    got = unpack(grads, n, D)
+    gref = orc.backward(scene, cams, G, "recipe", bg=(0.25, 0.5, 0.75), mag=True)
+    _check_grads(got, gref, gref["flagged"])
