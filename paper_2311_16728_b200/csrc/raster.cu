@@ -139,9 +139,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 struct RasterSmem {
-    float4 rec[2][BATCH * 3];  // double-buffered batch of pair records (2 x 12 KB)
+    // double-buffered batch of pair records (2 x 12 KB) + one sentinel record per buffer at
+    // index BATCH (never written by the bulk copies): the forward pads its groups with it
+    float4 rec[2][(BATCH + 1) * 3];
     uint64_t bar[2];
 };
+// the sentinel: far away (power -> -inf: cut), sigma 0 (alpha 0), q_limit -1
+__device__ __forceinline__ void init_sentinel(RasterSmem &S, int tid) {
+    if (tid < 2) {
+        S.rec[tid][3 * BATCH] = make_float4(-1e6f, -1e6f, 1.f, 0.f);
+        S.rec[tid][3 * BATCH + 1] = make_float4(1.f, 0.f, 0.f, 0.f);
+        S.rec[tid][3 * BATCH + 2] = make_float4(0.f, 0.f, 0.f, -1.f);
+    }
+}
 
 // CTA = WARPS warps of one 16x16 tile: blockIdx.x = tile_x * (8 / WARPS) + sub-tile.
 template <int WARPS>
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     const int warp = tid >> 5, lane = tid & 31;
     const unsigned lt = (1u << lane) - 1u;
     const float4 *src = prec + 3 * (size_t)range.x;
+    init_sentinel(S, tid);
     if (tid == 0) {
         mbar_init(&S.bar[0]);
         mbar_init(&S.bar[1]);
@@ -284,8 +295,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
             if (hit) wl[warp][seg * SEGP + nsel + __popc(b & lt)] = j;
             nsel += __popc(b);
             if (k + 32 >= cnt || (k + 32) % SEG == 0) {  // segment complete: its count, and FG
-                if (lane == 0) segn[warp][seg] = nsel;   // padding entries (record 0 of the batch:
-                if (lane < FG) wl[warp][seg * SEGP + nsel + lane] = 0;  // finite data) after it
+                if (lane == 0) segn[warp][seg] = nsel;   // padding entries (the sentinel record:
+                if (lane < FG) wl[warp][seg * SEGP + nsel + lane] = BATCH;  // never composited)
             }
         }
         __syncwarp();
@@ -309,12 +320,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                 bool ok[FG];
 #pragma unroll
                 for (int k = 0; k < FG; k++) {
-                    const int j = jj[k];  // past the list end: the padding (record 0)
+                    const int j = jj[k];  // past the list end: the sentinel (cut, alpha 0)
                     const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
                     float dx, dy;
                     const float p = pixel_power(fx, fy, g0, g1.x, dx, dy);
                     al[k] = fminf(ALPHA_MAX, g1.y * fast_exp(p));
-                    ok[k] = t + k < ns && !(p > 0.0f || p < POWER_CUT) && al[k] >= ALPHA_MIN;
+                    ok[k] = !(p > 0.0f || p < POWER_CUT) && al[k] >= ALPHA_MIN;
                     cr[k] = g1.z;
                     cg[k] = g1.w;
                     cb[k] = r[3 * j + 2].x;
