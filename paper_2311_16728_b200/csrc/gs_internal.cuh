@@ -224,14 +224,15 @@ __device__ __forceinline__ float q_limit(float sigma) {
     return fminf(9.0f, 2.0f * __logf(255.0f * sigma));
 }
 
-// 48-byte per-pair record consumed by the raster kernels (raster.cu):
-// (u, v, A, B) | (C, sigma, r, g) | (b, Gaussian id bits, 0, q_limit(sigma))
+// 48-byte per-pair record consumed by the raster kernels (raster.cu), the conic pre-scaled for
+// the power (exact: pixel_power): (u, v, -A/2, -B) | (-C/2, sigma, r, g) | (b, Gaussian id
+// bits, 0, q_limit(sigma))
 __device__ __forceinline__ void write_pair_record(float4 *__restrict__ prec, int64_t pos,
                                                   const float4 *__restrict__ rec0, const float4 *__restrict__ rec1,
                                                   const float4 *__restrict__ rec2, int64_t m, uint32_t gi) {
-    const float4 r1 = rec1[m];
-    prec[3 * pos] = rec0[m];
-    prec[3 * pos + 1] = r1;
+    const float4 r0 = rec0[m], r1 = rec1[m];
+    prec[3 * pos] = make_float4(r0.x, r0.y, -0.5f * r0.z, -r0.w);
+    prec[3 * pos + 1] = make_float4(-0.5f * r1.x, r1.y, r1.z, r1.w);
     prec[3 * pos + 2] = make_float4(rec2[m].x, __uint_as_float(gi), 0.f, q_limit(r1.y));
 }
 

@@ -43,12 +43,15 @@ constexpr int BATCH = 256;  // records per staged batch (list indices fit in a b
 constexpr int FEW_CHUNK = 5;  // chunked backward: per-lane atomics for entries with <= 5 contributing lanes
 constexpr int FEW_TILE = 6;   // tile backward: the same for <= 6 lanes (measured: 2, 4, 6, 8, 12)
 
-// power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order
-__device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float C, float &dx, float &dy) {
+// power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order.  The pair records carry
+// the conic pre-scaled, (hA, nB, hC) = (-A/2, -B, -C/2) (write_pair_record): scaling by -1/2 is
+// exact and commutes with rounding, so fma(hC dy, dy, (hA dx) dx) is the recipe's -0.5 qf bit
+// for bit and nB dx its -(B dx) -- the same power, one multiplication fewer per pixel and entry.
+__device__ __forceinline__ float pixel_power(float px, float py, const float4 g0, float hC, float &dx, float &dy) {
     dx = SUB(px, g0.x);
     dy = SUB(py, g0.y);
-    float qf = FMA(MUL(C, dy), dy, MUL(MUL(g0.z, dx), dx));
-    return FMA(-MUL(g0.w, dx), dy, MUL(-0.5f, qf));
+    const float hq = FMA(MUL(hC, dy), dy, MUL(MUL(g0.z, dx), dx));
+    return FMA(MUL(g0.w, dx), dy, hq);
 }
 
 // e^power with the SFU: ex2.approx.ftz(power * log2 e).  Forward and backward evaluate alpha
@@ -67,7 +70,7 @@ __device__ __forceinline__ float fast_exp(float power) {
 __device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, float qlim, float x0, float y0,
                                              float h = 3.f) {
     if (qlim < 0.f) return true;
-    const float A = g0.z, B = g0.w, C = g1.x;
+    const float A = -2.f * g0.z, B = -g0.w, C = -2.f * g1.x;  // the record's pre-scaled conic (exact)
     const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + h - g0.y;
     if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return false;
     float best = 3.4e38f;
@@ -92,7 +95,7 @@ __device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, f
 }
 
 // ---------------------------------------------------------------- per-pair records (gather)
-// rec[pos] = (u, v, A, B) | (C, sigma, r, g) | (b, id bits, 0, q_limit(sigma)), pos < P.
+// rec[pos] = (u, v, -A/2, -B) | (-C/2, sigma, r, g) | (b, id bits, 0, q_limit(sigma)), pos < P.
 __global__ void __launch_bounds__(256) k_gather_pairs(const uint32_t *__restrict__ vals,
                                                       const uint64_t *__restrict__ keys,
                                                       const float4 *__restrict__ rec0,
@@ -551,9 +554,9 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
     // power per pixel in the recipe's op order (bit-identical to pixel_power)
     const float dx = SUB(fx, g0.x);
     const float2 dy2 = __fadd2_rn(fy2, f2(-g0.y));
-    const float Adxdx = MUL(MUL(g0.z, dx), dx);
-    const float2 qf2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(Adxdx));
-    const float2 p2 = __ffma2_rn(f2(-MUL(g0.w, dx)), dy2, __fmul2_rn(f2(-0.5f), qf2));
+    const float hAdxdx = MUL(MUL(g0.z, dx), dx);  // pre-scaled conic (pixel_power)
+    const float2 hq2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(hAdxdx));
+    const float2 p2 = __ffma2_rn(f2(MUL(g0.w, dx)), dy2, hq2);
     const float2 e2 = make_float2(fast_exp(p2.x), fast_exp(p2.y));
     const float2 araw = __fmul2_rn(f2(g1.y), e2);
     const float aA = fminf(ALPHA_MAX, araw.x), aB = fminf(ALPHA_MAX, araw.y);
