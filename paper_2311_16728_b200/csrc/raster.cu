@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                 }
 #pragma unroll
                 for (int k = 0; k < FG; k++) {
-                    const float test_T = T * (1.0f - al[k]);
+                    const float test_T = __fmaf_rn(-T, al[k], T);  // T (1 - alpha) as one fma
                     const bool live = ok[k] && !done;
                     const bool stop = live && test_T < T_STOP;
                     const bool take = live && !(test_T < T_STOP);
