@@ -380,6 +380,7 @@ def run_ours(args):
     # and evaluated pairs (list entries up to each pixel's last contributor, which the
     # back-to-front replay visits)
     comp_pairs, eval_pairs, levels_meas = [], [], []
+    L.gs_set_render_stats(True)  # the composited counts are a diagnostic output (off when timed)
     for level in range(cfg["levels"], -1, -1):
         eng.render(level)
         torch.cuda.synchronize()
@@ -390,6 +391,7 @@ def run_ours(args):
         _, _, P_l = rw.status()
         levels_meas.append({"level": level, "V": int((v["radius"] > 0).sum().item()) / len(cams), "P": P_l / len(cams),
                             "px": rw.W * rw.H, "tiles": rw.tiles_x * rw.tiles_y})
+    L.gs_set_render_stats(False)
     pairs_per_step = sum(comp_pairs)
     flops_per_step = BWD_FLOP_PER_EVAL * sum(eval_pairs) + BWD_FLOP_PER_COMP * pairs_per_step
 

@@ -318,6 +318,11 @@ gs_status gs_permute_columns(const float *src, float *dst, int64_t ld, int32_t r
 /* Stable LSD radix sort of n (key, value) pairs on key bits [0, key_bits) (8-bit digits,
    one decoupled-look-back pass per digit).  Sorted in place in keys/vals; keys_alt/vals_alt
    are ping-pong buffers of n entries; temp of gs_sort_temp_size bytes. */
+/* Diagnostics: with on != 0 the forward also writes each pixel's number of composited
+   Gaussians (gs_debug_workspace_view n_composited); off (the default) it leaves that array as it
+   was -- the count costs ~6 % of the forward's instructions.  Process-wide setting. */
+gs_status gs_set_render_stats(int32_t on);
+
 gs_status gs_sort_temp_size(int64_t n, int32_t key_bits, size_t *bytes);
 gs_status gs_debug_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_alt, uint32_t *vals_alt, int64_t n,
                               int32_t key_bits, void *temp, size_t temp_bytes, gs_stream_t stream);

@@ -31,7 +31,7 @@ EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess",
            "gs_query_status", "gs_status_async", "gs_workspace_release", "gs_status_str",
            "gs_comm_shard", "gs_peer_barrier", "gs_reduce_adam_bcast", "gs_spatial_order_temp_size", "gs_spatial_order",
            "gs_permute_columns", "gs_sort_temp_size", "gs_debug_sort_pairs",
-           "gs_debug_workspace_view", "gs_set_binning", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
+           "gs_debug_workspace_view", "gs_set_binning", "gs_set_render_stats", "gs_profile_kernel", "gs_profile_read", "gs_debug_exp_scale"]
 
 
 class GsError(RuntimeError):
@@ -362,6 +362,11 @@ def gs_debug_workspace_view(ws, n, n_views, width, height) -> GsWsView:
                                          C.c_int32(width), C.c_int32(height), C.byref(out)),
            "gs_debug_workspace_view")
     return out
+
+
+def gs_set_render_stats(on: bool):
+    """Diagnostic composited counts in the forward (n_composited); off by default."""
+    _check(lib().gs_set_render_stats(C.c_int32(int(bool(on)))), "gs_set_render_stats")
 
 
 def gs_set_binning(mode: int):

@@ -636,6 +636,11 @@ gs_status gs_profile_read(double *total_ms, int64_t *launches) {
     return GS_OK;
 }
 
+gs_status gs_set_render_stats(int32_t on) {
+    set_render_stats(on ? 1 : 0);
+    return GS_OK;
+}
+
 gs_status gs_debug_exp_scale(const float *s, float *out, int64_t n, gs_stream_t stream) {
     if (!s || !out || n < 0) return GS_ERR_INVALID_ARG;
     return cuda_status(launch_exp_scale(s, out, n, (cudaStream_t)stream));

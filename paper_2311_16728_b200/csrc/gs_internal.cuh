@@ -329,6 +329,9 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
                               cudaStream_t s, bool scheduled = false);
 // A2 for the bucket binning fused with the raster schedule (one CTA; V * tiles <= 8192)
 bool fused_tile_schedule(const Layout &L);
+// diagnostic per-pixel composited counts in the forward (off on the hot path)
+void set_render_stats(int on);
+int render_stats();
 cudaError_t launch_tile_scan(const Layout &L, void *ws, cudaStream_t s);
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s);
 // A9 into the compacted scratch (one row per parameter, one column per visible Gaussian)

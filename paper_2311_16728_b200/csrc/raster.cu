@@ -173,7 +173,7 @@ __device__ __forceinline__ void warp_block(int bxi, int &tile_x, int &wx0, int &
 // Per-pixel outputs of the forward: colour (+ T_final bg), T, last position, composited count;
 // with CHUNKED the reverse pass turning the per-chunk records into (T after the chunk,
 // normalised colour behind it) for the chunked backward.
-template <bool CHUNKED>
+template <bool CHUNKED, bool STATS = true>
 __device__ __forceinline__ void fwd_finish(int view, int px, int py, int W, int H, float T, float c0, float c1,
                                            float c2, uint32_t last, uint32_t composited, float bg0, float bg1,
                                            float bg2, float *out_rgb, float *out_T, float *T_keep,
@@ -188,7 +188,7 @@ __device__ __forceinline__ void fwd_finish(int view, int px, int py, int W, int 
     if (out_T) out_T[(int64_t)view * HW + pix] = T;
     T_keep[(int64_t)view * HW + pix] = T;
     ncontrib[(int64_t)view * HW + pix] = last;
-    ncomp[(int64_t)view * HW + pix] = composited;
+    if (STATS) ncomp[(int64_t)view * HW + pix] = composited;
     if (CHUNKED && last > 0) {
         // reverse pass over the chunks up to the last composited one: normalised colour behind
         // each chunk, acc_end(k) = behind(k) / T_after(k), behind(k) = sum of the later chunks'
@@ -214,7 +214,9 @@ __device__ __forceinline__ void fwd_finish(int view, int px, int py, int W, int 
     }
 }
 
-template <int WARPS, bool CHUNKED>
+// STATS: also count the composited entries per pixel (n_composited, a diagnostic output:
+// gs_set_render_stats) -- off on the hot path, where it costs 2 of ~33 instructions per entry
+template <int WARPS, bool CHUNKED, bool STATS>
 __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restrict__ ranges,
                                                            const float4 *__restrict__ prec, int W, int H, int TX,
                                                            int tiles, float bg0, float bg1, float bg2,
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                     d1 += cg[k] * w;
                     d2 += cb[k] * w;
                     T = take ? test_T : T;
-                    composited += take ? 1u : 0u;
+                    if constexpr (STATS) composited += take ? 1u : 0u;
                     if (take) last = (uint32_t)(b0 + jj[k] + 1);
                 }
             }
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
     // never leave with a bulk copy still writing into this CTA's shared memory
     if (inflight >= 0 && tid == 0) mbar_wait(&S.bar[inflight], (phases >> inflight) & 1u);
     if (inside)
-        fwd_finish<CHUNKED>(view, px, py, W, H, T, c0, c1, c2, last, composited, bg0, bg1, bg2, out_rgb, out_T, T_keep,
+        fwd_finish<CHUNKED, STATS>(view, px, py, W, H, T, c0, c1, c2, last, composited, bg0, bg1, bg2, out_rgb, out_T, T_keep,
                             ncontrib, ncomp, CHUNKED ? chunk_base[view * tiles + tile] : 0, ly * TILE + lx,
                             chunk_bwd);
 }
@@ -970,11 +972,16 @@ cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static int g_render_stats = 0;
+void set_render_stats(int on) { g_render_stats = on; }
+int render_stats() { return g_render_stats; }
+
 template <int WARPS>
 static void fwd_launch(const Layout &L, void *ws, const float bg[3], float *out_rgb, float *out_T,
                        const uint32_t *cbase, float4 *cbwd, const uint32_t *order, cudaStream_t s) {
     dim3 grid(L.TX * (8 / WARPS), L.TY, L.V);
-    auto kern = cbwd ? k_raster_fwd<WARPS, true> : k_raster_fwd<WARPS, false>;
+    auto kern = render_stats() ? (cbwd ? k_raster_fwd<WARPS, true, true> : k_raster_fwd<WARPS, false, true>)
+                               : (cbwd ? k_raster_fwd<WARPS, true, false> : k_raster_fwd<WARPS, false, false>);
     launch_pdl(kern, grid, WARPS * 32, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.W, L.H, L.TX, L.tiles, bg[0],
                                      bg[1], bg[2], out_rgb, out_T, at<float>(ws, L.Tfinal),
                                      at<uint32_t>(ws, L.ncontrib), at<uint32_t>(ws, L.ncomp), cbase, cbwd, order);

@@ -200,6 +200,15 @@ def test_forward_parity_tiny_full_image():
     ok = ref["flag"][0] == 0
     np.testing.assert_array_equal(last[ok], ref["last"][0][ok])
     assert (ref["ncomp"] > 0).mean() > 0.3
+    # composited counts (a diagnostic output, gs_set_render_stats) equal the oracle's
+    L.gs_set_render_stats(True)
+    try:
+        r.forward(params, cams)
+        torch.cuda.synchronize()
+        nco = r.ws.views()["n_composited"].cpu().numpy().reshape(cams[0].height, cams[0].width)
+    finally:
+        L.gs_set_render_stats(False)
+    np.testing.assert_array_equal(nco[ok], ref["ncomp"][0][ok])
 
 
 @pytest.mark.parametrize("cfg,views,level", [("tum", 1, 0), ("tum", 1, 2), ("euroc", 4, 1), ("euroc", 2, 0), ("replica", 1, 0)])
