@@ -101,3 +101,46 @@ def test_engine_peer_densify(pg):
     for _ in range(2):
         eng.build_pyramids()
         assert np.isfinite([x.item() for x in eng.step()]).all()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_reduce_adam_bcast_multi_rank_arithmetic(world):
+    """The peer path of gs_reduce_adam_bcast for `world` ranks, emulated on one GPU without the
+    barriers (nothing waits on anything): `world` parameter / gradient buffers on this device
+    stand for the ranks' symmetric buffers; calling the kernel for every rank in turn must leave
+    every rank's parameters equal to one gs_adam_step on the summed gradient, every gradient
+    buffer zeroed, and each rank's moment shard equal to its range of the full moments."""
+    from paper_2311_16728_b200.comm import comm_shard
+    scene = make_scene("tum", n=5003)
+    n, D = scene.n, 3
+    cfg = AdamConfig(lr_means=1e-2)
+    p0 = pack_params(scene)
+    K, ld = p0.shape
+    gen = torch.Generator("cuda").manual_seed(5)
+    params = [p0.clone() for _ in range(world)]
+    grads = [torch.randn(p0.shape, device="cuda", generator=gen) for _ in range(world)]
+    for g in grads:
+        g[:, n:] = 0
+    gsum = torch.stack(grads).sum(0)  # rank order 0..world-1, as the kernel sums
+    gsum_seq = grads[0].clone()
+    for g in grads[1:]:
+        gsum_seq += g
+    ref_p = p0.clone()
+    ref = Adam(ref_p, n, D, cfg)
+    ref.step(gsum_seq.clone(), zero_grads=True)
+    shards = []
+    for r in range(world):
+        e0, e1 = comm_shard(n, D, r, world)
+        q = -(-(K * ld) // 4 // world) * 4
+        m = torch.zeros(q, device="cuda")
+        v = torch.zeros(q, device="cuda")
+        L.gs_reduce_adam_bcast(L.params_struct(params[r], n, D), [p.data_ptr() for p in params],
+                               [g.data_ptr() for g in grads], 0, 0, m, v, cfg.struct(), 1, None, r, world)
+        shards.append((e0, e1, m, v))
+    torch.cuda.synchronize()
+    for r in range(world):
+        assert torch.equal(params[r], ref_p), r
+        assert float(grads[r].abs().max()) == 0.0
+    mflat, vflat = ref.m.reshape(-1), ref.v.reshape(-1)
+    for e0, e1, m, v in shards:
+        assert torch.equal(m[:e1 - e0], mflat[e0:e1]) and torch.equal(v[:e1 - e0], vflat[e0:e1])
