@@ -23,10 +23,11 @@
 // pixels have stopped.
 //
 // The backward replays each pixel's list back to front: dL/dc, dL/dalpha
-// = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  The nine
-// per-pixel gradients of a Gaussian are summed over the warp with a transposing butterfly
-// (9 + 5 shuffles instead of 45) and added to the per-(view, Gaussian) record by nine lanes
-// with one scalar red.global.add each.
+// = T_k sum_c g_c (c_k - acc), dL/dsigma, dL/dpower -> dL/dmean2d, dL/dconic.  A warp owns an
+// 8x8 block as four 4x4 quadrants of eight lanes (two pixels per lane); each quadrant culls
+// and walks its own list, and the nine per-pixel gradients of its Gaussian are summed over its
+// eight lanes with a transposing butterfly (10 shuffles) and added to the per-(view, Gaussian)
+// record with one scalar red.global.add per lane.
 #include "gs_internal.cuh"
 
 namespace gsk {
@@ -40,8 +41,10 @@ constexpr float ALPHA_MIN = 1.0f / 255.0f;
 constexpr float T_STOP = 1e-4f;
 constexpr float POWER_CUT = -4.5f;
 constexpr int BATCH = 256;  // records per staged batch (list indices fit in a byte)
-constexpr int FEW_CHUNK = 5;  // chunked backward: per-lane atomics for entries with <= 5 contributing lanes
-constexpr int FEW_TILE = 6;   // tile backward: the same for <= 6 lanes (measured: 2, 4, 6, 8, 12)
+// backward: per-lane atomics instead of the group reductions when no quadrant group has more
+// than this many contributing lanes (measured: chunked 3, 5, 7; tile-serial 2, 3, 6, 8)
+constexpr int FEW_CHUNK = 5;
+constexpr int FEW_TILEQ = 3;
 
 // power = -1/2 (A dx^2 + C dy^2) - B dx dy in the recipe's op order.  The pair records carry
 // the conic pre-scaled, (hA, nB, hC) = (-A/2, -B, -C/2) (write_pair_record): scaling by -1/2 is
@@ -68,10 +71,10 @@ __device__ __forceinline__ float fast_exp(float power) {
 // (1e-3 relative + 1e-3 absolute) absorbs the rounding of the per-pixel fp32 power, so a
 // culled Gaussian can never pass the per-pixel tests.
 __device__ __forceinline__ bool block_misses(const float4 g0, const float4 g1, float qlim, float x0, float y0,
-                                             float h = 3.f) {
+                                             float h = 3.f, float w = 7.f) {
     if (qlim < 0.f) return true;
     const float A = -2.f * g0.z, B = -g0.w, C = -2.f * g1.x;  // the record's pre-scaled conic (exact)
-    const float ax = x0 - g0.x, bx = x0 + 7.f - g0.x, ay = y0 - g0.y, by = y0 + h - g0.y;
+    const float ax = x0 - g0.x, bx = x0 + w - g0.x, ay = y0 - g0.y, by = y0 + h - g0.y;
     if (ax <= 0.f && bx >= 0.f && ay <= 0.f && by >= 0.f) return false;
     float best = 3.4e38f;
     // edges x = X: f = A X^2 + 2 B X y + C y^2, y* = -B X / C clamped to [ay, by].  The
@@ -368,40 +371,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_raster_fwd(const uint2 *__restri
                             chunk_bwd);
 }
 
-// Warp sums of nine values: the eight of a[] with a transposing butterfly (at offsets 16, 8, 4
-// every lane keeps half of its values and receives the partner's other half) while the ninth
-// (b) is summed plainly alongside; at offset 2 the pair (r, b) is itself transposed and offset 1
-// finishes both: 4 + 1 + 2 + 1 + 1 + 1 + 1 + 1 = 12 shuffles instead of 9 + 5.  Lanes with (lane & 3) == 2 end with the total of value index
-// ((l >> 4) & 1) * 4 + ((l >> 3) & 1) * 2 + ((l >> 2) & 1); lanes with (lane & 2) == 0 with the
-// total of b.
-__device__ __forceinline__ float warp_sum9_transposed(float a[8], float b, int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-    float h[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const float send = b4 ? a[k] : a[k + 4];
-        const float keep = b4 ? a[k + 4] : a[k];
-        h[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    b += __shfl_xor_sync(0xffffffffu, b, 16);
-    float q[2];
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        const float send = b3 ? h[k] : h[k + 2];
-        const float keep = b3 ? h[k + 2] : h[k];
-        q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    b += __shfl_xor_sync(0xffffffffu, b, 8);
-    const float send = b2 ? q[0] : q[1];
-    float r = (b2 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
-    b += __shfl_xor_sync(0xffffffffu, b, 4);
-    // (r, b) transposed at offset 2: bit-1 lanes keep r, the others b
-    const float s2 = b1 ? b : r;
-    float x = (b1 ? r : b) + __shfl_xor_sync(0xffffffffu, s2, 2);
-    x += __shfl_xor_sync(0xffffffffu, x, 1);
-    return x;
-}
-
 // ================================================================ chunked backward (few tiles)
 // At pyramid levels with few tiles (V * tiles < CHUNK_MAX_TILES) each warp of the tile-serial
 // backward would walk a long list alone.  The forward (same kernel, CHUNKED instance) records,
@@ -525,12 +494,10 @@ __global__ void __launch_bounds__(1024) k_chunk_index(const uint2 *__restrict__ 
 }
 
 // ================================================================ two-pixel packed backward
-// Backward for levels with many tiles: a warp owns an 8x8 block and every lane two pixels
-// (x, y) and (x, y + 4), evaluated with Blackwell's packed fp32x2 instructions (FFMA2 / FMUL2 /
-// FADD2, IEEE round-to-nearest per element, so the power and alpha of each pixel are the same
-// bits as the scalar forward).  Per-pixel validity is folded into masked alphas instead of
-// branches; the list walk, record loads, the warp reduction and the atomics are shared by 64
-// pixels instead of 32.
+// A warp owns an 8x8 block, every lane two pixels, evaluated with Blackwell's packed fp32x2
+// instructions (FFMA2 / FMUL2 / FADD2, IEEE round-to-nearest per element, so the power and
+// alpha of each pixel are the same bits as the scalar forward).  Per-pixel validity is folded
+// into masked alphas instead of branches.
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
@@ -538,25 +505,59 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-// Per-lane state of the two pixels (x, y) and (x, y + 4) in the back-to-front replay.
+// Per-lane state of the lane's two pixels in the back-to-front replay.
 struct Pix2 {
     float2 T, acc0, acc1, acc2, g0, g1, g2;  // T after the entry, colour behind, dL/dpixel
     uint32_t lastA, lastB;                   // 1-based list position of the last composited
 };
 
-// One list entry j (1-based list position `position`) of the replay for the warp's 64 pixels:
-// recover T before it, dL/dalpha = T sum_c g_c (c - acc), then the gradient moments
-// S(a), S(b), S(a dx), S(a dy), S(b dy) with a = dL/dpower dx, b = dL/dpower dy, dL/dsigma and
-// dL/dcolour summed over the warp and added to the Gaussian's per-view record.
-// FEW: at most this many contributing lanes -> per-lane atomics instead of the warp reduction
+// ---- quadrant groups: the warp's 8x8 block as four 4x4 quadrants, eight lanes each (lane
+// 8q + i: quadrant q, pixels (i & 3, i >> 2) and (i & 3, (i >> 2) + 2) inside it).  Every group
+// walks its own list -- the Gaussians that reach its 4x4 quadrant -- so a warp step advances
+// four entries (one per group) and the walk is the longest of the four quadrant lists instead
+// of the 8x8 block's list.  Replica-like map, mean over the warps without the stop at the
+// last contributor: 283 vs 639 entries at level 2, 114 vs 224 at level 1, 62 vs 100 at level 0.
+
+// Sums of nine values over the eight lanes of a group: the eight of a[] with a transposing
+// butterfly at offsets 4, 2, 1 (lane i of the group ends with the total of value i), the ninth
+// (b, total in every lane) summed alongside: 4 + 2 + 1 + 3 = 10 shuffles.
+__device__ __forceinline__ float group_sum9_transposed(float a[8], float &b, int lane) {
+    const bool b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+    float h[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const float send = b2 ? a[k] : a[k + 4];
+        const float keep = b2 ? a[k + 4] : a[k];
+        h[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    b += __shfl_xor_sync(0xffffffffu, b, 4);
+    float q[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+        const float send = b1 ? h[k] : h[k + 2];
+        const float keep = b1 ? h[k + 2] : h[k];
+        q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    b += __shfl_xor_sync(0xffffffffu, b, 2);
+    const float send = b0 ? q[0] : q[1];
+    const float r = (b0 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
+    b += __shfl_xor_sync(0xffffffffu, b, 1);
+    return r;
+}
+
+// One warp step of the quadrant-group replay: every group its own entry j (the sentinel past
+// its list's end, 1-based list position `position`): recover T before it, dL/dalpha =
+// T sum_c g_c (c - acc), then the gradient moments S(a), S(b), S(a dx), S(a dy), S(b dy) with
+// a = dL/dpower dx, b = dL/dpower dy, dL/dsigma and dL/dcolour, summed over the group and
+// added to its Gaussian's per-view record.  FEW (warp-uniform): if no group has more than FEW
+// contributing lanes, those lanes add their own values.
 template <int FEW>
-__device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint32_t position, float fx,
-                                           float2 fy2, int lane, int red_off, float *g2dv) {
+__device__ __forceinline__ void bwdq_entry(Pix2 &P, const float4 *r, int j, uint32_t position, float fx,
+                                           float2 fy2, int lane, float *g2dv) {
     const float4 g0 = r[3 * j], g1 = r[3 * j + 1];
-    // power per pixel in the recipe's op order (bit-identical to pixel_power)
     const float dx = SUB(fx, g0.x);
     const float2 dy2 = __fadd2_rn(fy2, f2(-g0.y));
-    const float hAdxdx = MUL(MUL(g0.z, dx), dx);  // pre-scaled conic (pixel_power)
+    const float hAdxdx = MUL(MUL(g0.z, dx), dx);
     const float2 hq2 = __ffma2_rn(__fmul2_rn(f2(g1.x), dy2), dy2, f2(hAdxdx));
     const float2 p2 = __ffma2_rn(f2(MUL(g0.w, dx)), dy2, hq2);
     const float2 e2 = make_float2(fast_exp(p2.x), fast_exp(p2.y));
@@ -564,10 +565,10 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
     const float aA = fminf(ALPHA_MAX, araw.x), aB = fminf(ALPHA_MAX, araw.y);
     const bool vA = position <= P.lastA && !(p2.x > 0.0f || p2.x < POWER_CUT) && aA >= ALPHA_MIN;
     const bool vB = position <= P.lastB && !(p2.y > 0.0f || p2.y < POWER_CUT) && aB >= ALPHA_MIN;
-    if (!__any_sync(0xffffffffu, vA || vB)) return;
-    const float2 al = make_float2(vA ? aA : 0.f, vB ? aB : 0.f);            // masked alpha
-    const float2 ua = make_float2(vA && !(araw.x > ALPHA_MAX) ? aA : 0.f,  // unclamped part
-                                  vB && !(araw.y > ALPHA_MAX) ? aB : 0.f);
+    const unsigned bal = __ballot_sync(0xffffffffu, vA || vB);
+    if (bal == 0u) return;
+    const float2 al = make_float2(vA ? aA : 0.f, vB ? aB : 0.f);
+    const float2 ua = make_float2(vA && !(araw.x > ALPHA_MAX) ? aA : 0.f, vB && !(araw.y > ALPHA_MAX) ? aB : 0.f);
     const float2 ue = make_float2(ua.x != 0.f ? e2.x : 0.f, ua.y != 0.f ? e2.y : 0.f);
     P.T = __fmul2_rn(P.T, make_float2(rcp_approx(1.0f - al.x), rcp_approx(1.0f - al.y)));
     const float2 w2 = __fmul2_rn(al, P.T);
@@ -588,137 +589,33 @@ __device__ __forceinline__ void bwd2_entry(Pix2 &P, const float4 *r, int j, uint
     const float2 qc = __fmul2_rn(b2, dy2);
     float vals8[8] = {a2.x + a2.y, b2.x + b2.y, qa.x + qa.y, qb.x + qb.y,
                       qc.x + qc.y, dsig.x + dsig.y, dr.x + dr.y, dg.x + dg.y};
+    float v9 = db.x + db.y;
     const uint32_t gi = __float_as_uint(r[3 * j + 2].y);
-    float *dst = g2dv + 12 * gi;  // the view's 48-byte records (g2dv = g2d + 3 view n)
-    if (FEW > 0 && __popc(__ballot_sync(0xffffffffu, vA || vB)) <= FEW) {
-        // few contributing lanes (an entry touching the block's edge): their own atomics are
-        // cheaper than the warp reduction
-        if (vA || vB) {
+    float *dst = g2dv + 12 * gi;
+    const int gsh = lane & 24;  // this lane's group: ballot bits [gsh, gsh + 8)
+    if (FEW > 0) {
+        const bool few = __popc(bal & 0xffu) <= FEW && __popc(bal & 0xff00u) <= FEW &&
+                         __popc(bal & 0xff0000u) <= FEW && __popc(bal & 0xff000000u) <= FEW;
+        if (few) {
+            if (vA || vB) {
 #pragma unroll
-            for (int k = 0; k < 8; k++) atomicAdd(dst + k, vals8[k]);
-            atomicAdd(dst + 8, db.x + db.y);
+                for (int k = 0; k < 8; k++) atomicAdd(dst + k, vals8[k]);
+                atomicAdd(dst + 8, v9);
+            }
+            return;
         }
-        return;
     }
-    const float mine = warp_sum9_transposed(vals8, db.x + db.y, lane);
-    if ((lane & 3) == 2 || lane == 0) atomicAdd(dst + red_off, mine);
-}
-
-// per-lane slot of warp_sum9_transposed's result: value index for (lane & 3) == 2, 8 (b) for lane 0
-__device__ __forceinline__ int sum9_slot(int lane) {
-    return (lane & 3) == 2 ? ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1) : 8;
-}
-
-__global__ void __launch_bounds__(128) k_raster_bwd2(const uint2 *__restrict__ ranges,
-                                                     const float4 *__restrict__ prec, int64_t n, int W, int H,
-                                                     int TX, int tiles, float bg0, float bg1, float bg2,
-                                                     const float *__restrict__ dL_drgb,
-                                                     const float *__restrict__ T_keep,
-                                                     const uint32_t *__restrict__ ncontrib,
-                                                     float4 *__restrict__ g2d, const uint32_t *__restrict__ order) {
-    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
-    pdl_trigger();
-    __shared__ __align__(128) RasterSmem S;
-    __shared__ uint8_t wl[4][BATCH];
-    __shared__ uint32_t s_maxlast;
-    // tiles in longest-list-first order (less tail); blockIdx decides without an order
-    int view = blockIdx.z, ty = blockIdx.y, tx = blockIdx.x;
-    if (order) {
-        const uint32_t gt = order[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
-        view = gt / tiles;
-        ty = (gt % tiles) / TX;
-        tx = (gt % tiles) % TX;
-    }
-    const int tile = ty * TX + tx;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
-    const int px = tx * TILE + bx + (lane & 7);
-    const int pyA = ty * TILE + by + (lane >> 3), pyB = pyA + 4;
-    const float wx0 = (float)(tx * TILE + bx), wy0 = (float)(ty * TILE + by);
-    const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
-    const uint2 range = ranges[(int64_t)view * tiles + tile];
-    const float fx = (float)px;
-    const float2 fy2 = make_float2((float)pyA, (float)pyB);
-    float *g2dv = reinterpret_cast<float *>(g2d + 3 * (int64_t)view * n);
-    const int red_off = sum9_slot(lane);
-    const int64_t HW = (int64_t)H * W;
-    const int64_t pixA = (int64_t)pyA * W + px, pixB = (int64_t)pyB * W + px;
-    Pix2 P;
-    P.T = f2(1.f);
-    P.g0 = P.g1 = P.g2 = f2(0.f);
-    P.lastA = P.lastB = 0;
-    const float *gbase = dL_drgb + (int64_t)view * 3 * HW;
-    if (inA) {
-        P.T.x = T_keep[(int64_t)view * HW + pixA];
-        P.lastA = ncontrib[(int64_t)view * HW + pixA];
-        P.g0.x = gbase[pixA];
-        P.g1.x = gbase[HW + pixA];
-        P.g2.x = gbase[2 * HW + pixA];
-    }
-    if (inB) {
-        P.T.y = T_keep[(int64_t)view * HW + pixB];
-        P.lastB = ncontrib[(int64_t)view * HW + pixB];
-        P.g0.y = gbase[pixB];
-        P.g1.y = gbase[HW + pixB];
-        P.g2.y = gbase[2 * HW + pixB];
-    }
-    if (tid == 0) {
-        s_maxlast = 0;
-        mbar_init(&S.bar[0]);
-        mbar_init(&S.bar[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t wlast = max(P.lastA, P.lastB);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
-    if (lane == 0) atomicMax(&s_maxlast, wlast);
-    __syncthreads();
-    const int todo_all = (int)s_maxlast;
-    const float4 *src = prec + 3 * (size_t)range.x;
-    if (tid == 0 && todo_all > 0) {
-        int cnt0 = min(BATCH, todo_all);
-        bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
-    }
-    uint32_t phases = 0u;
-    P.acc0 = f2(bg0);
-    P.acc1 = f2(bg1);
-    P.acc2 = f2(bg2);
-    const unsigned lt = (1u << lane) - 1u;
-    for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
-        const int buf = it & 1;
-        const int cnt = min(BATCH, b_end);
-        const int b_start = b_end - cnt;
-        __syncthreads();
-        if (tid == 0 && b_start > 0) {
-            int cn = min(BATCH, b_start);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
-        }
-        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
-        phases ^= 1u << buf;
-        const float4 *r = S.rec[buf];
-        int nsel = 0;
-        for (int k = 0; k < cnt; k += 32) {
-            const int jj = k + lane;
-            const int idx = cnt - 1 - jj;
-            bool hit = jj < cnt && (uint32_t)(b_start + idx + 1) <= wlast &&
-                       !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, wx0, wy0, 7.f);
-            unsigned b = __ballot_sync(0xffffffffu, hit);
-            if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
-            nsel += __popc(b);
-        }
-        __syncwarp();
-        for (int t = 0; t < nsel; t++) {
-            const int j = wl[warp][t];
-            bwd2_entry<FEW_TILE>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, red_off, g2dv);
-        }
+    const float mine = group_sum9_transposed(vals8, v9, lane);
+    if ((bal >> gsh) & 0xffu) {  // the group has a contribution (its entry is not the sentinel)
+        const int i = lane & 7;
+        atomicAdd(dst + i, mine);
+        if (i == 0) atomicAdd(dst + 8, v9);
     }
 }
 
-// Chunked backward with the two-pixel layout: one CTA (4 warps, 8x8 blocks) per chunk; the
-// chunk's records are loaded once for the whole tile.
-__global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restrict__ ranges,
+// Chunked backward (levels with few tiles): one CTA (4 warps, 8x8 blocks) per chunk; the
+// chunk's records are loaded once for the whole tile and culled as in k_raster_bwdq.
+__global__ void __launch_bounds__(128) k_raster_bwdq_chunk(const uint2 *__restrict__ ranges,
                                                            const float4 *__restrict__ prec,
                                                            const uint32_t *__restrict__ chunk_base,
                                                            const uint32_t *__restrict__ chunk_tile,
@@ -731,18 +628,20 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
                                                            const uint32_t *__restrict__ chunk_order) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
-    __shared__ __align__(128) float4 rec[CHUNK * 3];
+    __shared__ __align__(128) float4 rec[(CHUNK + 1) * 3];  // + the sentinel at index CHUNK
     __shared__ uint64_t bar;
-    __shared__ uint8_t wl[4][CHUNK];
+    __shared__ uint8_t wl[4][4][CHUNK];
+    __shared__ uint8_t wl8[4][CHUNK];
     if ((int)blockIdx.x >= (int)hdr->nchunks) return;
     const int c = chunk_order[blockIdx.x];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane >> 3, gl = lane & 7;
     const uint32_t gt = chunk_tile[c];
     const int view = gt / tiles, tl = gt % tiles;
     const int tx = tl % TX, ty = tl / TX;
-    const int bx = (warp & 1) * 8, by = (warp >> 1) * 8;
-    const int lx = bx + (lane & 7), lyA = by + (lane >> 3);
-    const int px = tx * TILE + lx, pyA = ty * TILE + lyA, pyB = pyA + 4;
+    const int qx = (warp & 1) * 8 + (q & 1) * 4, qy = (warp >> 1) * 8 + (q >> 1) * 4;  // quadrant origin
+    const int lx = qx + (gl & 3), lyA = qy + (gl >> 2), lyB = lyA + 2;
+    const int px = tx * TILE + lx, pyA = ty * TILE + lyA, pyB = ty * TILE + lyB;
     const uint2 range = ranges[gt];
     const int b0 = (int)(c - chunk_base[gt]) * CHUNK;
     const int cnt = min(CHUNK, (int)(range.y - range.x) - b0);
@@ -772,7 +671,7 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
         const int64_t pix = (int64_t)pyB * W + px;
         const uint32_t last = ncontrib[(int64_t)view * HW + pix];
         if ((uint32_t)b0 < last) {
-            const float4 e = cb[(lyA + 4) * TILE + lx];
+            const float4 e = cb[lyB * TILE + lx];
             P.lastB = last;
             P.T.y = e.x;
             P.acc0.y = e.y;
@@ -783,37 +682,197 @@ __global__ void __launch_bounds__(128) k_raster_bwd2_chunk(const uint2 *__restri
             P.g2.y = gbase[2 * HW + pix];
         }
     }
-    uint32_t wlast = max(P.lastA, P.lastB);
+    uint32_t glast = max(P.lastA, P.lastB);  // the group's last composited position
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    for (int o = 4; o > 0; o >>= 1) glast = max(glast, __shfl_xor_sync(0xffffffffu, glast, o));
+    uint32_t wlast = glast;
+#pragma unroll
+    for (int o = 16; o > 4; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
     if (tid == 0) {
         mbar_init(&bar);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (tid < 3)  // the sentinel: far away (cut), sigma 0, id 0
+        rec[3 * CHUNK + tid] = tid == 0 ? make_float4(-1e6f, -1e6f, 1.f, 0.f)
+                                        : (tid == 1 ? make_float4(1.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, -1.f));
     if (__syncthreads_or(wlast != 0) == 0) return;  // no pixel of the tile reaches this chunk
     if (tid == 0) bulk_load(rec, prec + 3 * ((size_t)range.x + b0), (uint32_t)cnt * 48u, &bar);
     if (wlast == 0) return;  // warp-uniform; the copy is waited on by the warps that use it
     mbar_wait(&bar, 0u);
-    const unsigned lt = (1u << lane) - 1u;
-    const float wx0 = (float)(tx * TILE + bx), wy0 = (float)(ty * TILE + by);
+    // per group: the entries (back to front) that can reach its 4x4 quadrant -- the warp's
+    // 8x8 block culled first (one entry per lane), then each group tests the survivors
+    const float fqx = (float)(tx * TILE + qx), fqy = (float)(ty * TILE + qy);
+    const unsigned lt = (1u << gl) - 1u;
     int nsel = 0;
-    for (int k = 0; k < cnt; k += 32) {
-        const int jj = k + lane;
-        const int idx = cnt - 1 - jj;
-        bool hit = jj < cnt && (uint32_t)(b0 + idx + 1) <= wlast &&
-                   !block_misses(rec[3 * idx], rec[3 * idx + 1], rec[3 * idx + 2].w, wx0, wy0, 7.f);
-        unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (hit) wl[warp][nsel + __popc(b & lt)] = (uint8_t)idx;
-        nsel += __popc(b);
+    int n8 = 0;
+    {
+        const float wx0 = (float)(tx * TILE + (warp & 1) * 8), wy0 = (float)(ty * TILE + (warp >> 1) * 8);
+        const unsigned lt32 = (1u << lane) - 1u;
+        for (int k = 0; k < cnt; k += 32) {
+            const int jj = k + lane;
+            const int idx = cnt - 1 - jj;
+            const bool hit = jj < cnt && (uint32_t)(b0 + idx + 1) <= wlast &&
+                             !block_misses(rec[3 * idx], rec[3 * idx + 1], rec[3 * idx + 2].w, wx0, wy0, 7.f, 7.f);
+            const unsigned b = __ballot_sync(0xffffffffu, hit);
+            if (hit) wl8[warp][n8 + __popc(b & lt32)] = (uint8_t)idx;
+            n8 += __popc(b);
+        }
+        __syncwarp();
+    }
+    for (int k = 0; k < n8; k += 8) {
+        const int e = k + gl;
+        const int idx = e < n8 ? wl8[warp][e] : 0;
+        const bool hit = e < n8 && (uint32_t)(b0 + idx + 1) <= glast &&
+                         !block_misses(rec[3 * idx], rec[3 * idx + 1], rec[3 * idx + 2].w, fqx, fqy, 3.f, 3.f);
+        const unsigned gb = (__ballot_sync(0xffffffffu, hit) >> (lane & 24)) & 0xffu;
+        if (hit) wl[warp][q][nsel + __popc(gb & lt)] = (uint8_t)idx;
+        nsel += __popc(gb);
     }
     __syncwarp();
+    int nmax = nsel;
+#pragma unroll
+    for (int o = 16; o > 4; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     const float fx = (float)px;
     const float2 fy2 = make_float2((float)pyA, (float)pyB);
     float *g2dv = reinterpret_cast<float *>(g2d + 3 * (int64_t)view * n);
-    const int red_off = sum9_slot(lane);
-    for (int t = 0; t < nsel; t++) {
-        const int j = wl[warp][t];
-        bwd2_entry<FEW_CHUNK>(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, red_off, g2dv);
+    for (int t = 0; t < nmax; t++) {
+        const int j = t < nsel ? wl[warp][q][t] : CHUNK;
+        bwdq_entry<FEW_CHUNK>(P, rec, j, (uint32_t)(b0 + j + 1), fx, fy2, lane, g2dv);
+    }
+}
+
+// Tile-serial backward (levels with many tiles): one CTA (4 warps) per 16x16 tile, TMA
+// double-buffered record batches from the end of the list; the warp culls each batch against
+// its 8x8 block, each eight-lane group the survivors against its 4x4 quadrant, and every group
+// walks its own list.
+__global__ void __launch_bounds__(128) k_raster_bwdq(const uint2 *__restrict__ ranges,
+                                                     const float4 *__restrict__ prec, int64_t n, int W, int H,
+                                                     int TX, int tiles, float bg0, float bg1, float bg2,
+                                                     const float *__restrict__ dL_drgb,
+                                                     const float *__restrict__ T_keep,
+                                                     const uint32_t *__restrict__ ncontrib,
+                                                     float4 *__restrict__ g2d, const uint32_t *__restrict__ order) {
+    pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
+    pdl_trigger();
+    __shared__ __align__(128) RasterSmem S;
+    __shared__ uint8_t wl[4][4][BATCH];
+    __shared__ uint8_t wl8[4][BATCH];
+    __shared__ uint32_t s_maxlast;
+    int view = blockIdx.z, ty = blockIdx.y, tx = blockIdx.x;
+    if (order) {
+        const uint32_t gt = order[((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x];
+        view = gt / tiles;
+        ty = (gt % tiles) / TX;
+        tx = (gt % tiles) % TX;
+    }
+    const int tile = ty * TX + tx;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane >> 3, gl = lane & 7;
+    const int qx = (warp & 1) * 8 + (q & 1) * 4, qy = (warp >> 1) * 8 + (q >> 1) * 4;  // quadrant origin
+    const int px = tx * TILE + qx + (gl & 3);
+    const int pyA = ty * TILE + qy + (gl >> 2), pyB = pyA + 2;
+    const bool inA = px < W && pyA < H, inB = px < W && pyB < H;
+    const uint2 range = ranges[(int64_t)view * tiles + tile];
+    const float fx = (float)px;
+    const float2 fy2 = make_float2((float)pyA, (float)pyB);
+    float *g2dv = reinterpret_cast<float *>(g2d + 3 * (int64_t)view * n);
+    const int64_t HW = (int64_t)H * W;
+    const int64_t pixA = (int64_t)pyA * W + px, pixB = (int64_t)pyB * W + px;
+    Pix2 P;
+    P.T = f2(1.f);
+    P.g0 = P.g1 = P.g2 = f2(0.f);
+    P.lastA = P.lastB = 0;
+    const float *gbase = dL_drgb + (int64_t)view * 3 * HW;
+    if (inA) {
+        P.T.x = T_keep[(int64_t)view * HW + pixA];
+        P.lastA = ncontrib[(int64_t)view * HW + pixA];
+        P.g0.x = gbase[pixA];
+        P.g1.x = gbase[HW + pixA];
+        P.g2.x = gbase[2 * HW + pixA];
+    }
+    if (inB) {
+        P.T.y = T_keep[(int64_t)view * HW + pixB];
+        P.lastB = ncontrib[(int64_t)view * HW + pixB];
+        P.g0.y = gbase[pixB];
+        P.g1.y = gbase[HW + pixB];
+        P.g2.y = gbase[2 * HW + pixB];
+    }
+    init_sentinel(S, tid);
+    if (tid == 0) {
+        s_maxlast = 0;
+        mbar_init(&S.bar[0]);
+        mbar_init(&S.bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t glast = max(P.lastA, P.lastB);  // the group's last composited position
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) glast = max(glast, __shfl_xor_sync(0xffffffffu, glast, o));
+    uint32_t wlast = glast;
+#pragma unroll
+    for (int o = 16; o > 4; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
+    if (lane == 0) atomicMax(&s_maxlast, wlast);
+    __syncthreads();
+    const int todo_all = (int)s_maxlast;
+    const float4 *src = prec + 3 * (size_t)range.x;
+    if (tid == 0 && todo_all > 0) {
+        int cnt0 = min(BATCH, todo_all);
+        bulk_load(S.rec[0], src + 3 * (size_t)(todo_all - cnt0), (uint32_t)cnt0 * 48u, &S.bar[0]);
+    }
+    uint32_t phases = 0u;
+    P.acc0 = f2(bg0);
+    P.acc1 = f2(bg1);
+    P.acc2 = f2(bg2);
+    const unsigned lt = (1u << gl) - 1u;
+    const float fqx = (float)(tx * TILE + qx), fqy = (float)(ty * TILE + qy);
+    for (int b_end = todo_all, it = 0; b_end > 0; b_end -= BATCH, it++) {
+        const int buf = it & 1;
+        const int cnt = min(BATCH, b_end);
+        const int b_start = b_end - cnt;
+        __syncthreads();
+        if (tid == 0 && b_start > 0) {
+            int cn = min(BATCH, b_start);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_load(S.rec[buf ^ 1], src + 3 * (size_t)(b_start - cn), (uint32_t)cn * 48u, &S.bar[buf ^ 1]);
+        }
+        mbar_wait(&S.bar[buf], (phases >> buf) & 1u);
+        phases ^= 1u << buf;
+        const float4 *r = S.rec[buf];
+        int nsel = 0;
+        if ((uint32_t)b_start < wlast) {
+            int n8 = 0;
+            {
+                const float wx0 = (float)(tx * TILE + (warp & 1) * 8), wy0 = (float)(ty * TILE + (warp >> 1) * 8);
+                const unsigned lt32 = (1u << lane) - 1u;
+                for (int k = 0; k < cnt; k += 32) {
+                    const int jj = k + lane;
+                    const int idx = cnt - 1 - jj;
+                    const bool hit = jj < cnt && (uint32_t)(b_start + idx + 1) <= wlast &&
+                                     !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, wx0, wy0, 7.f, 7.f);
+                    const unsigned b = __ballot_sync(0xffffffffu, hit);
+                    if (hit) wl8[warp][n8 + __popc(b & lt32)] = (uint8_t)idx;
+                    n8 += __popc(b);
+                }
+                __syncwarp();
+            }
+            for (int k = 0; k < n8; k += 8) {
+                const int e = k + gl;
+                const int idx = e < n8 ? wl8[warp][e] : 0;
+                const bool hit = e < n8 && (uint32_t)(b_start + idx + 1) <= glast &&
+                                 !block_misses(r[3 * idx], r[3 * idx + 1], r[3 * idx + 2].w, fqx, fqy, 3.f, 3.f);
+                const unsigned gb = (__ballot_sync(0xffffffffu, hit) >> (lane & 24)) & 0xffu;
+                if (hit) wl[warp][q][nsel + __popc(gb & lt)] = (uint8_t)idx;
+                nsel += __popc(gb);
+            }
+        }
+        __syncwarp();
+        int nmax = nsel;
+#pragma unroll
+        for (int o = 16; o > 4; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+        for (int t = 0; t < nmax; t++) {
+            const int j = t < nsel ? wl[warp][q][t] : BATCH;
+            bwdq_entry<FEW_TILEQ>(P, r, j, (uint32_t)(b_start + j + 1), fx, fy2, lane, g2dv);
+        }
     }
 }
 
@@ -1021,7 +1080,7 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
 cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], const float *dL_drgb, cudaStream_t s) {
     ProfScope prof("k_raster_bwd", s);
     if (L.max_chunks > 0) {  // chunked path (few tiles): every chunk replayed independently
-        launch_pdl(k_raster_bwd2_chunk, (unsigned)L.max_chunks, 128, 0, s, 
+        launch_pdl(k_raster_bwdq_chunk, (unsigned)L.max_chunks, 128, 0, s, 
             at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), at<uint32_t>(ws, L.chunk_base),
             at<uint32_t>(ws, L.chunk_tile), at<WsHeader>(ws, L.hdr), L.n, L.W, L.H, L.TX, L.tiles, dL_drgb,
             at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.chunk_bwd), at<float4>(ws, L.grad2d),
@@ -1030,7 +1089,7 @@ cudaError_t launch_raster_bwd(const Layout &L, void *ws, const float bg[3], cons
     }
     // many tiles: two pixels per lane, packed fp32x2
     dim3 grid(L.TX, L.TY, L.V);
-    launch_pdl(k_raster_bwd2, grid, 128, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
+    launch_pdl(k_raster_bwdq, grid, 128, 0, s, at<uint2>(ws, L.ranges), at<float4>(ws, L.prec), L.n, L.W, L.H, L.TX,
                                        L.tiles, bg[0], bg[1], bg[2], dL_drgb, at<float>(ws, L.Tfinal),
                                        at<uint32_t>(ws, L.ncontrib), at<float4>(ws, L.grad2d), at<uint32_t>(ws, L.tile_order));
     return cudaGetLastError();
