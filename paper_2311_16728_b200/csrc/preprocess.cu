@@ -13,6 +13,7 @@
 // (R22) and added to the caller's gradient buffer.
 #include "gs_internal.cuh"
 
+
 namespace gsk {
 
 #define FMA __fmaf_rn
@@ -414,6 +415,9 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
     for (int k = 0; k < 9; k++) gR[k] = 0.f;
     float norm_acc = 0.f;
     const float S3[9] = {cv.S00, cv.S01, cv.S02, cv.S01, cv.S11, cv.S12, cv.S02, cv.S12, cv.S22};
+    float GS3a[9];  // dL/dSigma3 summed over the views
+#pragma unroll
+    for (int k = 0; k < 9; k++) GS3a[k] = 0.f;
     // ---- geometry: conic -> Sigma2 -> (Sigma3, J) -> (q, s), mean2d -> P
     for (int v = 0; v < V; v++) {
         int64_t m = (int64_t)v * n + i;
@@ -486,6 +490,13 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(const float *__restrict_
         // p_c = W P + t
 #pragma unroll
         for (int k = 0; k < 3; k++) gP[k] += W[k] * gpc0 + W[3 + k] * gpc1 + W[6 + k] * gpc2;
+        // dL/dSigma3 is of the world-frame covariance: summed over the views, then taken
+        // through Sigma3 = M M^T once after the loop (linear in it)
+#pragma unroll
+        for (int k = 0; k < 9; k++) GS3a[k] += GS3[k];
+    }
+    {
+        const float *GS3 = GS3a;
         // Sigma3 = M M^T: dL/dM = 2 GS3 M ; M = Rq diag(e)
 #pragma unroll
         for (int r = 0; r < 3; r++)
