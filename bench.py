@@ -237,8 +237,9 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 def use_chunked(view_tiles: int, cap: int) -> bool:
-    """Mirror of gs_internal.cuh use_chunked: the chunk-parallel raster path."""
-    return view_tiles < 1000
+    """Mirror of gs_internal.cuh use_chunked: the chunk-parallel raster path (few lists, or up to
+    8192 lists with a pair capacity of >= 1024 per list)."""
+    return view_tiles < 1000 or (view_tiles <= 8192 and cap >= 1024 * view_tiles)
 FUSED_SCHEDULE_TILES = 8192  # views x tiles up to this: one-CTA tile scan + schedule (raster.cu)
 
 

@@ -48,18 +48,26 @@ struct WsHeader {
     uint32_t nchunks;      // list chunks of the chunked raster path (raster.cu)
 };
 
-// Chunk-parallel raster backward for levels with few tiles: every 256-entry chunk of a tile
-// list is replayed by its own CTAs from state the forward recorded (raster.cu).
-constexpr int CHUNK = 64;              // list entries per chunk of the chunked raster path
+// Chunk-parallel raster backward for levels with few tiles or long lists: every CHUNK-entry
+// chunk of a tile list is replayed by its own CTA from state the forward recorded (raster.cu).
+constexpr int CHUNK = 128;             // list entries per chunk of the chunked raster path
 constexpr int TILE_PIX = 256;          // pixels per 16x16 tile (per-chunk record stride)
-// Chunk-parallel raster (raster.cu) below CHUNK_MAX_TILES (view, tile) lists: the coarse GP
-// levels, where few tiles with long lists would leave the tile-serial kernels with a long tail.
+// Chunk-parallel raster (raster.cu) below CHUNK_MAX_TILES (view, tile) lists -- the coarse GP
+// levels, where few tiles with long lists would leave the tile-serial kernels with a long tail --
+// and, up to CHUNK_LONG_MAX_TILES lists (the one-CTA tile scan builds the chunk tables), for
+// levels whose pair capacity allows CHUNK_LONG_MEAN pairs per list (the multi-view coarse levels).
 // Measured (graph replay, round 2): 600 -> 1000 takes Replica level 1 (836 lists) onto it,
-// 1.787 -> 1.728 ms per step; chunking larger levels (Replica level 0, EuRoC's 16-view levels)
-// is slower (1.837 vs 1.764 ms, 7.90 vs 7.25 ms): there the tile kernels fill the GPU and the
-// chunk records cost more than the tail.
+// 1.787 -> 1.728 ms per step; chunking Replica level 0 (3225 lists, 212 pairs on average) is
+// slower (1.837 vs 1.764 ms): there the tile kernels fill the GPU and the chunk records cost more
+// than the tail.  With the quadrant-group backward, 128-entry chunks (64 before) and the
+// long-list rule (EuRoC level 2: 1536 lists of 1813 pairs on average): Replica 1.617 -> 1.588 ms,
+// EuRoC 6.65 -> 6.33 ms; 512 pairs per list (EuRoC level 1 too) 6.46 ms, 2048 as 1024.
 constexpr int CHUNK_MAX_TILES = 1000;
-__host__ __device__ inline bool use_chunked(int64_t view_tiles, int64_t /*cap*/) { return view_tiles < CHUNK_MAX_TILES; }
+constexpr int64_t CHUNK_LONG_MAX_TILES = 8192;
+constexpr int64_t CHUNK_LONG_MEAN = 1024;
+__host__ __device__ inline bool use_chunked(int64_t view_tiles, int64_t cap) {
+    return view_tiles < CHUNK_MAX_TILES || (view_tiles <= CHUNK_LONG_MAX_TILES && cap >= CHUNK_LONG_MEAN * view_tiles);
+}
 
 // Byte offsets of every buffer inside a render workspace (pure function of n, V, W, H, cap).
 struct Layout {
