@@ -13,8 +13,8 @@
 // is in flight while batch b is composited, and no thread waits on dependent gathers.
 //
 // Layout: one thread per pixel; each warp owns an 8x4 pixel block (2 x 4 blocks per 16x16
-// tile); a CTA holds 8 warps (a whole tile) or, at pyramid levels with fewer tiles than
-// 4 x SMs, 2 or 1 warps (several CTAs per tile) so that every SM gets work.  For every batch
+// tile); a CTA holds 8 warps (a whole tile) or, at pyramid levels with fewer lists than
+// 2 x SMs, one warp (eight CTAs per tile) so that every SM gets work.  For every batch
 // of 256 records each warp builds, in parallel over the batch (one record per lane, ballot +
 // popc), the ordered list of Gaussians that can reach its block: the exact minimum of d^T Q d
 // over the block is compared with the Gaussian's limit min(9, 2 ln(255 sigma)) (3-sigma
@@ -1006,8 +1006,9 @@ cudaError_t launch_tile_scan(const Layout &L, void *ws, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, fewer (several CTAs per
-// tile) at pyramid levels with few tiles so that every SM gets work.
+// Warps per CTA: 8 (one CTA per tile) when the grid fills the GPU, else one (eight CTAs per
+// tile) at pyramid levels with few tiles so that every SM gets work.  Measured (round 2):
+// one-warp instead of two-warp CTAs for 148..295 lists (Replica level 2), 1.587 -> 1.582 ms.
 static int raster_warps(const Layout &L) {
     static int sms = 0;
     if (sms == 0) {
@@ -1017,9 +1018,7 @@ static int raster_warps(const Layout &L) {
         if (sms <= 0) sms = 148;
     }
     const int64_t t = (int64_t)L.V * L.tiles;
-    if (t >= 2 * sms) return 8;
-    if (t >= sms) return 2;
-    return 1;
+    return t >= 2 * sms ? 8 : 1;
 }
 
 cudaError_t launch_gather_pairs(const Layout &L, void *ws, cudaStream_t s) {
@@ -1071,7 +1070,6 @@ cudaError_t launch_raster_fwd(const Layout &L, void *ws, const float bg[3], floa
     }
     switch (raster_warps(L)) {
         case 8: fwd_launch<8>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
-        case 2: fwd_launch<2>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
         default: fwd_launch<1>(L, ws, bg, out_rgb, out_T, cbase, cbwd, order, s); break;
     }
     return cudaGetLastError();
