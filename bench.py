@@ -316,7 +316,7 @@ def run_ours(args):
         return 0
 
     if args.quick:  # A/B runs: the headline graph replay only
-        use_graph = world == 1 and not args.no_graph
+        use_graph = (world == 1 or eng.peer is not None or eng.sharded is not None) and not args.no_graph
         if use_graph:
             eng.capture()
             for _ in range(3):
@@ -421,10 +421,10 @@ def run_ours(args):
     eager_ms = statistics.median(v[2] for v in live.values())
     shares = {k: v[0] / v[2] for k, v in live.items()}
 
-    # ---- headline: K timed steps (one CUDA-graph replay per step on a single GPU; eager
-    # launches under torchrun, where the NCCL all-reduce sits inside the iteration)
-    # one GPU, or the peer-memory DP step (no NCCL call inside a step): CUDA-graph replay
-    use_graph = (world == 1 or eng.peer is not None) and not args.no_graph
+    # ---- headline: K timed steps, one CUDA-graph replay per step: one GPU, the peer-memory DP
+    # step, or the row-sharded NCCL DP step (its reduce-scatter / all-gather captured with it);
+    # eager launches only for the replicated all-reduce path
+    use_graph = (world == 1 or eng.peer is not None or eng.sharded is not None) and not args.no_graph
     if use_graph:
         eng.capture()
         for _ in range(2):
@@ -639,6 +639,10 @@ def run_ours(args):
         t = r.ws.tiles_x * r.ws.tiles_y * len(cams)
         bits = 32 + max(1, math.ceil(math.log2(max(t, 2))))
         launches_step += launches_per_iteration(bits, world == 1, chunked=use_chunked(t, r.ws.capacity), view_tiles=t)
+        if world > 1 and eng.peer is not None:  # peer barrier + fused reduce/Adam/broadcast + barrier for Adam
+            launches_step += 2
+        elif world > 1 and eng.sharded is not None and use_graph:  # device step counter of the row Adam
+            launches_step += 1
     launches = args.steps * launches_step
 
     # ---- sorted keys/s (A4): the level-0 pairs of this step (keys (tile << 32 | depth bits),

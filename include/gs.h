@@ -241,6 +241,15 @@ gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, floa
                             int64_t step, int32_t row_begin, int32_t row_end, int32_t zero_grads,
                             gs_stream_t stream);
 
+/* gs_adam_step_rows with the step counter on the device, for a data-parallel step captured in a
+   CUDA graph (the counter advances on every replay): step_dev (device, int64) holds the number
+   of steps taken; the call takes step *step_dev + 1 (bias corrections from it) and leaves
+   *step_dev incremented (stream-ordered: a one-thread kernel, then the step).  Otherwise as
+   gs_adam_step_rows.  GS_ERR_INVALID_ARG for a NULL step_dev. */
+gs_status gs_adam_step_rows_dev(gs_params *params, float *grads, float *m_rows, float *v_rows,
+                                const gs_adam_hparams *hp, int64_t *step_dev, int32_t row_begin, int32_t row_end,
+                                int32_t zero_grads, gs_stream_t stream);
+
 /* Synchronises stream, then reads the workspace status: *flags (host) bit 0 = pair capacity
    overflow; *pairs (host, may be NULL) = pair count of the last gs_preprocess.  Returns
    GS_ERR_CAPACITY if bit 0 is set. */

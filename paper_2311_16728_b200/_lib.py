@@ -26,7 +26,7 @@ GS_TILE = 16
 # every symbol declared in include/gs.h
 EXPORTS = ["gs_param_rows", "gs_param_ld", "gs_workspace_size", "gs_preprocess", "gs_render_forward",
            "gs_loss_workspace_size", "gs_photometric_loss", "gs_render_backward", "gs_render_backward_adam",
-           "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_densify_temp_size", "gs_densify_stats",
+           "gs_pyramid", "gs_adam_step", "gs_adam_step_rows", "gs_adam_step_rows_dev", "gs_densify_temp_size", "gs_densify_stats",
            "gs_densify_plan", "gs_densify_apply", "gs_densify_tags", "gs_geometry_densify",
            "gs_query_status", "gs_status_async", "gs_workspace_release", "gs_status_str",
            "gs_comm_shard", "gs_peer_barrier", "gs_reduce_adam_bcast", "gs_spatial_order_temp_size", "gs_spatial_order",
@@ -233,6 +233,13 @@ def gs_adam_step_rows(params: GsParams, grads, m_rows, v_rows, hp: GsAdamHparams
     _check(lib().gs_adam_step_rows(C.byref(params), _ptr(grads), _ptr(m_rows), _ptr(v_rows), C.byref(hp),
                                    C.c_int64(step), C.c_int32(row_begin), C.c_int32(row_end),
                                    C.c_int32(int(zero_grads)), _stream(stream)), "gs_adam_step_rows")
+
+
+def gs_adam_step_rows_dev(params: GsParams, grads, m_rows, v_rows, hp: GsAdamHparams, step_dev, row_begin: int,
+                          row_end: int, zero_grads: bool, stream=None):
+    _check(lib().gs_adam_step_rows_dev(C.byref(params), _ptr(grads), _ptr(m_rows), _ptr(v_rows), C.byref(hp),
+                                       _ptr(step_dev), C.c_int32(row_begin), C.c_int32(row_end),
+                                       C.c_int32(int(zero_grads)), _stream(stream)), "gs_adam_step_rows_dev")
 
 
 def gs_comm_shard(n: int, sh_degree: int, rank: int, world: int) -> tuple[int, int]:

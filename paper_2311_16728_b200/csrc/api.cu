@@ -371,6 +371,19 @@ gs_status gs_adam_step_rows(gs_params *params, float *grads, float *m_rows, floa
                                    (cudaStream_t)stream, row_begin, row_end));
 }
 
+gs_status gs_adam_step_rows_dev(gs_params *params, float *grads, float *m_rows, float *v_rows,
+                                const gs_adam_hparams *hp, int64_t *step_dev, int32_t row_begin, int32_t row_end,
+                                int32_t zero_grads, gs_stream_t stream) {
+    gs_status st = check_params(params);
+    if (st) return st;
+    const int32_t K = gs_param_rows(params->sh_degree);
+    if (!grads || !hp || !step_dev || row_begin < 0 || row_end > K || row_begin > row_end) return GS_ERR_INVALID_ARG;
+    if (!hp->sgd_mode && (!m_rows || !v_rows)) return GS_ERR_INVALID_ARG;
+    if (row_begin == row_end || params->n == 0) return GS_OK;
+    return cuda_status(launch_adam(*params, grads, m_rows, v_rows, *hp, 1, 0, params->n, zero_grads,
+                                   (cudaStream_t)stream, row_begin, row_end, step_dev));
+}
+
 gs_status gs_densify_temp_size(int64_t n, size_t *bytes) {
     if (!bytes || n < 0) return GS_ERR_INVALID_ARG;
     *bytes = densify_temp_bytes(n);

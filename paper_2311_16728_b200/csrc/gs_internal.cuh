@@ -370,7 +370,8 @@ cudaError_t launch_loss(const float *render, const float *gt, int V, int H, int 
 size_t loss_ws_bytes(int V, int H, int W);
 cudaError_t launch_pyramid(const float *img, int N, int C, int H, int W, int levels, float *out, cudaStream_t s);
 cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
-                        int64_t g0, int64_t g1, int zero, cudaStream_t s, int row_begin = 0, int row_end = -1);
+                        int64_t g0, int64_t g1, int zero, cudaStream_t s, int row_begin = 0, int row_end = -1,
+                        int64_t *step_dev = nullptr);
 cudaError_t launch_exp_scale(const float *s, float *out, int64_t n, cudaStream_t st);
 
 }  // namespace gsk

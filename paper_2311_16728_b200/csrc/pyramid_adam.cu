@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(ADAM_THREADS) k_adam(float *__restrict__ P, fl
                                                        int64_t g0, int64_t g1, int row0, AdamArgs a) {
     pdl_wait();  // PDL: the predecessor grid has completed (gs_internal.cuh)
     pdl_trigger();
+    adam_device_step(a);  // device-step mode only
     const int row = blockIdx.y;
     const float lr = a.lr[row_class(row0 + row)];
     const int64_t per_row = ld / 4;
@@ -235,9 +236,16 @@ cudaError_t launch_adam_fused(const gs_params &p, const Layout &L, void *ws, flo
     return cudaGetLastError();
 }
 
+__global__ void k_step_inc(int64_t *step_dev) { *step_dev += 1; }
+
 cudaError_t launch_adam(const gs_params &p, float *g, float *m, float *v, const gs_adam_hparams &hp, int64_t step,
-                        int64_t g0, int64_t g1, int zero, cudaStream_t s, int row_begin, int row_end) {
-    AdamArgs a = adam_args(hp, step, zero);
+                        int64_t g0, int64_t g1, int zero, cudaStream_t s, int row_begin, int row_end,
+                        int64_t *step_dev) {
+    if (step_dev) {  // device-step mode: take step *step_dev + 1 and count it (graph replay)
+        k_step_inc<<<1, 1, 0, s>>>(step_dev);
+        step = 1;
+    }
+    AdamArgs a = adam_args(hp, step, zero, step_dev);
     if (row_end < 0) row_end = gs_param_rows(p.sh_degree);
     const int rows = row_end - row_begin;
     int64_t per_row = p.ld / 4;

@@ -94,8 +94,21 @@ class ShardedAdam:
         self.n, self.D = n, sh_degree
         self.cfg = cfg or AdamConfig()
         self.hp = self.cfg.struct()
-        self.t = 0
+        self._t = 0
+        self.device_step = False  # True: the step counter lives on the device (CUDA-graph replay)
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=padded_params.device)
         self.rebind(padded_params, padded_grads, n)
+
+    @property
+    def t(self) -> int:
+        return int(self.t_dev.item()) if self.device_step else self._t
+
+    def use_device_step(self):
+        """Count steps on the device (gs_adam_step_rows_dev), so a captured step replays with the
+        right bias corrections; keeps the count."""
+        if not self.device_step:
+            self.t_dev.fill_(self._t)
+        self.device_step = True
 
     def rebind(self, padded_params: torch.Tensor, padded_grads: torch.Tensor, n: int,
                m_full: torch.Tensor | None = None, v_full: torch.Tensor | None = None):
@@ -128,11 +141,15 @@ class ShardedAdam:
     def _adam_rows(self):
         from . import _lib as L
         ps = L.params_struct(self.params, self.n, self.D)
-        L.gs_adam_step_rows(ps, self.grads, self.m, self.v, self.hp, self.t, self.r0, self.r1, False)
+        if self.device_step:
+            L.gs_adam_step_rows_dev(ps, self.grads, self.m, self.v, self.hp, self.t_dev, self.r0, self.r1, False)
+        else:
+            L.gs_adam_step_rows(ps, self.grads, self.m, self.v, self.hp, self._t, self.r0, self.r1, False)
 
     def step(self):
         reduce_scatter_rows(self.padded_grads, self.R, self.group)   # A10
-        self.t += 1
+        if not self.device_step:
+            self._t += 1
         if self.r1 > self.r0:
             self._adam_rows()                                          # A11 on this rank's rows
         all_gather_rows(self.padded_params, self.R, self.group)       # replicas identical again
@@ -447,13 +464,15 @@ class MappingEngine:
     def capture(self, gts_pinned: torch.Tensor | None = None, out_pinned: torch.Tensor | None = None):
         """Capture one step -- A0 + the Eq. 5 pass (and, with pinned host buffers, the H2D copy of
         the targets and the D2H copy of the losses) -- into a CUDA graph; `replay()` then runs it
-        with a single launch.  Single GPU only (the fused backward+Adam with a device-resident
-        step counter; the DP path has an NCCL collective between backward and Adam)."""
-        if (self.distributed() and self.peer is None) or self.sharded is not None:
-            raise RuntimeError("graph capture: the single-GPU fused path or the peer-memory DP step (no NCCL call "
-                               "inside the step)")
+        with a single launch.  The single-GPU fused path, the peer-memory DP step, and the
+        row-sharded NCCL DP step (its reduce-scatter and all-gather are captured with it; the
+        optimiser counts steps on the device).  Not the replicated all-reduce path."""
+        if self.distributed() and self.peer is None and self.sharded is None:
+            raise RuntimeError("graph capture: the single-GPU fused path or a sharded / peer-memory DP step")
         if self.adam is not None:
             self.adam.use_device_step()
+        if self.sharded is not None:
+            self.sharded.use_device_step()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         host = gts_pinned is not None

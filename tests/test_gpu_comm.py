@@ -144,3 +144,59 @@ def test_reduce_adam_bcast_multi_rank_arithmetic(world):
     mflat, vflat = ref.m.reshape(-1), ref.v.reshape(-1)
     for e0, e1, m, v in shards:
         assert torch.equal(m[:e1 - e0], mflat[e0:e1]) and torch.equal(v[:e1 - e0], vflat[e0:e1])
+
+
+@pytest.mark.parametrize("sgd", [False, True])
+def test_adam_step_rows_dev_equals_host_step(pg, sgd):
+    """gs_adam_step_rows_dev (step counter on the device, advanced by the call) takes the same
+    steps, bit for bit, as gs_adam_step_rows with the host's 1-based counter."""
+    scene = make_scene("tum", n=2003)
+    n, D = scene.n, 3
+    cfg = AdamConfig(sgd=sgd, lr_means=1e-2)
+    hp = cfg.struct()
+    p0 = pack_params(scene)
+    K = p0.shape[0]
+    r0, r1 = 4, 41
+    pa, pb = p0.clone(), p0.clone()
+    ma, va = torch.zeros((r1 - r0, p0.shape[1]), device="cuda"), torch.zeros((r1 - r0, p0.shape[1]), device="cuda")
+    mb, vb = ma.clone(), va.clone()
+    t_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+    gen = torch.Generator("cuda").manual_seed(7)
+    for step in range(1, 4):
+        g = torch.randn(p0.shape, device="cuda", generator=gen)
+        L.gs_adam_step_rows(L.params_struct(pa, n, D), g, ma, va, hp, step, r0, r1, False)
+        L.gs_adam_step_rows_dev(L.params_struct(pb, n, D), g, mb, vb, hp, t_dev, r0, r1, False)
+        torch.cuda.synchronize()
+        assert torch.equal(pa, pb) and int(t_dev.item()) == step
+        if not sgd:
+            assert torch.equal(ma, mb) and torch.equal(va, vb)
+    assert torch.equal(pa[:r0], p0[:r0]) and torch.equal(pa[r1:K], p0[r1:K])  # other rows untouched
+
+
+def test_engine_sharded_nccl_step_captures_and_replays(pg):
+    """The row-sharded NCCL DP step (reduce-scatter -> Adam on the rank's rows -> all-gather ->
+    zeroed gradients) captured in a CUDA graph: replays continue the eager trajectory (same
+    losses as an engine stepping eagerly from the same state) and count steps on the device."""
+    def make():
+        scene = make_scene("tiny")
+        cams = make_cameras("tiny", 1)
+        r = Renderer(scene.n, 0, 1, cams[0].width, cams[0].height, 1 << 16)
+        gt = r.forward(pack_params(scene), cams)[0].clone()
+        return MappingEngine(perturb(scene, 4), cams, gt, n_levels=1, comm="nccl", shard_optimizer=True)
+    eng, ref = make(), make()
+    assert eng.sharded is not None
+    for _ in range(2):
+        eng.step()
+        ref.step()
+    eng.capture()  # also runs one (warm-up) step
+    ref.step()
+    assert eng.sharded.t == ref.sharded.t
+    for _ in range(3):
+        eng.replay()
+        lb = [x.item() for x in ref.step()]
+    torch.cuda.synchronize()
+    la = eng.graph_losses.cpu().numpy().reshape(-1)
+    np.testing.assert_allclose(la, np.ravel(lb), rtol=1e-3)
+    assert eng.sharded.t == ref.sharded.t == 2 * 6
+    n = eng.n
+    torch.testing.assert_close(eng.params[:, :n], ref.params[:, :n], rtol=1e-4, atol=1e-5)
