@@ -21,6 +21,7 @@
 
 #include "gs_internal.cuh"
 
+
 namespace gsk {
 
 
@@ -48,6 +49,8 @@ __global__ void __launch_bounds__(BIN_THREADS) k_bin_scatter(const int4 *__restr
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&hdr->flags, 1u);
         return;
     }
+    // the grid covers all n Gaussians; CTAs past the compacted visible list have nothing to bin
+    if (blockIdx.x * blockDim.x >= hdr->vis_count) return;
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = t < hdr->vis_count;
     const uint32_t gi = live ? vis_list[t] : 0u;
