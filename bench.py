@@ -425,8 +425,18 @@ def run_ours(args):
     # step, or the row-sharded NCCL DP step (its reduce-scatter / all-gather captured with it);
     # eager launches only for the replicated all-reduce path
     use_graph = (world == 1 or eng.peer is not None or eng.sharded is not None) and not args.no_graph
+    graph_note = None
     if use_graph:
-        eng.capture()
+        try:
+            eng.capture()
+        except Exception as ex:  # noqa: BLE001  (multi-rank NCCL capture is unmeasured: fall back to eager)
+            if world == 1:
+                raise
+            use_graph, graph_note = False, f"capture failed, eager launches: {type(ex).__name__}: {ex}"[:300]
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+    if use_graph:
         for _ in range(2):
             eng.replay()
         torch.cuda.synchronize()
@@ -731,7 +741,7 @@ def run_ours(args):
             "render_fps_eager": 1000.0 / render_ms_eager * len(cams) * world,
             "render_replica": replica,
             "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
-            "timing": {"headline": "CUDA graph replay per step" if use_graph else "eager launches",
+            "timing": {"headline": "CUDA graph replay per step" if use_graph else (graph_note or "eager launches"),
                        "eager_ms_per_step": eager_ms / args.steps},
         }
         print(json.dumps(line), flush=True)
